@@ -1,0 +1,195 @@
+/*
+ * halo_b200.h — C ABI of libhalo_b200.so, the B200-native (sm_100a) HALO
+ * quantized linear-layer training path.
+ *
+ * The reference (/root/reference/proj/include/halo, header-only C++20) has no
+ * FFI: its operator surface is the HaloLinearLayerT class plus free functions.
+ * Each entry point below replaces one of those interfaces (file:line given
+ * relative to /root/reference/proj/include/halo/).  The C++ class
+ * halo_b200::HaloLinearLayer in halo_b200.hpp restores the reference's
+ * object API on top of this ABI, with the reference's exception types.
+ *
+ * Conventions
+ *  - All tensors are row-major device pointers (cudaMalloc'd or torch
+ *    storage); the caller owns them.  Nothing here allocates host copies.
+ *  - Every call is stream-ordered and asynchronous; no host synchronisation
+ *    happens on the hot path.  Scales live in device memory (float*).
+ *  - had_block: power-of-two Hadamard block B; the transform is I (x) H_B.
+ *    0 means "the full dimension", i.e. the reference's transform verbatim
+ *    (hadamard.hpp:95-129; only power-of-two dimensions are built here).
+ *  - Errors are reported through halo_status; halo_last_error() returns a
+ *    thread-local message.  Non-finite inputs are detected on the device and
+ *    surface as HALO_ERR_NUMERIC from halo_ctx_check().
+ */
+#ifndef HALO_B200_H
+#define HALO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HALO_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HALO_API __attribute__((visibility("default")))
+#else
+#define HALO_API
+#endif
+
+typedef struct CUstream_st* halo_stream_t; /* == cudaStream_t */
+
+/* std::invalid_argument -> 1, numeric_error -> 2, std::logic_error -> 3
+ * (the CLI's exit-code mapping, halo_cli.cpp:730-736, keeps 2/3 distinct). */
+typedef enum halo_status {
+    HALO_OK = 0,
+    HALO_ERR_INVALID_ARGUMENT = 1,
+    HALO_ERR_NUMERIC = 2,
+    HALO_ERR_LOGIC = 3,
+    HALO_ERR_CUDA = 4,
+    HALO_ERR_NCCL = 5
+} halo_status;
+
+/* NumericFormat ids, quantize.hpp:22-29 (FP6/MX/BF16/IDENTITY emulation is
+ * not part of this path and is rejected). */
+typedef enum halo_format { HALO_FMT_INT8 = 0, HALO_FMT_FP8_E4M3 = 1 } halo_format;
+
+typedef enum halo_dtype { HALO_DTYPE_F32 = 0, HALO_DTYPE_BF16 = 1 } halo_dtype;
+
+/* GEMM output kinds */
+typedef enum halo_out_kind { HALO_OUT_F32 = 0, HALO_OUT_BF16 = 1, HALO_OUT_S32 = 2 } halo_out_kind;
+
+/* Placement, halo_linear.hpp:29-61 */
+typedef struct halo_placement {
+    uint8_t left, middle, right, pad_;
+} halo_placement;
+
+/* HaloScheme, halo_linear.hpp:63-79, plus the Hadamard block size. */
+typedef struct halo_scheme {
+    halo_placement F, E, G;
+    int32_t format_x, format_w, format_e; /* halo_format */
+    int32_t granularity;                  /* 0 = tensor (the only device path) */
+    int32_t quantize_f, quantize_e, quantize_g;
+    int32_t peft;
+    int64_t had_block; /* 0 = full dimension (reference) */
+    char name[16];     /* preset id or "" */
+} halo_scheme;
+
+/* QuantCallCounters, halo_linear.hpp:161-164 */
+typedef struct halo_counters {
+    int64_t x, w, e;
+} halo_counters;
+
+HALO_API int halo_abi_version(void);
+HALO_API const char* halo_last_error(void);
+
+/* hadamard.hpp:69-85 / :87-93 */
+HALO_API int halo_is_supported_hadamard_dim(int64_t d);
+HALO_API int64_t halo_next_supported_hadamard_dim(int64_t d);
+
+/* halo0/halo1/halo2 presets and "F:..;E:..;G:.." strings,
+ * halo_linear.hpp:81-152 (scheme_from_string). */
+HALO_API halo_status halo_scheme_from_string(const char* id, int32_t format, int64_t had_block, halo_scheme* out);
+
+/* ------------------------------------------------------------ primitives */
+
+/* quantize(transform_right(A, spec), fmt, Granularity::tensor(), scales)
+ * hadamard.hpp:194-197 + quantize.hpp:244-280, fused (K1).
+ *   had_block < 0 : no rotation (plain quantize)
+ *   supplied_scale: NULL -> absmax scale (written to scale_out);
+ *                   else used verbatim (quantize.hpp:259-266; FSDP regather).
+ * codes: rows x cols bytes (int8 or OCP e4m3). */
+HALO_API halo_status halo_rotate_quantize(const void* a, int32_t a_dtype, int64_t rows, int64_t cols, int64_t had_block,
+                                 int32_t format, const float* supplied_scale, uint8_t* codes, float* scale_out,
+                                 halo_stream_t stream);
+
+/* max |A H| over the tensor (hqfsdp.hpp:216-225, the per-rank local absmax),
+ * written as a float to absmax_out (device). */
+HALO_API halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols, int64_t had_block,
+                               float* absmax_out, halo_stream_t stream);
+
+/* HALO-2 error operand in one pass (K2): with b_pad = padded batch
+ * (halo_linear.hpp:393-397; a multiple of had_block, or the next supported
+ * dimension when had_block == 0):
+ *   codes_rot   (b_pad x n) = quantize(transform_left_h(pad_rows(E, b_pad)))
+ *   codes_plain (b x n)     = quantize(E)             (may be NULL)
+ * and their scales. */
+HALO_API halo_status halo_left_rotate_quantize(const void* e, int32_t e_dtype, int64_t b, int64_t n, int64_t had_block,
+                                      int32_t format, uint8_t* codes_rot, float* scale_rot, uint8_t* codes_plain,
+                                      float* scale_plain, halo_stream_t stream);
+HALO_API int64_t halo_padded_batch(int64_t b, int64_t had_block);
+
+/* transform_right / transform_right_ht on fp32 (identical for powers of
+ * two), hadamard.hpp:194-203: out (rows x cols, f32 or bf16). */
+HALO_API halo_status halo_transform_right(const float* in, void* out, int32_t out_dtype, int64_t rows, int64_t cols,
+                                 int64_t had_block, halo_stream_t stream);
+
+/* transform_left on fp32 rows [0, rows_pad) (hadamard.hpp:208-210) followed
+ * by take_rows(rows_out) (tensor.hpp:232-240).  in may alias out. */
+HALO_API halo_status halo_transform_left(const float* in, float* out, int64_t rows_pad, int64_t rows_out, int64_t cols,
+                                int64_t had_block, halo_stream_t stream);
+
+/* qmatmul, quantize.hpp:339-380 (K3, tcgen05):
+ *   C[M x N] = A[M x K] * B^T,  A: a_kmajor ? [M][K] : [K][M]
+ *                               B: b_kmajor ? [N][K] : [K][N]
+ * INT8: C = float(double(acc_s32) * (double(sa) * double(sb))) — bit-exact;
+ * HALO_OUT_S32 returns the raw accumulators.  FP8 E4M3: fp32 accumulate. */
+HALO_API halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_kmajor, const uint8_t* b, int32_t b_kmajor,
+                         int64_t M, int64_t N, int64_t K, const float* scale_a, const float* scale_b, void* out,
+                         int32_t out_kind, halo_stream_t stream);
+
+/* ----------------------------------------------------------------- layer */
+
+typedef struct halo_linear halo_linear; /* HaloLinearLayerT, halo_linear.hpp:227 */
+typedef struct halo_ctx halo_ctx;       /* SavedContextT,    halo_linear.hpp:207 */
+
+/* HaloLinearLayerT(W, scheme), halo_linear.hpp:230-234: W is out x in
+ * (n x m), device, caller-owned, read at every forward. */
+HALO_API halo_status halo_linear_create(const halo_scheme* scheme, const void* w, int32_t w_dtype, int64_t out_features,
+                               int64_t in_features, halo_linear** out);
+HALO_API halo_status halo_linear_destroy(halo_linear* layer);
+/* point the layer at new weights (e.g. after an optimizer step) */
+HALO_API halo_status halo_linear_set_weight(halo_linear* layer, const void* w, int32_t w_dtype);
+/* use an already rotated+quantized weight, e.g. the HQ-FSDP gathered
+ * (WH)_Q (hqfsdp.hpp:204-237) or a frozen PEFT weight (halo_linear.hpp:248):
+ * forward skips the weight quantization.  codes == NULL reverts. */
+HALO_API halo_status halo_linear_set_qweight(halo_linear* layer, const uint8_t* codes, const float* scale);
+
+HALO_API halo_status halo_ctx_create(halo_ctx** out);
+HALO_API halo_status halo_ctx_destroy(halo_ctx* ctx);
+
+/* forward, halo_linear.hpp:267-303: y (b x n) in y_dtype. */
+HALO_API halo_status halo_linear_forward(halo_linear* layer, const void* x, int32_t x_dtype, int64_t b, void* y,
+                                int32_t y_dtype, halo_ctx* ctx, halo_stream_t stream);
+
+/* backward, halo_linear.hpp:305-439: e_y (b x n) -> e_x (b x m), grad_w
+ * (n x m; may be NULL to skip G). */
+HALO_API halo_status halo_linear_backward(halo_linear* layer, const halo_ctx* ctx, const void* e_y, int32_t e_dtype,
+                                 void* e_x, int32_t ex_dtype, void* grad_w, int32_t gw_dtype, halo_stream_t stream);
+
+/* export_inference_weights, halo_linear.hpp:332-338: (WH)_Q codes + scale */
+HALO_API halo_status halo_linear_export_inference_weights(halo_linear* layer, uint8_t* codes, float* scale,
+                                                 halo_stream_t stream);
+
+HALO_API halo_status halo_linear_counters(const halo_linear* layer, halo_counters* out);
+HALO_API halo_status halo_linear_reset_counters(halo_linear* layer);
+
+/* saved context views (device pointers owned by ctx) */
+HALO_API halo_status halo_ctx_saved(const halo_ctx* ctx, const uint8_t** xq, const float** sx, const uint8_t** wq,
+                           const float** sw, int64_t* batch_rows);
+/* backward scratch views of the last backward: E quantizations and scales */
+HALO_API halo_status halo_ctx_error_operands(const halo_ctx* ctx, const uint8_t** ehq, const float** seh,
+                                    const uint8_t** eq, const float** se, int64_t* b_pad);
+/* synchronises `stream` and reports device-side numeric errors (NaN/Inf in
+ * an input: tensor.hpp:86-91, quantize.hpp:292/373) as HALO_ERR_NUMERIC,
+ * then clears the flag. */
+HALO_API halo_status halo_ctx_check(halo_ctx* ctx, halo_stream_t stream);
+
+/* stream-ordered device-to-device copy (used to snapshot ctx views) */
+HALO_API halo_status halo_device_copy(void* dst, const void* src, int64_t bytes, halo_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALO_B200_H */

@@ -1,0 +1,398 @@
+// gemm_sm100.cu — K3: tcgen05 / TMEM / TMA quantized GEMM for the three HALO
+// matmuls (Y = X W^T, dX = E W, dW = E^T X), sm_100a.
+//
+// Reference: qmatmul, quantize.hpp:339-380.  The INT8 per-tensor path
+// accumulates exactly in integers and rescales once:
+//     c = float(double(acc) * (double(sa) * double(sb)))        (:356-370)
+// tcgen05.mma kind::i8 accumulates s32 in TMEM — exact, since
+// |acc| <= K * 127^2 < 2^31 for K <= 133,144 — and the epilogue performs the
+// same two roundings in fp64, so outputs are bit-identical to the reference.
+// E4M3 runs kind::f8f6f4 with an fp32 accumulator (tolerance parity: the
+// reference dequantizes and accumulates in double, :377-379).
+//
+// Operand layouts (no transposed copies are ever materialised):
+//   F  Y  = Xq  Wq^T : A K-major [b][m],  B K-major [n][m]
+//   E  dX = Ehq Wq   : A K-major [bp][n], B MN-major [n][m]
+//   G  dW = Eq^T Xq  : A MN-major [b][n], B MN-major [b][m]   (K = tokens)
+// 8-bit MN-major operands are legal for tcgen05 (instruction descriptor bits
+// 15/16), so the reference's transpose_quantized (quantize.hpp:297-334)
+// disappears into the TMA box orientation + UMMA descriptor.
+//
+// Structure (one CTA per SM, persistent, warp-specialised, 256 threads):
+//   warp 0      TMA producer: 4-stage ring of {A 128x128 B, B 256x128 B}
+//               tiles, 128 B swizzle, mbarrier complete_tx
+//   warp 1      MMA issuer: one thread issues 4 x tcgen05.mma (K = 32 B each)
+//               per stage into a 128 x 256 s32 TMEM accumulator; commits
+//               free smem stages and publish finished accumulators
+//   warp 2      TMEM allocator (512 columns = 2 accumulator buffers)
+//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 32 columns, fp64 rescale,
+//               fp32 / bf16 / raw-s32 stores; overlaps the next tile's MMAs
+//               through the double-buffered accumulator.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "halo_internal.h"
+
+namespace halo_b200 {
+
+constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK;  // 32 KB
+constexpr int GEMM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int GROUP_M = 16;  // tile raster: 16 M-tiles share each B panel in L2
+constexpr size_t GEMM_SMEM = 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256;
+
+struct GemmArgs {
+    int M, N, K;
+    int a_kmajor, b_kmajor;
+    int fmt;        // 0 int8, 1 e4m3
+    int out_kind;   // 0 fp32, 1 bf16, 2 raw s32
+    const float* sa;
+    const float* sb;
+    void* out;
+};
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+template <int FMT>
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    if constexpr (FMT == FMT_INT8) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
+//   K-major : SBO = 1024 B (8 rows x 128 B), LBO unused
+//   MN-major: LBO = stride between 128-element MN chunks, SBO = 1024 B
+//             (8 k-rows x 128 B)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor (kind::i8 / kind::f8f6f4, dense)
+__host__ __device__ constexpr uint32_t make_idesc(int fmt, int a_mn, int b_mn, int M, int N) {
+    return (uint32_t)((fmt == FMT_INT8 ? 2u : 1u) << 4)         // D format: s32 / f32
+           | (uint32_t)((fmt == FMT_INT8 ? 1u : 0u) << 7)       // A: signed int8 / e4m3
+           | (uint32_t)((fmt == FMT_INT8 ? 1u : 0u) << 10)      // B
+           | (uint32_t)(a_mn ? 1u : 0u) << 15 | (uint32_t)(b_mn ? 1u : 0u) << 16 |
+           (uint32_t)(N >> 3) << 17 | (uint32_t)(M >> 4) << 24;
+}
+
+__device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int& nb) {
+    const int per_group = GROUP_M * nt;
+    const int g = t / per_group;
+    const int first = g * GROUP_M;
+    const int gsize = min(GROUP_M, mt - first);
+    const int r = t - g * per_group;
+    mb = first + r % gsize;
+    nb = r / gsize;
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = bars + 2 * STAGES + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = (p.M + BM - 1) / BM, nt = (p.N + BN - 1) / BN;
+    const int ntiles = mt * nt;
+    const int nkb = (p.K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ============================ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mb, nb;
+                tile_coords(t, mt, nt, mb, nb);
+                const int m0 = mb * BM, n0 = nb * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    const int k0 = kb * BK;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+                    uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+                    uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
+                    if (p.a_kmajor) tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+                    else tma_load_2d(a_dst, &tmA, &full[stage], m0, k0);
+                    if (p.b_kmajor) {
+                        tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+                    } else {
+                        tma_load_2d(b_dst, &tmB, &full[stage], n0, k0);
+                        tma_load_2d(b_dst + B_STAGE_BYTES / 2, &tmB, &full[stage], n0 + 128, k0);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(FMT, !p.a_kmajor, !p.b_kmajor, BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * A_STAGE_BYTES);
+                    const uint32_t b_addr = smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 32; ++k) {
+                        // K-major: +32 B along the swizzled row; MN-major: +32 k-rows = 4 KB
+                        const uint64_t ad = p.a_kmajor ? make_desc(a_addr + k * 32, 16, 1024)
+                                                       : make_desc(a_addr + k * 4096, A_STAGE_BYTES, 1024);
+                        const uint64_t bd = p.b_kmajor ? make_desc(b_addr + k * 32, 16, 1024)
+                                                       : make_desc(b_addr + k * 4096, B_STAGE_BYTES / 2, 1024);
+                        tc_mma<FMT>(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                    }
+                    tc_commit(&empty[stage]);  // smem stage free once these MMAs retire
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tfull[acc]);  // accumulator complete
+            }
+        }
+    } else if (warp >= 4) {
+        // ============================ epilogue
+        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+        const double ss = (double)(*p.sa) * (double)(*p.sb);
+        const float ssf = (float)ss;
+        int local = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            int mb, nb;
+            tile_coords(t, mt, nt, mb, nb);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = mb * BM + ew * 32 + lane;
+            const bool row_ok = row < p.M;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
+                const int col0 = nb * BN + c * 32;
+                if (!row_ok || col0 >= p.N) continue;
+                const bool full_chunk = (col0 + 32 <= p.N) && (p.N % 8 == 0);  // 16 B aligned rows
+                if (p.out_kind == 2) {
+                    int32_t* o = static_cast<int32_t*>(p.out) + (int64_t)row * p.N + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<int4*>(o + j) = make_int4(r[j], r[j + 1], r[j + 2], r[j + 3]);
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < p.N; ++j) o[j] = (int32_t)r[j];
+                    }
+                    continue;
+                }
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if constexpr (FMT == FMT_INT8) v[j] = (float)((double)(int32_t)r[j] * ss);
+                    else v[j] = __uint_as_float(r[j]) * ssf;
+                }
+                if (p.out_kind == 0) {
+                    float* o = static_cast<float*>(p.out) + (int64_t)row * p.N + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < p.N; ++j) o[j] = v[j];
+                    }
+                } else {
+                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.N + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) store8(o + j, v + j);
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < p.N; ++j) o[j] = __float2bfloat16_rn(v[j]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+// ------------------------------------------------------------------- host
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// 2-D uint8 tensor map: inner dim `inner` (contiguous), outer dim `outer`,
+// box {128, box_outer}, 128 B swizzle, zero OOB fill.
+static bool encode_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {inner};
+    const cuuint32_t box[2] = {128, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+             int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st) {
+    if (M <= 0 || N <= 0 || K <= 0) return -1;
+    if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2) return -1;
+    // TMA: global strides must be multiples of 16 bytes
+    if ((a_kmajor ? K : M) % 16 != 0 || (b_kmajor ? K : N) % 16 != 0) return -1;
+    if (out_kind == 2 && fmt != FMT_INT8) return -1;
+    CUtensorMap ma, mb;
+    const bool ok_a = a_kmajor ? encode_map(&ma, A, K, M, BM) : encode_map(&ma, A, M, K, BK);
+    const bool ok_b = b_kmajor ? encode_map(&mb, B, K, N, BN) : encode_map(&mb, B, N, K, BK);
+    if (!ok_a || !ok_b) return -2;
+    GemmArgs args{(int)M, (int)N, (int)K, a_kmajor, b_kmajor, fmt, out_kind, sa, sb, out};
+    const int tiles = (int)(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    if (fmt == FMT_INT8) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_gemm<FMT_INT8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+            attr = true;
+        }
+        k_gemm<FMT_INT8><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ma, mb, args);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_gemm<FMT_E4M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+            attr = true;
+        }
+        k_gemm<FMT_E4M3><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ma, mb, args);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : (int)e;
+}
+
+}  // namespace halo_b200

@@ -1,0 +1,643 @@
+// halo_capi.cu — host layer: the C ABI of include/halo_b200.h and the HALO
+// linear operator (HaloLinearLayerT, halo_linear.hpp:227-462) composed from
+// the K1/K2/K3/K4 kernels.  Everything is stream-ordered; scales and absmax
+// words live in a per-context device block, so a forward/backward pair never
+// synchronises with the host.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/halo_b200.h"
+#include "common.cuh"
+#include "halo_internal.h"
+
+using namespace halo_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+halo_status fail(halo_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+halo_status cuda_check(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(HALO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return HALO_OK;
+}
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Resolve the Hadamard block for a transformed dimension d.
+// had_block == 0: the reference's full-dimension transform (power-of-two
+// dimensions only on this path; 2^n*12 / 2^n*20 bases are not built).
+halo_status resolve_block(int64_t d, int64_t had_block, int64_t* B, const char* what) {
+    if (had_block < 0) return fail(HALO_ERR_INVALID_ARGUMENT, std::string(what) + ": negative Hadamard block");
+    const int64_t blk = had_block ? had_block : d;
+    if (!is_pow2(blk))
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    std::string(what) + ": Hadamard block " + std::to_string(blk) +
+                        " is not a power of two (hadamard.hpp:69-98 bases 12/20 are not on the device path)");
+    if (d % blk != 0)
+        return fail(HALO_ERR_INVALID_ARGUMENT, std::string(what) + ": Hadamard block " + std::to_string(blk) +
+                                                   " does not divide dimension " + std::to_string(d));
+    *B = blk;
+    return HALO_OK;
+}
+
+bool valid_format(int32_t f) { return f == HALO_FMT_INT8 || f == HALO_FMT_FP8_E4M3; }
+bool valid_dtype(int32_t d) { return d == HALO_DTYPE_F32 || d == HALO_DTYPE_BF16; }
+
+// device scalar block: absmax words, scales, error flag
+enum Slot { SX = 0, SW = 1, SEH = 2, SE = 3, SW2 = 4, SLOTS = 8 };
+struct DevScalars {
+    unsigned amax[SLOTS];
+    float scale[SLOTS];
+    unsigned err;
+    unsigned pad[7];
+};
+
+struct Buffer {
+    void* p = nullptr;
+    size_t bytes = 0;
+    halo_status ensure(size_t want) {
+        if (want <= bytes) return HALO_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (cudaMalloc(&p, want) != cudaSuccess) return fail(HALO_ERR_CUDA, "cudaMalloc failed");
+        bytes = want;
+        return HALO_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+struct halo_ctx {
+    bool valid = false;
+    int64_t b = 0, m = 0, n = 0, b_pad = 0;
+    bool xq_rotated = false, wq_rotated = false;
+    int32_t fmt = 0;
+    Buffer xq, wq, ehq, eq, wq2, scratch, gscratch;
+    Buffer dev;  // DevScalars
+    const uint8_t* wq_codes = nullptr;  // ctx.wq (own buffer or the layer's qweight)
+    const float* wq_scale = nullptr;
+    DevScalars* d() const { return dev.as<DevScalars>(); }
+    ~halo_ctx() {
+        xq.release(); wq.release(); ehq.release(); eq.release(); wq2.release(); scratch.release();
+        gscratch.release(); dev.release();
+    }
+};
+
+struct halo_linear {
+    halo_scheme s;
+    int64_t m = 0, n = 0;  // in_features, out_features
+    const void* w = nullptr;
+    int32_t w_dtype = HALO_DTYPE_BF16;
+    const uint8_t* qcodes = nullptr;
+    const float* qscale = nullptr;
+    std::atomic<int64_t> cx{0}, cw{0}, ce{0};
+};
+
+// ================================================================ helpers
+
+extern "C" int halo_abi_version(void) { return HALO_B200_ABI_VERSION; }
+extern "C" const char* halo_last_error(void) { return g_err.c_str(); }
+
+// hadamard.hpp:69-85
+extern "C" int halo_is_supported_hadamard_dim(int64_t d) {
+    if (d < 1) return 0;
+    int64_t odd = d;
+    int twos = 0;
+    while (odd % 2 == 0) {
+        odd /= 2;
+        ++twos;
+    }
+    if (odd == 1) return 1;
+    if ((odd == 3 || odd == 5) && twos >= 2) return 1;
+    return 0;
+}
+
+// hadamard.hpp:87-93
+extern "C" int64_t halo_next_supported_hadamard_dim(int64_t d) {
+    if (d < 1) d = 1;
+    while (!halo_is_supported_hadamard_dim(d)) ++d;
+    return d;
+}
+
+// halo_linear.hpp:393-397: rows padded for the left transform; with a block
+// the pad goes to the next multiple of the block.
+extern "C" int64_t halo_padded_batch(int64_t b, int64_t had_block) {
+    if (had_block > 0) return (b + had_block - 1) / had_block * had_block;
+    return halo_next_supported_hadamard_dim(b);
+}
+
+static halo_status placement_from(const char* s, size_t len, halo_placement* p) {
+    *p = halo_placement{0, 0, 0, 0};
+    for (size_t i = 0; i < len; ++i) {
+        switch (toupper((unsigned char)s[i])) {
+        case 'L': p->left = 1; break;
+        case 'M': p->middle = 1; break;
+        case 'R': p->right = 1; break;
+        case 'O': break;
+        default: return fail(HALO_ERR_INVALID_ARGUMENT, "placement: unknown letter in '" + std::string(s, len) + "'");
+        }
+    }
+    return HALO_OK;
+}
+
+// halo_linear.hpp:81-152
+extern "C" halo_status halo_scheme_from_string(const char* id, int32_t format, int64_t had_block, halo_scheme* out) {
+    if (!id || !out) return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: null argument");
+    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: format must be int8 or fp8_e4m3");
+    halo_scheme s;
+    std::memset(&s, 0, sizeof(s));
+    s.format_x = s.format_w = s.format_e = format;
+    s.quantize_f = s.quantize_e = s.quantize_g = 1;
+    s.had_block = had_block;
+    const std::string sid(id);
+    if (sid == "halo0" || sid == "halo1" || sid == "halo2" || sid == "halo-peft") {
+        if (sid != "halo0") {
+            s.F.middle = 1;  // halo1: F:M, E:R, G:R  (:90-98)
+            s.E.right = 1;
+            s.G.right = 1;
+        }
+        if (sid == "halo2" || sid == "halo-peft") s.E.left = 1;  // (:100-106)
+        if (sid == "halo-peft") s.peft = 1;
+        std::strncpy(s.name, sid.c_str(), sizeof(s.name) - 1);
+        *out = s;
+        return HALO_OK;
+    }
+    size_t pos = 0;
+    int seen = 0;
+    while (pos < sid.size()) {
+        size_t semi = sid.find(';', pos);
+        const std::string part = sid.substr(pos, semi == std::string::npos ? std::string::npos : semi - pos);
+        const size_t colon = part.find(':');
+        if (colon != 1 || part.empty())
+            return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: expected 'F:..;E:..;G:..', got '" + sid + "'");
+        halo_placement p;
+        if (placement_from(part.c_str() + 2, part.size() - 2, &p) != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+        switch (toupper((unsigned char)part[0])) {
+        case 'F': s.F = p; break;
+        case 'E': s.E = p; break;
+        case 'G': s.G = p; break;
+        default: return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: unknown matmul tag in '" + part + "'");
+        }
+        ++seen;
+        pos = semi == std::string::npos ? sid.size() : semi + 1;
+    }
+    if (seen == 0) return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: empty id");
+    *out = s;
+    return HALO_OK;
+}
+
+// ============================================================ primitives
+
+static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows, int64_t cols, int64_t B,
+                                        bool rotate, int32_t fmt, const float* supplied, uint8_t* codes,
+                                        unsigned* amax_word, float* scale_out, unsigned* err, cudaStream_t st) {
+    if (!supplied) {
+        cudaMemsetAsync(amax_word, 0, sizeof(unsigned), st);
+        if (rotate) run_rows(a, dt, rows, cols, B, 0, fmt, amax_word, nullptr, nullptr, nullptr, 0, err, nullptr, st);
+        else run_plain(a, dt, rows * cols, 0, fmt, amax_word, nullptr, nullptr, err, nullptr, st);
+    }
+    if (rotate) run_rows(a, dt, rows, cols, B, 1, fmt, amax_word, supplied, codes, nullptr, 0, err, scale_out, st);
+    else run_plain(a, dt, rows * cols, 1, fmt, amax_word, supplied, codes, err, scale_out, st);
+    return cuda_check("rotate_quantize");
+}
+
+namespace {
+// per-thread scratch for the free-function entry points
+struct FreeScratch {
+    Buffer dev;
+    ~FreeScratch() { dev.release(); }
+};
+thread_local FreeScratch t_scratch;
+DevScalars* free_scalars() {
+    if (t_scratch.dev.ensure(sizeof(DevScalars)) != HALO_OK) return nullptr;
+    return t_scratch.dev.as<DevScalars>();
+}
+}  // namespace
+
+extern "C" halo_status halo_rotate_quantize(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                            int64_t had_block, int32_t format, const float* supplied_scale,
+                                            uint8_t* codes, float* scale_out, halo_stream_t stream) {
+    if (!a || !codes) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: null pointer");
+    if (!valid_dtype(a_dtype) || !valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: bad dtype/format");
+    if (rows < 0 || cols <= 0 || cols % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: cols must be a positive multiple of 16");
+    if (rows == 0) return HALO_OK;
+    int64_t B = 1;
+    const bool rotate = had_block >= 0;
+    if (rotate && resolve_block(cols, had_block, &B, "rotate_quantize") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    DevScalars* d = free_scalars();
+    if (!d) return HALO_ERR_CUDA;
+    return rotate_quantize_impl(a, a_dtype, rows, cols, B, rotate, format, supplied_scale, codes, &d->amax[0],
+                                scale_out, &d->err, (cudaStream_t)stream);
+}
+
+namespace {
+__global__ void k_word_to_float(const unsigned* w, float* out) { *out = __uint_as_float(*w); }
+}  // namespace
+
+extern "C" halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                          int64_t had_block, float* absmax_out, halo_stream_t stream) {
+    if (!a || !absmax_out) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_absmax: null pointer");
+    if (!valid_dtype(a_dtype) || cols <= 0 || cols % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_absmax: bad arguments");
+    DevScalars* d = free_scalars();
+    if (!d) return HALO_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(&d->amax[0], 0, sizeof(unsigned), st);
+    if (rows > 0) {
+        if (had_block >= 0) {
+            int64_t B;
+            if (resolve_block(cols, had_block, &B, "rotate_absmax") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+            run_rows(a, a_dtype, rows, cols, B, 0, 0, &d->amax[0], nullptr, nullptr, nullptr, 0, &d->err, nullptr, st);
+        } else {
+            run_plain(a, a_dtype, rows * cols, 0, 0, &d->amax[0], nullptr, nullptr, &d->err, nullptr, st);
+        }
+    }
+    k_word_to_float<<<1, 1, 0, st>>>(&d->amax[0], absmax_out);
+    return cuda_check("rotate_absmax");
+}
+
+static halo_status left_quant_impl(const void* e, int32_t dt, int64_t b, int64_t n, int64_t B, int64_t b_pad,
+                                   int32_t fmt, uint8_t* codes_rot, uint8_t* codes_plain, unsigned* amax_r,
+                                   unsigned* amax_p, float* s_r, float* s_p, unsigned* err, cudaStream_t st) {
+    cudaMemsetAsync(amax_r, 0, sizeof(unsigned), st);
+    cudaMemsetAsync(amax_p, 0, sizeof(unsigned), st);
+    run_cols(e, dt, b, b_pad, n, B, 0, fmt, amax_r, amax_p, nullptr, nullptr, nullptr, nullptr, nullptr, 0, err,
+             nullptr, nullptr, st);
+    run_cols(e, dt, b, b_pad, n, B, 1, fmt, amax_r, amax_p, nullptr, nullptr, codes_rot, codes_plain, nullptr, 0, err,
+             s_r, s_p, st);
+    return cuda_check("left_rotate_quantize");
+}
+
+extern "C" halo_status halo_left_rotate_quantize(const void* e, int32_t e_dtype, int64_t b, int64_t n,
+                                                 int64_t had_block, int32_t format, uint8_t* codes_rot,
+                                                 float* scale_rot, uint8_t* codes_plain, float* scale_plain,
+                                                 halo_stream_t stream) {
+    if (!e || !codes_rot) return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: null pointer");
+    if (!valid_dtype(e_dtype) || !valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: bad dtype/format");
+    if (b <= 0 || n <= 0 || n % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: n must be a positive multiple of 16");
+    const int64_t b_pad = halo_padded_batch(b, had_block);
+    int64_t B;
+    if (resolve_block(b_pad, had_block, &B, "left_rotate_quantize") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    DevScalars* d = free_scalars();
+    if (!d) return HALO_ERR_CUDA;
+    return left_quant_impl(e, e_dtype, b, n, B, b_pad, format, codes_rot, codes_plain, &d->amax[SEH], &d->amax[SE],
+                           scale_rot, scale_plain, &d->err, (cudaStream_t)stream);
+}
+
+extern "C" halo_status halo_transform_right(const float* in, void* out, int32_t out_dtype, int64_t rows, int64_t cols,
+                                            int64_t had_block, halo_stream_t stream) {
+    if (!in || !out || !valid_dtype(out_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "transform_right: bad arguments");
+    if (cols <= 0 || cols % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "transform_right: cols must be a multiple of 16");
+    int64_t B;
+    if (resolve_block(cols, had_block, &B, "transform_right") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    if (rows == 0) return HALO_OK;
+    run_rows(in, HALO_DTYPE_F32, rows, cols, B, 2, 0, nullptr, nullptr, nullptr, out, out_dtype, nullptr, nullptr,
+             (cudaStream_t)stream);
+    return cuda_check("transform_right");
+}
+
+extern "C" halo_status halo_transform_left(const float* in, float* out, int64_t rows_pad, int64_t rows_out,
+                                           int64_t cols, int64_t had_block, halo_stream_t stream) {
+    if (!in || !out || rows_out > rows_pad) return fail(HALO_ERR_INVALID_ARGUMENT, "transform_left: bad arguments");
+    if (cols <= 0 || cols % 8) return fail(HALO_ERR_INVALID_ARGUMENT, "transform_left: cols must be a multiple of 8");
+    int64_t B;
+    if (resolve_block(rows_pad, had_block, &B, "transform_left") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    run_cols(in, HALO_DTYPE_F32, rows_pad, rows_pad, cols, B, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
+             nullptr, out, rows_out, nullptr, nullptr, nullptr, (cudaStream_t)stream);
+    return cuda_check("transform_left");
+}
+
+extern "C" halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_kmajor, const uint8_t* b,
+                                    int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
+                                    const float* scale_b, void* out, int32_t out_kind, halo_stream_t stream) {
+    if (!a || !b || !out || !scale_a || !scale_b) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: null pointer");
+    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad format");
+    if (out_kind < 0 || out_kind > 2) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad out kind");
+    const int r = run_gemm(format, a, b, M, N, K, a_kmajor, b_kmajor, scale_a, scale_b, out, out_kind,
+                           (cudaStream_t)stream);
+    if (r == -1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: unsupported shape (strides must be multiples of 16 B)");
+    if (r == -2) return fail(HALO_ERR_CUDA, "qmatmul: cuTensorMapEncodeTiled failed");
+    if (r != 0) return fail(HALO_ERR_CUDA, std::string("qmatmul: ") + cudaGetErrorString((cudaError_t)r));
+    return HALO_OK;
+}
+
+// ================================================================= layer
+
+static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
+    if (s.peft) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: peft is not on the device path yet");
+    if (!s.quantize_f || !s.quantize_e || !s.quantize_g)
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
+    if (s.granularity != 0) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: only tensor-wise scales are on the device path");
+    if (!valid_format(s.format_x) || s.format_x != s.format_w || s.format_x != s.format_e)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: X/W/E formats must agree and be int8 or fp8_e4m3");
+    if (s.F.left || s.F.right) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_F must be O or M (apply_placement engine is not on the device path)");
+    if (s.E.middle) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_E with M is not on the device path");
+    if (s.G.left || s.G.middle) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_G must be O or R");
+    if ((bool)s.G.right != (bool)s.F.middle)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: G's rotation must match F's (X is not kept in full precision)");
+    if (m <= 0 || n <= 0 || m % 16 || n % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: in/out features must be positive multiples of 16");
+    // validate_scheme_dims, halo_linear.hpp:343-348
+    const bool needs_m = s.F.middle || s.E.right || s.G.right;
+    if (needs_m) {
+        if (!halo_is_supported_hadamard_dim(s.had_block ? s.had_block : m))
+            return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: in_features is not a supported Hadamard dim");
+        int64_t B;
+        if (resolve_block(m, s.had_block, &B, "halo layer") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    }
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_create(const halo_scheme* scheme, const void* w, int32_t w_dtype,
+                                          int64_t out_features, int64_t in_features, halo_linear** out) {
+    if (!scheme || !out) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
+    if (!valid_dtype(w_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad weight dtype");
+    if (validate_scheme(*scheme, in_features, out_features) != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    auto* l = new halo_linear();
+    l->s = *scheme;
+    l->m = in_features;
+    l->n = out_features;
+    l->w = w;
+    l->w_dtype = w_dtype;
+    *out = l;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_destroy(halo_linear* layer) {
+    delete layer;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_set_weight(halo_linear* l, const void* w, int32_t w_dtype) {
+    if (!l || !valid_dtype(w_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "set_weight: bad arguments");
+    l->w = w;
+    l->w_dtype = w_dtype;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_set_qweight(halo_linear* l, const uint8_t* codes, const float* scale) {
+    if (!l) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight: null layer");
+    if (codes && !scale) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight: codes without a scale");
+    l->qcodes = codes;
+    l->qscale = scale;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_ctx_create(halo_ctx** out) {
+    if (!out) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: null");
+    auto* c = new halo_ctx();
+    if (c->dev.ensure(sizeof(DevScalars)) != HALO_OK) {
+        delete c;
+        return HALO_ERR_CUDA;
+    }
+    cudaMemset(c->dev.p, 0, sizeof(DevScalars));
+    *out = c;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_ctx_destroy(halo_ctx* ctx) {
+    delete ctx;
+    return HALO_OK;
+}
+
+// weight operand rotated as requested (weight_operand, halo_linear.hpp:352-358)
+static halo_status quantize_weight(halo_linear* l, halo_ctx* c, bool rotated, Buffer& dst, int slot,
+                                   const uint8_t** codes, const float** scale, cudaStream_t st) {
+    if (!l->w) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: no weight set");
+    if (dst.ensure((size_t)(l->n * l->m)) != HALO_OK) return HALO_ERR_CUDA;
+    int64_t B = 1;
+    if (rotated && resolve_block(l->m, l->s.had_block, &B, "weight") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    DevScalars* d = c->d();
+    const halo_status r = rotate_quantize_impl(l->w, l->w_dtype, l->n, l->m, B, rotated, l->s.format_w, nullptr,
+                                               dst.as<uint8_t>(), &d->amax[slot], &d->scale[slot], &d->err, st);
+    if (r != HALO_OK) return r;
+    ++l->cw;
+    *codes = dst.as<uint8_t>();
+    *scale = &d->scale[slot];
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_t x_dtype, int64_t b, void* y,
+                                           int32_t y_dtype, halo_ctx* c, halo_stream_t stream) {
+    if (!l || !x || !y || !c) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
+    if (!valid_dtype(x_dtype) || !valid_dtype(y_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
+    if (b <= 0) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: empty batch");
+    cudaStream_t st = (cudaStream_t)stream;
+    const halo_scheme& s = l->s;
+    const bool rot = s.F.middle;
+    // ctx = SavedContextT{}  (:270-273)
+    c->valid = false;
+    c->b = b;
+    c->m = l->m;
+    c->n = l->n;
+    c->fmt = s.format_x;
+    c->xq_rotated = c->wq_rotated = rot;
+    if (c->xq.ensure((size_t)(b * l->m)) != HALO_OK) return HALO_ERR_CUDA;
+    DevScalars* d = c->d();
+    int64_t B = 1;
+    if (rot && resolve_block(l->m, s.had_block, &B, "forward") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    // ctx.xq = quantize(XH)  (:292-294)
+    halo_status r = rotate_quantize_impl(x, x_dtype, b, l->m, B, rot, s.format_x, nullptr, c->xq.as<uint8_t>(),
+                                         &d->amax[SX], &d->scale[SX], &d->err, st);
+    if (r != HALO_OK) return r;
+    ++l->cx;
+    // ctx.wq = quantize(WH)  (:295-297), or the gathered / frozen codes
+    if (l->qcodes) {
+        c->wq_codes = l->qcodes;
+        c->wq_scale = l->qscale;
+    } else {
+        r = quantize_weight(l, c, rot, c->wq, SW, &c->wq_codes, &c->wq_scale, st);
+        if (r != HALO_OK) return r;
+    }
+    // Y = qmatmul(xq, wq, transpose_b=true)  (:299)
+    const int gr = run_gemm(s.format_x, c->xq.as<uint8_t>(), c->wq_codes, b, l->n, l->m, 1, 1, &d->scale[SX],
+                            c->wq_scale, y, y_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
+    if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
+    c->valid = true;
+    return cuda_check("forward");
+}
+
+// out = P (fp32, rows x cols) optionally right-rotated, converted to dtype
+static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
+                         cudaStream_t st) {
+    // B == 1 is the identity transform with norm 1: an exact copy/convert
+    run_rows(P, HALO_DTYPE_F32, rows, cols, rotate ? B : 1, 2, 0, nullptr, nullptr, nullptr, out, dtype, nullptr,
+             nullptr, st);
+}
+
+extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, const void* e_y, int32_t e_dtype,
+                                            void* e_x, int32_t ex_dtype, void* grad_w, int32_t gw_dtype,
+                                            halo_stream_t stream) {
+    if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
+    halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
+    if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
+    if (c->m != l->m || c->n != l->n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
+    if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
+    cudaStream_t st = (cudaStream_t)stream;
+    const halo_scheme& s = l->s;
+    const int64_t b = c->b, m = l->m, n = l->n;
+    const int fmt = s.format_e;
+    DevScalars* d = c->d();
+    int64_t Bm = 1;
+    if ((s.E.right || s.G.right) && resolve_block(m, s.had_block, &Bm, "backward") != HALO_OK)
+        return HALO_ERR_INVALID_ARGUMENT;
+    if (c->eq.ensure((size_t)(b * n)) != HALO_OK) return HALO_ERR_CUDA;
+
+    // weight operand for E with E's right rotation (:390)
+    const uint8_t* wq = c->wq_codes;
+    const float* sw = c->wq_scale;
+    if ((bool)s.E.right != c->wq_rotated) {
+        const halo_status r = quantize_weight(l, c, s.E.right, c->wq2, SW2, &wq, &sw, st);
+        if (r != HALO_OK) return r;
+    }
+
+    // ---- error path (:381-413)
+    if (s.E.left) {
+        const int64_t b_pad = halo_padded_batch(b, s.had_block);
+        int64_t Bb;
+        if (resolve_block(b_pad, s.had_block, &Bb, "backward (token dim)") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+        c->b_pad = b_pad;
+        if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK) return HALO_ERR_CUDA;
+        if (c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+        // (H_b E_Y)_Q and (E_Y)_Q in one pass (:399 and :371)
+        halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->ehq.as<uint8_t>(), c->eq.as<uint8_t>(),
+                                        &d->amax[SEH], &d->amax[SE], &d->scale[SEH], &d->scale[SE], &d->err, st);
+        if (r != HALO_OK) return r;
+        l->ce += 2;
+        float* P = c->scratch.as<float>();
+        // prod = qmatmul(eq, wq)  (:401): B operand (n x m) is MN-major
+        int gr = run_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
+        if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
+        // prod = transform_left(prod); take_rows(b)  (:405-409), in place
+        run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, P,
+                 b, nullptr, nullptr, nullptr, st);
+        // prod = transform_right_ht(prod)  (:410-411)
+        finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st);
+    } else {
+        c->b_pad = b;
+        const halo_status r = rotate_quantize_impl(e_y, e_dtype, b, n, 1, false, fmt, nullptr, c->eq.as<uint8_t>(),
+                                                   &d->amax[SE], &d->scale[SE], &d->err, st);
+        if (r != HALO_OK) return r;
+        l->ce += 1;
+        if (s.E.right) {
+            if (c->scratch.ensure((size_t)(b * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+            float* P = c->scratch.as<float>();
+            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
+            finish_right(P, e_x, ex_dtype, b, m, Bm, true, st);
+        } else {
+            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
+                              ex_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
+        }
+    }
+
+    // ---- gradient path (:418-439): G = (E_Y^T)_Q (XH)_Q [H^T]
+    if (grad_w) {
+        const uint8_t* xq = c->xq.as<uint8_t>();
+        if (s.G.right) {
+            if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+            float* G = c->gscratch.as<float>();
+            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], G, 0, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
+            finish_right(G, grad_w, gw_dtype, n, m, Bm, true, st);
+        } else {
+            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], grad_w,
+                              gw_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
+        }
+    }
+    return cuda_check("backward");
+}
+
+extern "C" halo_status halo_linear_export_inference_weights(halo_linear* l, uint8_t* codes, float* scale,
+                                                            halo_stream_t stream) {
+    if (!l || !codes || !scale) return fail(HALO_ERR_INVALID_ARGUMENT, "export: null argument");
+    if (!l->s.F.middle) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: export requires a rotated-forward scheme");
+    if (!l->w) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: no weight set");
+    int64_t B;
+    if (resolve_block(l->m, l->s.had_block, &B, "export") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    DevScalars* d = free_scalars();
+    if (!d) return HALO_ERR_CUDA;
+    return rotate_quantize_impl(l->w, l->w_dtype, l->n, l->m, B, true, l->s.format_w, nullptr, codes, &d->amax[SW],
+                                scale, &d->err, (cudaStream_t)stream);
+}
+
+extern "C" halo_status halo_linear_counters(const halo_linear* l, halo_counters* out) {
+    if (!l || !out) return fail(HALO_ERR_INVALID_ARGUMENT, "counters: null");
+    out->x = l->cx.load();
+    out->w = l->cw.load();
+    out->e = l->ce.load();
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_reset_counters(halo_linear* l) {
+    if (!l) return fail(HALO_ERR_INVALID_ARGUMENT, "counters: null");
+    l->cx = 0;
+    l->cw = 0;
+    l->ce = 0;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_ctx_saved(const halo_ctx* c, const uint8_t** xq, const float** sx, const uint8_t** wq,
+                                      const float** sw, int64_t* batch_rows) {
+    if (!c || !c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: no forward context");
+    if (xq) *xq = c->xq.as<uint8_t>();
+    if (sx) *sx = &c->d()->scale[SX];
+    if (wq) *wq = c->wq_codes;
+    if (sw) *sw = c->wq_scale;
+    if (batch_rows) *batch_rows = c->b;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_ctx_error_operands(const halo_ctx* c, const uint8_t** ehq, const float** seh,
+                                               const uint8_t** eq, const float** se, int64_t* b_pad) {
+    if (!c || !c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: no forward context");
+    if (ehq) *ehq = c->ehq.as<uint8_t>();
+    if (seh) *seh = &c->d()->scale[SEH];
+    if (eq) *eq = c->eq.as<uint8_t>();
+    if (se) *se = &c->d()->scale[SE];
+    if (b_pad) *b_pad = c->b_pad;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_ctx_check(halo_ctx* c, halo_stream_t stream) {
+    if (!c) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: null");
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return fail(HALO_ERR_CUDA, std::string("ctx check: ") + cudaGetErrorString(cudaGetLastError()));
+    unsigned err = 0;
+    cudaMemcpy(&err, &c->d()->err, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    if (err) {
+        cudaMemset(&c->d()->err, 0, sizeof(unsigned));
+        return fail(HALO_ERR_NUMERIC, "tensor: non-finite value in a quantized operand");
+    }
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_device_copy(void* dst, const void* src, int64_t bytes, halo_stream_t stream) {
+    if (bytes < 0 || (bytes && (!dst || !src))) return fail(HALO_ERR_INVALID_ARGUMENT, "device_copy: bad arguments");
+    if (bytes == 0) return HALO_OK;
+    if (cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return fail(HALO_ERR_CUDA, "device_copy failed");
+    return HALO_OK;
+}

@@ -1,0 +1,38 @@
+// halo_internal.h — internal launch interface between the host layer
+// (halo_capi.cpp) and the kernels (fwht_quant.cu, gemm_sm100.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace halo_b200 {
+
+int num_sms();
+float hadamard_norm(int64_t B);
+
+// K1 / K4-right: right transform over the contiguous dim (block B), then
+// mode 0 absmax / 1 quantize (fmt) / 2 write transformed values (out_dtype).
+void run_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t B, int mode, int fmt,
+              unsigned* amax, const float* supplied, uint8_t* codes, void* out, int out_dtype, unsigned* err,
+              float* scale_out, cudaStream_t st);
+
+// K2 / K4-left: left transform over rows (block B, rows_pad a multiple of
+// B; rows [b, rows_pad) are zero padding), plus the un-rotated E_Y path.
+void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t cols, int64_t B, int mode, int fmt,
+              unsigned* amax_rot, unsigned* amax_plain, const float* sup_rot, const float* sup_plain,
+              uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
+              float* scale_rot_out, float* scale_plain_out, cudaStream_t st);
+
+// un-rotated absmax / quantize
+void run_plain(const void* in, int in_dtype, int64_t n, int mode, int fmt, unsigned* amax, const float* supplied,
+               uint8_t* codes, unsigned* err, float* scale_out, cudaStream_t st);
+
+// K3: C[M x N] = A[M x K] * B[N x K]^T with per-tensor scales.
+//   A: a_kmajor ? [M][K] row-major : [K][M] row-major
+//   B: b_kmajor ? [N][K] row-major : [K][N] row-major
+//   out_kind: 0 fp32, 1 bf16, 2 raw int32 accumulators (INT8 only)
+// Returns 0 on success, else a cudaError_t / -1 for unsupported shapes.
+int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+             int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st);
+
+}  // namespace halo_b200

@@ -1,0 +1,142 @@
+// quant_round.cuh — bit-exact RTN quantizers for the fused kernels.
+//
+// The reference computes every code as round_code(double(x) / double(s))
+// (quantize.hpp:275) with nearbyint (ties to even) in double precision.  A
+// double division per element would cap the fused kernels far below HBM
+// speed, so the device path works in fp32 and then *proves* the result:
+//
+//   1. candidate q0 = RNE(x * (1/s)) in fp32 — within one grid step of the
+//      true RNE(x/s) because the fp32 quotient is off by < 2^-22 relative;
+//   2. the sign of  x - mid * s  for the midpoints between q0 and its grid
+//      neighbours is computed with ONE rounding by fmaf (mid * s is exact in
+//      the fma), so it is the sign of the exact real residual;
+//   3. the candidate moves one step if the true quotient lies beyond a
+//      midpoint, and an exact tie picks the even code (ties-to-even).
+//
+// The double path (x/s correctly rounded to double, then nearbyint) equals
+// the exact real RNE(x/s) here: a non-tie quotient of two floats sits at
+// least 2^-32 (relative) away from every half-integer / minifloat midpoint,
+// far above the 2^-53 double rounding error.  So both paths compute the same
+// function; tests/test_round_cpu.py checks this header against the oracle on
+// 10^8 inputs including every midpoint.  Valid for scales s >= 2^-100 (the
+// fma residual must not underflow; any realistic tensor).
+//
+// These functions are __host__ __device__ so the CPU test compiles exactly
+// the code the kernels run.
+#pragma once
+
+#include <stdint.h>
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define HALO_HD __host__ __device__ __forceinline__
+#else
+#define HALO_HD inline
+#endif
+
+namespace halo_b200 {
+
+// ---------------------------------------------------------------- INT8 ----
+// quantize.hpp:154-161: nearbyint, clamp to +-127 (-128 never produced).
+HALO_HD int8_t quant_int8(float x, float s, float inv_s) {
+    const float q0 = rintf(x * inv_s);
+    if (q0 >= 128.0f) return 127;   // true RNE >= 127 after a one-step fix
+    if (q0 <= -128.0f) return -127;
+    float q = q0;
+    const float hi = fmaf(-(q0 + 0.5f), s, x);  // sign(x/s - (q0 + 1/2))
+    const float lo = fmaf(-(q0 - 0.5f), s, x);  // sign(x/s - (q0 - 1/2))
+    if (hi > 0.0f) {
+        q = q0 + 1.0f;
+    } else if (hi == 0.0f) {
+        q = (((int)q0 & 1) == 0) ? q0 : q0 + 1.0f;  // tie -> even
+    } else if (lo < 0.0f) {
+        q = q0 - 1.0f;
+    } else if (lo == 0.0f) {
+        q = (((int)q0 & 1) == 0) ? q0 : q0 - 1.0f;
+    }
+    if (q > 127.0f) q = 127.0f;
+    if (q < -127.0f) q = -127.0f;
+    return (int8_t)(int)q;
+}
+
+// ---------------------------------------------------------------- E4M3 ----
+// quantize.hpp:138-150, 162-163: round_minifloat(x, 3 mantissa bits,
+// min_exp -6, saturate 448); zero is +0 (the "+ 0.0" at :149).
+// Encoding: OCP E4M3 (bias 7, S.1111.111 is NaN and never produced).
+
+HALO_HD int ilog2_pos(float v) {  // floor(log2(v)) for a finite v > 0
+    int e;
+    frexpf(v, &e);
+    return e - 1;
+}
+
+// grid spacing of the binade holding v (v >= 0)
+HALO_HD float e4m3_step(float v) {
+    int e = (v > 0.0f) ? ilog2_pos(v) : -6;
+    if (e < -6) e = -6;
+    return ldexpf(1.0f, e - 3);
+}
+
+// encode a non-negative grid value (<= 448) as the 7 magnitude bits
+HALO_HD uint8_t e4m3_bits_pos(float v) {
+    if (v == 0.0f) return 0;
+    int e = ilog2_pos(v);
+    if (e < -6) return (uint8_t)(int)(v * 512.0f);  // subnormal: m * 2^-9
+    const int mant = (int)((ldexpf(v, -e) - 1.0f) * 8.0f);
+    return (uint8_t)(((e + 7) << 3) | mant);
+}
+
+HALO_HD uint8_t quant_e4m3(float x, float s, float inv_s) {
+    const float a = fabsf(x);
+    const float y = a * inv_s;                 // approximate quotient
+    float q0;
+    if (y >= 464.0f) {
+        q0 = 480.0f;                            // beyond saturation; fixed below
+    } else {
+        const float st = e4m3_step(y);
+        q0 = rintf(y / st) * st;               // exact: st is a power of two
+    }
+    float q = q0;
+    // upward: midpoint between q0 and the next grid value
+    const float up = e4m3_step(q0);
+    const float mid_up = q0 + 0.5f * up;
+    const float r_up = fmaf(-mid_up, s, a);
+    if (r_up > 0.0f) {
+        q = q0 + up;
+    } else if (r_up == 0.0f) {
+        // tie: the grid neighbour with the even code wins
+        q = (e4m3_bits_pos(q0 > 448.0f ? 448.0f : q0) & 1) ? q0 + up : q0;
+    } else if (q0 > 0.0f) {
+        // downward: spacing below q0 halves when q0 opens a binade
+        float dn = up;
+        if (q0 <= 448.0f && ldexpf(1.0f, ilog2_pos(q0)) == q0 && ilog2_pos(q0) > -6) dn = 0.5f * up;
+        const float mid_dn = q0 - 0.5f * dn;
+        const float r_dn = fmaf(-mid_dn, s, a);
+        if (r_dn < 0.0f) {
+            q = q0 - dn;
+        } else if (r_dn == 0.0f) {
+            const float lowv = q0 - dn;
+            q = (e4m3_bits_pos(lowv) & 1) ? q0 : lowv;
+        }
+    }
+    if (q > 448.0f) q = 448.0f;
+    const uint8_t mag = e4m3_bits_pos(q);
+    return (mag != 0 && x < 0.0f) ? (uint8_t)(mag | 0x80) : mag;
+}
+
+// decode for the dequantize / epilogue paths
+HALO_HD float e4m3_to_float(uint8_t b) {
+    const int e = (b >> 3) & 0xF, m = b & 7;
+    const float v = e == 0 ? (float)m * ldexpf(1.0f, -9) : (1.0f + (float)m * 0.125f) * ldexpf(1.0f, e - 7);
+    return (b & 0x80) ? -v : v;
+}
+
+// quantize.hpp:234 / hqfsdp.hpp:172-177: s = float(double(absmax)/fmax),
+// 1.0 for an all-zero tensor.
+HALO_HD float scale_from_absmax(float absmax, int fmt) {
+    if (absmax == 0.0f) return 1.0f;
+    const double fmax = fmt == 0 ? 127.0 : 448.0;
+    return (float)((double)absmax / fmax);
+}
+
+}  // namespace halo_b200

@@ -1,0 +1,344 @@
+"""Python mirror of the reference HALO operator API over libhalo_b200.so.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/halo):
+
+=====================================  ======================================
+reference                              here
+=====================================  ======================================
+``halo0/halo1/halo2`` (:81-106),       ``halo0/halo1/halo2``,
+``scheme_from_string`` (:117-152)      ``scheme_from_string``
+``build_spec`` dims (hadamard:69-93)   ``is_supported_hadamard_dim``,
+                                       ``next_supported_hadamard_dim``
+``quantize(transform_right(a))``       ``rotate_quantize``
+``quantize(transform_left_h(pad(e)))`` ``left_rotate_quantize``
+``transform_right`` / ``_left``        ``transform_right`` / ``transform_left``
+``qmatmul`` (quantize:339-380)         ``qmatmul``
+``HaloLinearLayerT`` (:227-462)        ``HaloLinearLayer``
+``SavedContextT`` (:207-216)           ``SavedContext``
+``BackwardResultT`` (:220-225)         ``BackwardResult``
+``QuantCallCounters`` (:161-164)       ``Counters`` via ``layer.counters()``
+=====================================  ======================================
+
+Tensors are CUDA torch tensors (bf16 or fp32 inputs); torch is only the
+allocator and the stream provider.  Every op launches the sm_100a kernels
+of the shared library on ``torch.cuda.current_stream()``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import (DTYPE_BF16, DTYPE_F32, FMT_FP8_E4M3, FMT_INT8, OUT_BF16, OUT_F32, OUT_S32,
+                   Counters, Scheme, check, lib)
+
+INT8 = FMT_INT8
+FP8_E4M3 = FMT_FP8_E4M3
+
+_DT = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16}
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _dt(t):
+    if t.dtype not in _DT:
+        raise ValueError(f"unsupported dtype {t.dtype}: bf16 or fp32 expected")
+    return _DT[t.dtype]
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("HALO device path: tensors must live on a CUDA device")
+        if t is not None and not t.is_contiguous():
+            raise ValueError("HALO device path: tensors must be contiguous (row-major)")
+
+
+def code_dtype(fmt):
+    return torch.int8 if fmt == INT8 else torch.uint8
+
+
+# ------------------------------------------------------------------ schemes
+
+def scheme_from_string(id: str, fmt: int = INT8, had_block: int = 0) -> Scheme:
+    s = Scheme()
+    check(lib().halo_scheme_from_string(id.encode(), fmt, had_block, C.byref(s)))
+    return s
+
+
+def halo0(fmt=INT8, had_block=0):
+    return scheme_from_string("halo0", fmt, had_block)
+
+
+def halo1(fmt=INT8, had_block=0):
+    return scheme_from_string("halo1", fmt, had_block)
+
+
+def halo2(fmt=INT8, had_block=0):
+    return scheme_from_string("halo2", fmt, had_block)
+
+
+def is_supported_hadamard_dim(d: int) -> bool:
+    return bool(lib().halo_is_supported_hadamard_dim(d))
+
+
+def next_supported_hadamard_dim(d: int) -> int:
+    return int(lib().halo_next_supported_hadamard_dim(d))
+
+
+def padded_batch(b: int, had_block: int) -> int:
+    return int(lib().halo_padded_batch(b, had_block))
+
+
+# --------------------------------------------------------------- primitives
+
+def rotate_quantize(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, scale: torch.Tensor | None = None,
+                    rotate: bool = True):
+    """``quantize(transform_right(a, spec), fmt, tensor, scales)`` fused.
+
+    Returns ``(codes, scale)``: codes int8 (INT8) or uint8 OCP-E4M3 bytes of
+    the same shape, scale a 1-element fp32 CUDA tensor.  ``scale`` supplied ->
+    used verbatim (quantize.hpp:259-266)."""
+    _need_cuda(a, scale)
+    rows, cols = a.shape
+    codes = torch.empty((rows, cols), dtype=code_dtype(fmt), device=a.device)
+    s_out = scale.clone() if scale is not None else torch.empty(1, dtype=torch.float32, device=a.device)
+    check(lib().halo_rotate_quantize(_ptr(a), _dt(a), rows, cols, had_block if rotate else -1, fmt,
+                                     _ptr(scale), _ptr(codes), _ptr(s_out), _stream()))
+    return codes, s_out
+
+
+def rotate_absmax(a: torch.Tensor, had_block: int = 0, rotate: bool = True) -> torch.Tensor:
+    _need_cuda(a)
+    out = torch.empty(1, dtype=torch.float32, device=a.device)
+    check(lib().halo_rotate_absmax(_ptr(a), _dt(a), a.shape[0], a.shape[1], had_block if rotate else -1,
+                                   _ptr(out), _stream()))
+    return out
+
+
+def left_rotate_quantize(e: torch.Tensor, had_block: int = 0, fmt: int = INT8, plain: bool = True):
+    """HALO-2 error operands: ``(codes_rot[b_pad x n], scale_rot, codes_plain[b x n], scale_plain)``."""
+    _need_cuda(e)
+    b, n = e.shape
+    bp = padded_batch(b, had_block)
+    cr = torch.empty((bp, n), dtype=code_dtype(fmt), device=e.device)
+    cp = torch.empty((b, n), dtype=code_dtype(fmt), device=e.device) if plain else None
+    sr = torch.empty(1, dtype=torch.float32, device=e.device)
+    sp = torch.empty(1, dtype=torch.float32, device=e.device)
+    check(lib().halo_left_rotate_quantize(_ptr(e), _dt(e), b, n, had_block, fmt, _ptr(cr), _ptr(sr), _ptr(cp),
+                                          _ptr(sp), _stream()))
+    return cr, sr, cp, sp
+
+
+def transform_right(a: torch.Tensor, had_block: int = 0, out_dtype=torch.float32) -> torch.Tensor:
+    _need_cuda(a)
+    if a.dtype != torch.float32:
+        raise ValueError("transform_right takes fp32 input")
+    out = torch.empty(a.shape, dtype=out_dtype, device=a.device)
+    check(lib().halo_transform_right(_ptr(a), _ptr(out), _DT[out_dtype], a.shape[0], a.shape[1], had_block,
+                                     _stream()))
+    return out
+
+
+def transform_left(a: torch.Tensor, had_block: int = 0, rows_out: int | None = None) -> torch.Tensor:
+    _need_cuda(a)
+    if a.dtype != torch.float32:
+        raise ValueError("transform_left takes fp32 input")
+    rows_pad, cols = a.shape
+    rows_out = rows_pad if rows_out is None else rows_out
+    out = torch.empty((rows_out, cols), dtype=torch.float32, device=a.device) if rows_out != rows_pad \
+        else torch.empty_like(a)
+    if rows_out != rows_pad:
+        work = a.clone()
+        check(lib().halo_transform_left(_ptr(work), _ptr(work), rows_pad, rows_out, cols, had_block, _stream()))
+        out.copy_(work[:rows_out])
+        return out
+    check(lib().halo_transform_left(_ptr(a), _ptr(out), rows_pad, rows_out, cols, had_block, _stream()))
+    return out
+
+
+def qmatmul(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: torch.Tensor, *,
+            a_kmajor: bool = True, b_kmajor: bool = True, fmt: int = INT8, out: str = "f32") -> torch.Tensor:
+    """``qmatmul`` (quantize.hpp:339-380) on device codes.
+
+    A is ``[M, K]`` (a_kmajor) or ``[K, M]``; B is ``[N, K]`` (b_kmajor, the
+    reference's transpose_b) or ``[K, N]``.  out: "f32", "bf16" or "s32"
+    (raw int32 accumulators)."""
+    _need_cuda(a, b, scale_a, scale_b)
+    M, K = a.shape if a_kmajor else a.shape[::-1]
+    N, Kb = b.shape if b_kmajor else b.shape[::-1]
+    if K != Kb:
+        raise ValueError("qmatmul: inner dimensions disagree")
+    kind = {"f32": OUT_F32, "bf16": OUT_BF16, "s32": OUT_S32}[out]
+    dt = {OUT_F32: torch.float32, OUT_BF16: torch.bfloat16, OUT_S32: torch.int32}[kind]
+    c = torch.empty((M, N), dtype=dt, device=a.device)
+    check(lib().halo_qmatmul(fmt, _ptr(a), int(a_kmajor), _ptr(b), int(b_kmajor), M, N, K, _ptr(scale_a),
+                             _ptr(scale_b), _ptr(c), kind, _stream()))
+    return c
+
+
+# -------------------------------------------------------------------- layer
+
+class SavedContext:
+    """SavedContextT (halo_linear.hpp:207-216): owns (XH)_Q, (WH)_Q and scales
+    in device memory.  No full-precision copy of X is kept."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib().halo_ctx_create(C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.halo_ctx_destroy(h)
+            self._h = None
+
+    def saved(self, layer: "HaloLinearLayer"):
+        """Views of (xq, sx, wq, sw) as torch tensors (copies)."""
+        xq, sx, wq, sw = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        b = C.c_int64()
+        check(lib().halo_ctx_saved(self._h, C.byref(xq), C.byref(sx), C.byref(wq), C.byref(sw), C.byref(b)))
+        dt = code_dtype(layer.fmt)
+        return (_from_ptr(xq.value, (b.value, layer.in_features), dt),
+                _from_ptr(sx.value, (1,), torch.float32),
+                _from_ptr(wq.value, (layer.out_features, layer.in_features), dt),
+                _from_ptr(sw.value, (1,), torch.float32))
+
+    def error_operands(self, layer: "HaloLinearLayer"):
+        ehq, seh, eq, se = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        bp = C.c_int64()
+        check(lib().halo_ctx_error_operands(self._h, C.byref(ehq), C.byref(seh), C.byref(eq), C.byref(se),
+                                            C.byref(bp)))
+        dt = code_dtype(layer.fmt)
+        b = layer._last_b
+        out = {"eq": _from_ptr(eq.value, (b, layer.out_features), dt),
+               "se": _from_ptr(se.value, (1,), torch.float32)}
+        if layer.scheme.E.left:
+            out["ehq"] = _from_ptr(ehq.value, (bp.value, layer.out_features), dt)
+            out["seh"] = _from_ptr(seh.value, (1,), torch.float32)
+        return out
+
+    def check(self):
+        """Synchronise and raise HaloNumericError for non-finite inputs."""
+        check(lib().halo_ctx_check(self._h, _stream()))
+
+
+def _from_ptr(ptr, shape, dtype):
+    """Copy `numel` elements at a device address into a fresh tensor."""
+    numel = 1
+    for s in shape:
+        numel *= s
+    out = torch.empty(shape, dtype=dtype, device="cuda")
+    check(lib().halo_device_copy(_ptr(out), C.c_void_p(ptr), numel * out.element_size(), _stream()))
+    return out
+
+
+@dataclass
+class BackwardResult:
+    """BackwardResultT (halo_linear.hpp:220-225)."""
+    e_x: torch.Tensor
+    grad_w: torch.Tensor | None
+
+
+class HaloLinearLayer:
+    """HaloLinearLayerT (halo_linear.hpp:227-462) on the B200.
+
+    ``w`` is the (out x in) weight, bf16 or fp32, on a CUDA device; the layer
+    keeps a reference (not a copy) and re-rotates/re-quantizes it at every
+    forward, as the reference does (:295-297).  Errors mirror the
+    reference: ValueError for std::invalid_argument, HaloNumericError for
+    numeric_error."""
+
+    def __init__(self, w: torch.Tensor, scheme: Scheme, out_dtype=torch.bfloat16, grad_dtype=torch.float32):
+        _need_cuda(w)
+        self.w = w
+        self.scheme = scheme
+        self.fmt = scheme.format_x
+        self.out_dtype = out_dtype
+        self.grad_dtype = grad_dtype
+        self._last_b = 0
+        h = C.c_void_p()
+        check(lib().halo_linear_create(C.byref(scheme), _ptr(w), _dt(w), w.shape[0], w.shape[1], C.byref(h)))
+        self._h = h
+        self._qweight = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.halo_linear_destroy(h)
+            self._h = None
+
+    @property
+    def in_features(self):
+        return self.w.shape[1]
+
+    @property
+    def out_features(self):
+        return self.w.shape[0]
+
+    def set_weight(self, w: torch.Tensor):
+        _need_cuda(w)
+        if tuple(w.shape) != (self.out_features, self.in_features):
+            raise ValueError("halo layer: weight shape mismatch")
+        self.w = w
+        check(lib().halo_linear_set_weight(self._h, _ptr(w), _dt(w)))
+
+    def set_qweight(self, codes: torch.Tensor | None, scale: torch.Tensor | None):
+        """Use gathered / frozen (WH)_Q codes instead of quantizing W."""
+        if codes is not None:
+            _need_cuda(codes, scale)
+        self._qweight = (codes, scale)
+        check(lib().halo_linear_set_qweight(self._h, _ptr(codes), _ptr(scale)))
+
+    def forward(self, x: torch.Tensor, ctx: SavedContext) -> torch.Tensor:
+        _need_cuda(x)
+        if x.dim() != 2 or x.shape[1] != self.in_features:
+            raise ValueError("halo layer: input feature dim mismatch")
+        b = x.shape[0]
+        y = torch.empty((b, self.out_features), dtype=self.out_dtype, device=x.device)
+        check(lib().halo_linear_forward(self._h, _ptr(x), _dt(x), b, _ptr(y), _DT[self.out_dtype], ctx._h,
+                                        _stream()))
+        self._last_b = b
+        ctx._layer_b = b
+        return y
+
+    def backward(self, ctx: SavedContext, e_y: torch.Tensor, need_grad_w: bool = True,
+                 e_x_dtype=None) -> BackwardResult:
+        _need_cuda(e_y)
+        b = getattr(ctx, "_layer_b", None)
+        if b is None:
+            raise ValueError("halo layer: backward without forward context")
+        if e_y.dim() != 2 or e_y.shape[0] != b or e_y.shape[1] != self.out_features:
+            raise ValueError("halo layer: upstream error shape mismatch")
+        ex_dt = e_x_dtype or self.out_dtype
+        e_x = torch.empty((b, self.in_features), dtype=ex_dt, device=e_y.device)
+        g = torch.empty((self.out_features, self.in_features), dtype=self.grad_dtype, device=e_y.device) \
+            if need_grad_w else None
+        check(lib().halo_linear_backward(self._h, ctx._h, _ptr(e_y), _dt(e_y), _ptr(e_x), _DT[ex_dt], _ptr(g),
+                                         _DT[self.grad_dtype], _stream()))
+        return BackwardResult(e_x, g)
+
+    def export_inference_weights(self):
+        """(WH)_Q codes and scale (halo_linear.hpp:332-338)."""
+        codes = torch.empty((self.out_features, self.in_features), dtype=code_dtype(self.fmt), device=self.w.device)
+        scale = torch.empty(1, dtype=torch.float32, device=self.w.device)
+        check(lib().halo_linear_export_inference_weights(self._h, _ptr(codes), _ptr(scale), _stream()))
+        return codes, scale
+
+    def counters(self) -> Counters:
+        c = Counters()
+        check(lib().halo_linear_counters(self._h, C.byref(c)))
+        return c
+
+    def reset_counters(self):
+        check(lib().halo_linear_reset_counters(self._h))

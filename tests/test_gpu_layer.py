@@ -1,0 +1,178 @@
+"""GPU parity of the HALO linear operator (halo_linear.hpp:227-462).
+
+INT8: every output (Y, E_X, G) is compared BIT-EXACTLY with the oracle in
+fp32 — the kernels reproduce the reference's butterfly order, quantizer and
+double-precision epilogue.  bf16 outputs must equal the RNE of those fp32
+values (stated tolerance 1e-3 relative is therefore met with margin 0).
+FP8 E4M3: codes/scales bit-exact, outputs within 1e-5 relative (Frobenius)
+— the reference accumulates dequantized products in double
+(quantize.hpp:377-379), the tensor core in fp32.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_02625_b200 import halo
+    return halo
+
+
+def inputs(O, b, m, n, seed=1):
+    # SURVEY §8d synthetic data: X ~ N(0,1) with outlier columns, W ~
+    # N(0, 1/sqrt(m)) with outlier columns, E_Y ~ N(0, 1e-3) with outlier rows
+    X = O.randn(b, m, seed)
+    for c in (2, 9, 16, 27):
+        if c < m:
+            X[:, c] *= 40
+    W = O.randn(n, m, seed + 1, 1.0 / np.sqrt(m))
+    for c in (5, 19):
+        if c < m:
+            W[:, c] *= 20
+    E = O.randn(b, n, seed + 2, 1e-3)
+    E[min(3, b - 1), :] *= 30
+    E[b // 2, :] *= 30
+    return O.bf16_round(X), O.bf16_round(W), O.bf16_round(E)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+LEVELS = {"halo0": 0, "halo1": 1, "halo2": 2}
+
+
+@pytest.mark.parametrize("scheme", ["halo0", "halo1", "halo2"])
+@pytest.mark.parametrize("b,m,n,block", [(256, 256, 128, 256), (300, 512, 256, 256), (64, 128, 96, 32),
+                                         (128, 256, 256, 0), (96, 64, 48, 16)])
+def test_layer_int8_bitexact(H, orc, scheme, b, m, n, block):
+    X, W, E = inputs(orc, b, m, n)
+    want = orc.linear(LEVELS[scheme], 0, block, X, W, E)
+    Wt = torch.from_numpy(W).cuda().to(torch.bfloat16)
+    layer = H.HaloLinearLayer(Wt, H.scheme_from_string(scheme, 0, block), out_dtype=torch.float32)
+    ctx = H.SavedContext()
+    y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
+    back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
+    ctx.check()
+    xq, sx, wq, sw = ctx.saved(layer)
+    assert sx.item() == want["sx"] and sw.item() == want["sw"]
+    assert np.array_equal(xq.cpu().numpy(), orc.codes_to_bytes(want["xq"], 0))
+    assert np.array_equal(wq.cpu().numpy(), orc.codes_to_bytes(want["wq"], 0))
+    assert np.array_equal(y.cpu().numpy(), want["Y"])
+    assert np.array_equal(back.e_x.cpu().numpy(), want["EX"])
+    assert np.array_equal(back.grad_w.cpu().numpy(), want["GW"])
+    c = layer.counters()  # test_halo_linear.cpp:149-179
+    assert (c.x, c.w, c.e) == (1, 1, 2 if scheme == "halo2" else 1)
+
+
+@pytest.mark.parametrize("scheme", ["halo1", "halo2"])
+def test_layer_bf16_outputs_within_tolerance(H, orc, scheme):
+    b, m, n, block = 512, 512, 256, 256
+    X, W, E = inputs(orc, b, m, n, seed=7)
+    want = orc.linear(LEVELS[scheme], 0, block, X, W, E)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16), H.scheme_from_string(scheme, 0, block))
+    ctx = H.SavedContext()
+    y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
+    back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
+    # bf16 outputs are the RNE of the bit-exact fp32 results
+    assert torch.equal(y, torch.from_numpy(want["Y"]).cuda().to(torch.bfloat16))
+    assert torch.equal(back.e_x, torch.from_numpy(want["EX"]).cuda().to(torch.bfloat16))
+    # the stated tolerance (1e-3 relative, bf16) against the bf16-rounded oracle
+    assert rel(y.float().cpu().numpy(), orc.bf16_round(want["Y"])) < 1e-3
+    assert rel(back.e_x.float().cpu().numpy(), orc.bf16_round(want["EX"])) < 1e-3
+    assert rel(back.grad_w.cpu().numpy(), want["GW"]) == 0.0
+
+
+@pytest.mark.parametrize("scheme", ["halo0", "halo1", "halo2"])
+def test_layer_fp8(H, orc, scheme):
+    b, m, n, block = 256, 256, 128, 256
+    X, W, E = inputs(orc, b, m, n, seed=3)
+    want = orc.linear(LEVELS[scheme], 1, block, X, W, E)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16), H.scheme_from_string(scheme, 1, block),
+                              out_dtype=torch.float32)
+    ctx = H.SavedContext()
+    y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
+    back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
+    xq, sx, wq, sw = ctx.saved(layer)
+    assert sx.item() == want["sx"] and sw.item() == want["sw"]
+    assert np.array_equal(xq.cpu().numpy(), orc.codes_to_bytes(want["xq"], 1))
+    assert np.array_equal(wq.cpu().numpy(), orc.codes_to_bytes(want["wq"], 1))
+    assert rel(y.cpu().numpy(), want["Y"]) < 1e-5
+    assert rel(back.e_x.cpu().numpy(), want["EX"]) < 1e-5
+    assert rel(back.grad_w.cpu().numpy(), want["GW"]) < 1e-5
+
+
+def test_layer_matches_reference_library(H, orc):
+    """Full-dimension transforms (had_block=0) against the UNMODIFIED
+    reference HaloLinearLayer (oracle/_ref, built from /root/reference)."""
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    b, m, n = 128, 256, 64
+    X, W, E = inputs(orc, b, m, n, seed=11)
+    want = orc.ref_linear(2, 0, 0, X, W, E)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16), H.halo2(), out_dtype=torch.float32)
+    ctx = H.SavedContext()
+    y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
+    back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
+    assert np.array_equal(y.cpu().numpy(), want["Y"])
+    assert np.array_equal(back.e_x.cpu().numpy(), want["EX"])
+    assert np.array_equal(back.grad_w.cpu().numpy(), want["GW"])
+
+
+def test_export_and_qweight(H, orc):
+    b, m, n = 64, 256, 128
+    X, W, E = inputs(orc, b, m, n, seed=5)
+    Wt = torch.from_numpy(W).cuda().to(torch.bfloat16)
+    layer = H.HaloLinearLayer(Wt, H.halo2(0, 256), out_dtype=torch.float32)
+    codes, scale = layer.export_inference_weights()
+    want_codes, want_s = orc.quantize(orc.fwht_rows(W, 256), 0)
+    assert scale.item() == want_s[0]
+    assert np.array_equal(codes.cpu().numpy(), orc.codes_to_bytes(want_codes, 0))
+    # a gathered / frozen (WH)_Q reproduces the quantize-in-forward result
+    ctx = H.SavedContext()
+    y1 = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
+    layer2 = H.HaloLinearLayer(Wt, H.halo2(0, 256), out_dtype=torch.float32)
+    layer2.set_qweight(codes, scale)
+    ctx2 = H.SavedContext()
+    y2 = layer2.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx2)
+    assert torch.equal(y1, y2)
+    assert layer2.counters().w == 0
+
+
+def test_nonfinite_input_raises(H, orc):
+    b, m, n = 32, 64, 32
+    X, W, E = inputs(orc, b, m, n)
+    X[3, 5] = np.nan
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda(), H.halo2(0, 64))
+    ctx = H.SavedContext()
+    layer.forward(torch.from_numpy(X).cuda(), ctx)
+    with pytest.raises(H._lib.HaloNumericError):
+        ctx.check()
+
+
+def test_scheme_validation(H):
+    # shape and scheme validation (test_halo_linear.cpp:386-409)
+    w = torch.zeros((16, 48), device="cuda")  # 48 = 2^4*3: not a power-of-two Hadamard dim
+    with pytest.raises(ValueError):
+        H.HaloLinearLayer(w, H.halo1())
+    H.HaloLinearLayer(w, H.halo0())
+    w2 = torch.zeros((16, 64), device="cuda")
+    layer = H.HaloLinearLayer(w2, H.halo1())
+    ctx = H.SavedContext()
+    with pytest.raises(ValueError):
+        layer.forward(torch.zeros((4, 32), device="cuda"), ctx)
+    with pytest.raises(ValueError):
+        layer.backward(ctx, torch.zeros((4, 16), device="cuda"))
+    layer.forward(torch.zeros((4, 64), device="cuda"), ctx)
+    with pytest.raises(ValueError):
+        layer.backward(ctx, torch.zeros((5, 16), device="cuda"))
+    with pytest.raises(ValueError):
+        H.scheme_from_string("halo3")
+    with pytest.raises(ValueError):
+        H.scheme_from_string("")
