@@ -189,6 +189,30 @@ HALO_API halo_status halo_ctx_check(halo_ctx* ctx, halo_stream_t stream);
 /* stream-ordered device-to-device copy (used to snapshot ctx views) */
 HALO_API halo_status halo_device_copy(void* dst, const void* src, int64_t bytes, halo_stream_t stream);
 
+/* ------------------------------------------------- Llama MLP block glue */
+/* h = silu(g) * u ; bf16, n elements (n % 8 == 0).  model.hpp:77-96 is the
+ * reference's silu; the Llama MLP gates it with the up projection. */
+HALO_API halo_status halo_swiglu_forward(const void* g, const void* u, void* h, int64_t n, halo_stream_t stream);
+HALO_API halo_status halo_swiglu_backward(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n,
+                                          halo_stream_t stream);
+/* out = a + b elementwise (f32 or bf16), n % 8 == 0 */
+HALO_API halo_status halo_add(const void* a, const void* b, void* out, int32_t dtype, int64_t n,
+                              halo_stream_t stream);
+
+/* ------------------------------------------------------------- profiling */
+/* Kernel classes: 0 K1 row-FWHT+quantize, 1 K2 column-FWHT+dual quantize,
+ * 2 K3 tcgen05 GEMM, 3 K4 output un-rotation, 4 elementwise glue.
+ * work = algorithmic bytes (classes 0,1,3,4) or integer ops (class 2). */
+typedef struct halo_profile {
+    int64_t launches[5];
+    double ms[5];
+    double work[5];
+} halo_profile;
+/* bracket every kernel launch with CUDA events on its stream (off by default) */
+HALO_API halo_status halo_profile_enable(int on);
+/* synchronises the device, reduces the recorded launches, clears them */
+HALO_API halo_status halo_profile_read(halo_profile* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,17 @@ class Counters(C.Structure):
     _fields_ = [("x", C.c_int64), ("w", C.c_int64), ("e", C.c_int64)]
 
 
+PROFILE_CLASSES = ("k1_rows_fwht_quant", "k2_cols_fwht_quant", "k3_gemm", "k4_unrotate", "glue")
+
+
+class Profile(C.Structure):
+    _fields_ = [("launches", C.c_int64 * 5), ("ms", C.c_double * 5), ("work", C.c_double * 5)]
+
+    def as_dict(self):
+        return {name: {"launches": int(self.launches[i]), "ms": float(self.ms[i]), "work": float(self.work[i])}
+                for i, name in enumerate(PROFILE_CLASSES)}
+
+
 _lib = None
 
 _vp = C.c_void_p
@@ -113,6 +124,14 @@ def lib():
                                           C.POINTER(_vp), C.POINTER(_i64)]
     L.halo_ctx_check.argtypes = [_vp, _vp]
     L.halo_device_copy.argtypes = [_vp, _vp, _i64, _vp]
+    L.halo_swiglu_forward.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.halo_swiglu_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _vp]
+    L.halo_add.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp]
+    L.halo_profile_enable.argtypes = [C.c_int]
+    L.halo_profile_read.argtypes = [C.POINTER(Profile)]
+    for fn in ("halo_swiglu_forward", "halo_swiglu_backward", "halo_add", "halo_profile_enable",
+               "halo_profile_read"):
+        getattr(L, fn).restype = C.c_int
     for fn in ("halo_scheme_from_string", "halo_rotate_quantize", "halo_rotate_absmax",
                "halo_left_rotate_quantize", "halo_transform_right", "halo_transform_left",
                "halo_qmatmul", "halo_linear_create", "halo_linear_destroy", "halo_linear_set_weight",
@@ -150,5 +169,6 @@ EXPORTS = (
     "halo_linear_set_weight", "halo_linear_set_qweight", "halo_ctx_create", "halo_ctx_destroy",
     "halo_linear_forward", "halo_linear_backward", "halo_linear_export_inference_weights",
     "halo_linear_counters", "halo_linear_reset_counters", "halo_ctx_saved",
-    "halo_ctx_error_operands", "halo_ctx_check", "halo_device_copy",
+    "halo_ctx_error_operands", "halo_ctx_check", "halo_device_copy", "halo_swiglu_forward",
+    "halo_swiglu_backward", "halo_add", "halo_profile_enable", "halo_profile_read",
 )

@@ -89,12 +89,48 @@ __device__ __forceinline__ void atomic_absmax(unsigned* slot, float v) {
     atomicMax(slot, __float_as_uint(v));
 }
 
-__device__ __forceinline__ bool finite8(const float v[8]) {
-    bool ok = true;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ok = ok && isfinite(v[i]);
-    return ok;
+// branch-free non-finite test: all exponent bits set
+__device__ __forceinline__ uint32_t nonfinite_bits(float x) {
+    return (uint32_t)((__float_as_uint(x) & 0x7f800000u) == 0x7f800000u);
 }
+__device__ __forceinline__ bool finite8(const float v[8]) {
+    uint32_t bad = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) bad |= nonfinite_bits(v[i]);
+    return bad == 0;
+}
+
+// raw 8-element vectors: loads are issued before any arithmetic so a warp
+// keeps several 16-32 B requests in flight
+template <typename T>
+struct Raw8;
+template <>
+struct Raw8<__nv_bfloat16> {
+    uint4 r;
+    __device__ __forceinline__ void load(const __nv_bfloat16* p) { r = __ldg(reinterpret_cast<const uint4*>(p)); }
+    __device__ __forceinline__ void zero() { r = make_uint4(0, 0, 0, 0); }
+    __device__ __forceinline__ void get(float v[8]) const {
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            v[2 * i] = __uint_as_float(w[i] << 16);
+            v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+};
+template <>
+struct Raw8<float> {
+    float4 a, b;
+    __device__ __forceinline__ void load(const float* p) {
+        a = __ldg(reinterpret_cast<const float4*>(p));
+        b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    }
+    __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+    __device__ __forceinline__ void get(float v[8]) const {
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+};
 
 // scale and its reciprocal from the device absmax word (or a supplied scale)
 __device__ __forceinline__ void resolve_scale(const unsigned* absmax_bits, const float* supplied, int fmt,

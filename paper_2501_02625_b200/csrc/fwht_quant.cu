@@ -22,11 +22,9 @@
 // K1 (rows, B <= 256): one warp per 256-element chunk, 8 contiguous elements
 //   per lane (one 16 B load), stages 1,2,4 in registers, 8..128 via
 //   shfl.xor 1..16.  Grid-stride over chunks.
-// K2 (cols, B <= 256): a CTA stages a 256-row x 64-column tile in shared
-//   memory (row pitch 68 floats: conflict-free column reads); each thread
-//   owns one column x 32 rows (rows t+8i): stages 1,2,4 via shfl.xor 1,2,4,
-//   8..128 in registers.  The same pass emits the un-rotated E_Y codes.
-// B > 256: a CTA-per-segment shared-memory kernel (parity / sweep path).
+// The production kernels for 8 <= B <= 256 (rows) and B <= 256 (columns)
+// live in fwht2.cu; this file keeps the warp-shuffle row kernel for B < 8
+// and a CTA-per-segment shared-memory kernel for B > 256 (parity / sweep).
 #include "common.cuh"
 #include "halo_internal.h"
 
@@ -114,145 +112,6 @@ __global__ void __launch_bounds__(256) k_rows_small(const InT* __restrict__ in, 
         const unsigned bad = __any_sync(0xffffffffu, !ok);
         if (lane == 0) {
             atomic_absmax(absmax, amax);
-            if (bad) atomicOr(err, ERRF_NONFINITE);
-        }
-    }
-}
-
-// --------------------------------------------------------------- columns --
-constexpr int KC_ROWS = 256, KC_COLS = 64, KC_PITCH = 68;
-
-// K2 / K4-left.  in: rows x cols (rows >= b real rows; rows in [b, rows_pad)
-// are the zero padding of halo_linear.hpp:393-397).  B | rows_pad.
-//   MODE_ABSMAX: absmax of H*in -> absmax_rot, absmax of in -> absmax_plain
-//   MODE_QUANT : codes of H*in (rows_pad rows) and of in (b rows)
-//   MODE_XFORM : fp32 H*in -> out (first rows_out rows), in may alias out
-template <typename InT, int LOGB, int FMT, int MODE>
-__global__ void __launch_bounds__(256) k_cols_small(const InT* in, int64_t b, int64_t rows_pad, int64_t cols,
-                                                    int lb_rt, float norm, unsigned* absmax_rot, unsigned* absmax_plain,
-                                                    const float* sup_rot, const float* sup_plain,
-                                                    uint8_t* __restrict__ codes_rot,
-                                                    uint8_t* __restrict__ codes_plain, float* out,
-                                                    int64_t rows_out, unsigned* err, float* scale_rot_out,
-                                                    float* scale_plain_out) {
-    extern __shared__ __align__(16) float tile[];  // [KC_ROWS][KC_PITCH]
-    const int lb = LOGB >= 0 ? LOGB : lb_rt;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t col_tiles = (cols + KC_COLS - 1) / KC_COLS;
-    const int64_t row_tiles = (rows_pad + KC_ROWS - 1) / KC_ROWS;
-    float s_r = 1.f, i_r = 1.f, s_p = 1.f, i_p = 1.f;
-    if constexpr (MODE == MODE_QUANT) {
-        resolve_scale(absmax_rot, sup_rot, FMT, &s_r, &i_r);
-        resolve_scale(absmax_plain, sup_plain, FMT, &s_p, &i_p);
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            if (scale_rot_out) *scale_rot_out = s_r;
-            if (scale_plain_out) *scale_plain_out = s_p;
-        }
-    }
-    float amax_r = 0.f, amax_p = 0.f;
-    bool ok = true;
-    for (int64_t t = blockIdx.x; t < col_tiles * row_tiles; t += gridDim.x) {
-        const int64_t r0 = (t / col_tiles) * KC_ROWS;
-        const int64_t c0 = (t % col_tiles) * KC_COLS;
-        // ---- load (coalesced, 8 elements per vector) + plain path
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int vi = tid + 256 * k;
-            const int r = vi >> 3, cv = (vi & 7) * 8;
-            const int64_t gr = r0 + r, gc = c0 + cv;
-            float v[8];
-            if (gr < b && gc < cols) {
-                load8(in + gr * cols + gc, v);
-                if constexpr (MODE == MODE_ABSMAX) {
-                    ok = ok && finite8(v);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) amax_p = fmaxf(amax_p, fabsf(v[i]));
-                } else if constexpr (MODE == MODE_QUANT) {
-                    if (codes_plain) quant_store8<FMT>(codes_plain + gr * cols + gc, v, s_p, i_p);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = 0.f;
-            }
-            float* d = tile + r * KC_PITCH + cv;
-            reinterpret_cast<float4*>(d)[0] = make_float4(v[0], v[1], v[2], v[3]);
-            reinterpret_cast<float4*>(d)[1] = make_float4(v[4], v[5], v[6], v[7]);
-        }
-        __syncthreads();
-        // ---- column butterflies: thread owns column c, rows tp + 8*i
-        const int tp = lane & 7;
-#pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
-            const int c = pass * 32 + warp * 4 + (lane >> 3);
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = tile[(tp + 8 * i) * KC_PITCH + c];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {  // len = 1, 2, 4 across lanes
-                if ((1 << j) < (1 << lb)) {
-                    const int m = 1 << j;
-                    const bool upper = (lane & m) != 0;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
-                        v[i] = upper ? (o - v[i]) : (v[i] + o);
-                    }
-                }
-            }
-#pragma unroll
-            for (int len = 1; len < 32; len <<= 1) {  // len*8 = 8 .. 128 in registers
-                if ((len * 8) < (1 << lb)) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if ((i & len) == 0) {
-                            const float x = v[i], y = v[i + len];
-                            v[i] = x + y;
-                            v[i + len] = x - y;
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= norm;
-            if constexpr (MODE == MODE_ABSMAX) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    ok = ok && isfinite(v[i]);
-                    amax_r = fmaxf(amax_r, fabsf(v[i]));
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) tile[(tp + 8 * i) * KC_PITCH + c] = v[i];
-            }
-        }
-        __syncthreads();
-        // ---- store (coalesced)
-        if constexpr (MODE != MODE_ABSMAX) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int vi = tid + 256 * k;
-                const int r = vi >> 3, cv = (vi & 7) * 8;
-                const int64_t gr = r0 + r, gc = c0 + cv;
-                const float* sp = tile + r * KC_PITCH + cv;
-                const float4 a = reinterpret_cast<const float4*>(sp)[0];
-                const float4 bq = reinterpret_cast<const float4*>(sp)[1];
-                const float v[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
-                if constexpr (MODE == MODE_QUANT) {
-                    if (gr < rows_pad && gc < cols) quant_store8<FMT>(codes_rot + gr * cols + gc, v, s_r, i_r);
-                } else {
-                    if (gr < rows_out && gc < cols) store8(out + gr * cols + gc, v);
-                }
-            }
-            __syncthreads();
-        }
-    }
-    if constexpr (MODE == MODE_ABSMAX) {
-        amax_r = warp_max(amax_r);
-        amax_p = warp_max(amax_p);
-        const unsigned bad = __any_sync(0xffffffffu, !ok);
-        if (lane == 0) {
-            atomic_absmax(absmax_rot, amax_r);
-            atomic_absmax(absmax_plain, amax_p);
             if (bad) atomicOr(err, ERRF_NONFINITE);
         }
     }
@@ -411,10 +270,7 @@ template <typename InT, int FMT, int MODE, typename OutT>
 static void launch_rows_small(int logb, const InT* in, int64_t n, float norm, unsigned* amax, const float* sup,
                               uint8_t* codes, OutT* out, unsigned* err, float* sout, cudaStream_t st) {
     const unsigned blocks = grid_cap(((n + 255) / 256 + 7) / 8, 8);
-    if (logb == 8)
-        k_rows_small<InT, 8, FMT, MODE, OutT><<<blocks, 256, 0, st>>>(in, n, logb, norm, amax, sup, codes, out, err, sout);
-    else
-        k_rows_small<InT, -1, FMT, MODE, OutT><<<blocks, 256, 0, st>>>(in, n, logb, norm, amax, sup, codes, out, err, sout);
+    k_rows_small<InT, -1, FMT, MODE, OutT><<<blocks, 256, 0, st>>>(in, n, logb, norm, amax, sup, codes, out, err, sout);
 }
 
 template <typename InT, int FMT, int MODE, typename OutT>
@@ -474,20 +330,6 @@ static void rows_dispatch(int mode, int fmt, const InT* in, int64_t rows, int64_
 }
 
 // ---- left transform over rows (K2 / K4-left) ----------------------------
-template <typename InT, int FMT, int MODE>
-static void launch_cols_small(int logb, const InT* in, int64_t b, int64_t rows_pad, int64_t cols, float norm,
-                              unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr,
-                              uint8_t* cp, float* out, int64_t rows_out, unsigned* err, float* sro, float* spo,
-                              cudaStream_t st) {
-    const size_t smem = (size_t)KC_ROWS * KC_PITCH * sizeof(float);
-    const int64_t tiles = ((cols + KC_COLS - 1) / KC_COLS) * ((rows_pad + KC_ROWS - 1) / KC_ROWS);
-    const unsigned blocks = grid_cap(tiles, 3);
-    auto kern = logb == 8 ? k_cols_small<InT, 8, FMT, MODE> : k_cols_small<InT, -1, FMT, MODE>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<blocks, 256, smem, st>>>(in, b, rows_pad, cols, logb, norm, ar, ap, sr, sp, cr, cp, out, rows_out, err,
-                                    sro, spo);
-}
-
 template <typename InT>
 static void plain_dispatch(int mode, int fmt, const InT* in, int64_t n, unsigned* amax, const float* sup,
                            uint8_t* codes, unsigned* err, float* sout, cudaStream_t st) {
@@ -502,16 +344,6 @@ static void cols_dispatch(int mode, int fmt, const InT* in, int64_t b, int64_t r
                           unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp,
                           float* out, int64_t rows_out, unsigned* err, float* sro, float* spo, cudaStream_t st) {
     const float norm = hadamard_norm(B);
-    if (B <= 256) {
-        const int lb = ilog2i(B);
-#define HALO_C(F, M) launch_cols_small<InT, F, M>(lb, in, b, rows_pad, cols, norm, ar, ap, sr, sp, cr, cp, out, rows_out, err, sro, spo, st)
-        if (mode == MODE_ABSMAX) HALO_C(0, MODE_ABSMAX);
-        else if (mode == MODE_XFORM) { if constexpr (std::is_same<InT, float>::value) HALO_C(0, MODE_XFORM); }
-        else if (fmt == FMT_INT8) HALO_C(FMT_INT8, MODE_QUANT);
-        else HALO_C(FMT_E4M3, MODE_QUANT);
-#undef HALO_C
-        return;
-    }
     // large B: segments run down a column (element stride = cols); `lanes`
     // adjacent columns share a CTA.  The un-rotated E_Y path is k_plain.
     int lanes = (int)(32768 / B);
@@ -537,6 +369,10 @@ static void cols_dispatch(int mode, int fmt, const InT* in, int64_t b, int64_t r
 void run_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t B, int mode, int fmt,
               unsigned* amax, const float* sup, uint8_t* codes, void* out, int out_dtype, unsigned* err,
               float* scale_out, cudaStream_t st) {
+    // production kernels (fwht2.cu) for 8 <= B <= 256; this file keeps the
+    // generic paths for the remaining block sizes
+    if (rows_v2(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))
+        return;
     if (mode != MODE_XFORM) {
         if (in_dtype == DT_BF16) rows_quant<__nv_bfloat16>(mode, fmt, static_cast<const __nv_bfloat16*>(in), rows, cols, B, amax, sup, codes, err, scale_out, st);
         else rows_quant<float>(mode, fmt, static_cast<const float*>(in), rows, cols, B, amax, sup, codes, err, scale_out, st);
@@ -552,6 +388,9 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
               unsigned* amax_rot, unsigned* amax_plain, const float* sup_rot, const float* sup_plain,
               uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
               float* scale_rot_out, float* scale_plain_out, cudaStream_t st) {
+    if (cols_v2(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
+                codes_plain, out, rows_out, err, scale_rot_out, scale_plain_out, st))
+        return;
     if (in_dtype == DT_BF16)
         cols_dispatch<__nv_bfloat16>(mode, fmt, static_cast<const __nv_bfloat16*>(in), b, rows_pad, cols, B, amax_rot,
                                      amax_plain, sup_rot, sup_plain, codes_rot, codes_plain, out, rows_out, err,

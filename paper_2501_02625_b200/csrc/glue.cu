@@ -1,0 +1,96 @@
+// glue.cu — the elementwise glue between HALO linears in a Llama MLP block
+// (down(silu(gate(x)) * up(x))): SwiGLU forward / backward and a residual
+// add.  HBM-streaming, 16 B vector loads, grid-stride over 148 x k CTAs.
+//
+// The reference's toy block uses silu between fc1 and fc2 (model.hpp:77-96,
+// 169-171, 193-195); the Llama MLP gates it with a second projection.
+#include "common.cuh"
+#include "halo_internal.h"
+
+namespace halo_b200 {
+
+__device__ __forceinline__ float sigmoidf_(float g) { return 1.0f / (1.0f + __expf(-g)); }
+
+// H = silu(G) * U, all bf16, n % 8 == 0
+__global__ void __launch_bounds__(256) k_swiglu_fwd(const __nv_bfloat16* __restrict__ G,
+                                                    const __nv_bfloat16* __restrict__ U,
+                                                    __nv_bfloat16* __restrict__ H, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
+        float g[8], u[8], h[8];
+        load8(G + i, g);
+        load8(U + i, u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[j] = g[j] * sigmoidf_(g[j]) * u[j];
+        store8(H + i, h);
+    }
+}
+
+// dU = dH * silu(G); dG = dH * U * s * (1 + G * (1 - s)),  s = sigmoid(G)
+__global__ void __launch_bounds__(256) k_swiglu_bwd(const __nv_bfloat16* __restrict__ dH,
+                                                    const __nv_bfloat16* __restrict__ G,
+                                                    const __nv_bfloat16* __restrict__ U,
+                                                    __nv_bfloat16* __restrict__ dG, __nv_bfloat16* __restrict__ dU,
+                                                    int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
+        float dh[8], g[8], u[8], dg[8], du[8];
+        load8(dH + i, dh);
+        load8(G + i, g);
+        load8(U + i, u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float s = sigmoidf_(g[j]);
+            du[j] = dh[j] * g[j] * s;
+            dg[j] = dh[j] * u[j] * s * (1.0f + g[j] * (1.0f - s));
+        }
+        store8(dG + i, dg);
+        store8(dU + i, du);
+    }
+}
+
+// out = a + b (bf16 or fp32 elements, computed in fp32)
+template <typename T>
+__global__ void __launch_bounds__(256) k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
+                                             int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
+        float x[8], y[8];
+        load8(a + i, x);
+        load8(b + i, y);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] += y[j];
+        store8(out + i, x);
+    }
+}
+
+static unsigned ew_grid(int64_t n) {
+    int64_t want = (n / 8 + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (want > cap) want = cap;
+    if (want < 1) want = 1;
+    return (unsigned)want;
+}
+
+void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st) {
+    k_swiglu_fwd<<<ew_grid(n), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(G), static_cast<const __nv_bfloat16*>(U),
+                                              static_cast<__nv_bfloat16*>(H), n);
+}
+
+void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void* dU, int64_t n, cudaStream_t st) {
+    k_swiglu_bwd<<<ew_grid(n), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(dH), static_cast<const __nv_bfloat16*>(G),
+        static_cast<const __nv_bfloat16*>(U), static_cast<__nv_bfloat16*>(dG), static_cast<__nv_bfloat16*>(dU), n);
+}
+
+void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st) {
+    if (dtype == DT_BF16)
+        k_add<__nv_bfloat16><<<ew_grid(n), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a),
+                                                          static_cast<const __nv_bfloat16*>(b),
+                                                          static_cast<__nv_bfloat16*>(out), n);
+    else
+        k_add<float><<<ew_grid(n), 256, 0, st>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+                                                  static_cast<float*>(out), n);
+}
+
+}  // namespace halo_b200

@@ -8,7 +8,9 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/halo_b200.h"
 #include "common.cuh"
@@ -85,6 +87,59 @@ struct Buffer {
     }
 };
 
+// ---------------------------------------------------------------- profiler
+// When enabled, every kernel launch of the layer is bracketed by CUDA events
+// on its stream and tagged with its class and algorithmic work (bytes for
+// the HBM-bound kernels, int ops for the GEMM).  halo_profile_read()
+// synchronises and reduces.  Off by default: zero cost on the hot path.
+struct ProfRec {
+    int cls;
+    double work;
+    cudaEvent_t a, b;
+};
+struct Profiler {
+    bool on = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    std::mutex mu;
+    cudaEvent_t ev() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+Profiler g_prof;
+
+struct ProfScope {
+    bool active;
+    ProfRec r;
+    cudaStream_t st;
+    ProfScope(int cls, double work, cudaStream_t s) : active(g_prof.on), st(s) {
+        if (!active) return;
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        r.cls = cls;
+        r.work = work;
+        r.a = g_prof.ev();
+        r.b = g_prof.ev();
+        cudaEventRecord(r.a, st);
+    }
+    ~ProfScope() {
+        if (!active) return;
+        cudaEventRecord(r.b, st);
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.recs.push_back(r);
+    }
+};
+
+enum ProfClass { PC_K1 = 0, PC_K2 = 1, PC_GEMM = 2, PC_K4 = 3, PC_GLUE = 4 };
+
+int dt_bytes(int dt) { return dt == HALO_DTYPE_BF16 ? 2 : 4; }
+
 }  // namespace
 
 struct halo_ctx {
@@ -112,6 +167,12 @@ struct halo_linear {
     const float* qscale = nullptr;
     std::atomic<int64_t> cx{0}, cw{0}, ce{0};
 };
+
+static int prof_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+                     int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st) {
+    ProfScope ps(PC_GEMM, 2.0 * (double)M * (double)N * (double)K, st);
+    return run_gemm(fmt, A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, out, out_kind, st);
+}
 
 // ================================================================ helpers
 
@@ -211,11 +272,15 @@ extern "C" halo_status halo_scheme_from_string(const char* id, int32_t format, i
 static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows, int64_t cols, int64_t B,
                                         bool rotate, int32_t fmt, const float* supplied, uint8_t* codes,
                                         unsigned* amax_word, float* scale_out, unsigned* err, cudaStream_t st) {
+    const double n = (double)rows * (double)cols;
     if (!supplied) {
         cudaMemsetAsync(amax_word, 0, sizeof(unsigned), st);
+        ProfScope ps(PC_K1, 0.0, st);  // phase A: its bytes are booked on phase B
         if (rotate) run_rows(a, dt, rows, cols, B, 0, fmt, amax_word, nullptr, nullptr, nullptr, 0, err, nullptr, st);
         else run_plain(a, dt, rows * cols, 0, fmt, amax_word, nullptr, nullptr, err, nullptr, st);
     }
+    // algorithmic bytes of the whole op: one read of the input + the codes
+    ProfScope ps(PC_K1, n * (dt_bytes(dt) + 1), st);
     if (rotate) run_rows(a, dt, rows, cols, B, 1, fmt, amax_word, supplied, codes, nullptr, 0, err, scale_out, st);
     else run_plain(a, dt, rows * cols, 1, fmt, amax_word, supplied, codes, err, scale_out, st);
     return cuda_check("rotate_quantize");
@@ -280,8 +345,13 @@ static halo_status left_quant_impl(const void* e, int32_t dt, int64_t b, int64_t
                                    unsigned* amax_p, float* s_r, float* s_p, unsigned* err, cudaStream_t st) {
     cudaMemsetAsync(amax_r, 0, sizeof(unsigned), st);
     cudaMemsetAsync(amax_p, 0, sizeof(unsigned), st);
-    run_cols(e, dt, b, b_pad, n, B, 0, fmt, amax_r, amax_p, nullptr, nullptr, nullptr, nullptr, nullptr, 0, err,
-             nullptr, nullptr, st);
+    {
+        ProfScope ps(PC_K2, 0.0, st);
+        run_cols(e, dt, b, b_pad, n, B, 0, fmt, amax_r, amax_p, nullptr, nullptr, nullptr, nullptr, nullptr, 0, err,
+                 nullptr, nullptr, st);
+    }
+    // one read of E_Y, rotated codes (b_pad rows) and plain codes (b rows)
+    ProfScope ps(PC_K2, (double)b * n * dt_bytes(dt) + (double)b_pad * n + (codes_plain ? (double)b * n : 0.0), st);
     run_cols(e, dt, b, b_pad, n, B, 1, fmt, amax_r, amax_p, nullptr, nullptr, codes_rot, codes_plain, nullptr, 0, err,
              s_r, s_p, st);
     return cuda_check("left_rotate_quantize");
@@ -332,7 +402,7 @@ extern "C" halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_
     if (!a || !b || !out || !scale_a || !scale_b) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: null pointer");
     if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad format");
     if (out_kind < 0 || out_kind > 2) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad out kind");
-    const int r = run_gemm(format, a, b, M, N, K, a_kmajor, b_kmajor, scale_a, scale_b, out, out_kind,
+    const int r = prof_gemm(format, a, b, M, N, K, a_kmajor, b_kmajor, scale_a, scale_b, out, out_kind,
                            (cudaStream_t)stream);
     if (r == -1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: unsupported shape (strides must be multiples of 16 B)");
     if (r == -2) return fail(HALO_ERR_CUDA, "qmatmul: cuTensorMapEncodeTiled failed");
@@ -469,7 +539,7 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         if (r != HALO_OK) return r;
     }
     // Y = qmatmul(xq, wq, transpose_b=true)  (:299)
-    const int gr = run_gemm(s.format_x, c->xq.as<uint8_t>(), c->wq_codes, b, l->n, l->m, 1, 1, &d->scale[SX],
+    const int gr = prof_gemm(s.format_x, c->xq.as<uint8_t>(), c->wq_codes, b, l->n, l->m, 1, 1, &d->scale[SX],
                             c->wq_scale, y, y_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
     if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
     c->valid = true;
@@ -480,6 +550,7 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
 static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
                          cudaStream_t st) {
     // B == 1 is the identity transform with norm 1: an exact copy/convert
+    ProfScope ps(PC_K4, (double)rows * cols * (4 + dt_bytes(dtype)), st);
     run_rows(P, HALO_DTYPE_F32, rows, cols, rotate ? B : 1, 2, 0, nullptr, nullptr, nullptr, out, dtype, nullptr,
              nullptr, st);
 }
@@ -526,9 +597,10 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         l->ce += 2;
         float* P = c->scratch.as<float>();
         // prod = qmatmul(eq, wq)  (:401): B operand (n x m) is MN-major
-        int gr = run_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
+        int gr = prof_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
         if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
         // prod = transform_left(prod); take_rows(b)  (:405-409), in place
+        ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
         run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, P,
                  b, nullptr, nullptr, nullptr, st);
         // prod = transform_right_ht(prod)  (:410-411)
@@ -542,11 +614,11 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         if (s.E.right) {
             if (c->scratch.ensure((size_t)(b * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
             float* P = c->scratch.as<float>();
-            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
+            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
             finish_right(P, e_x, ex_dtype, b, m, Bm, true, st);
         } else {
-            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
+            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
                               ex_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
         }
@@ -558,11 +630,11 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         if (s.G.right) {
             if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
             float* G = c->gscratch.as<float>();
-            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], G, 0, st);
+            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], G, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
             finish_right(G, grad_w, gw_dtype, n, m, Bm, true, st);
         } else {
-            int gr = run_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], grad_w,
+            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], grad_w,
                               gw_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
         }
@@ -639,5 +711,62 @@ extern "C" halo_status halo_device_copy(void* dst, const void* src, int64_t byte
     if (bytes == 0) return HALO_OK;
     if (cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
         return fail(HALO_ERR_CUDA, "device_copy failed");
+    return HALO_OK;
+}
+
+// ============================================================ glue + profile
+
+extern "C" halo_status halo_swiglu_forward(const void* g, const void* u, void* h, int64_t n, halo_stream_t stream) {
+    if (!g || !u || !h || n < 0 || n % 8) return fail(HALO_ERR_INVALID_ARGUMENT, "swiglu_forward: bad arguments");
+    if (n == 0) return HALO_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    ProfScope ps(PC_GLUE, (double)n * 6, st);
+    run_swiglu_fwd(g, u, h, n, st);
+    return cuda_check("swiglu_forward");
+}
+
+extern "C" halo_status halo_swiglu_backward(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n,
+                                            halo_stream_t stream) {
+    if (!dh || !g || !u || !dg || !du || n < 0 || n % 8)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "swiglu_backward: bad arguments");
+    if (n == 0) return HALO_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    ProfScope ps(PC_GLUE, (double)n * 10, st);
+    run_swiglu_bwd(dh, g, u, dg, du, n, st);
+    return cuda_check("swiglu_backward");
+}
+
+extern "C" halo_status halo_add(const void* a, const void* b, void* out, int32_t dtype, int64_t n,
+                                halo_stream_t stream) {
+    if (!a || !b || !out || !valid_dtype(dtype) || n < 0 || n % 8)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "add: bad arguments");
+    if (n == 0) return HALO_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    ProfScope ps(PC_GLUE, (double)n * 3 * dt_bytes(dtype), st);
+    run_add(a, b, out, dtype, n, st);
+    return cuda_check("add");
+}
+
+extern "C" halo_status halo_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_profile_read(halo_profile* out) {
+    if (!out) return fail(HALO_ERR_INVALID_ARGUMENT, "profile_read: null");
+    std::memset(out, 0, sizeof(*out));
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(HALO_ERR_CUDA, "profile_read: device error");
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (const ProfRec& r : g_prof.recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        out->launches[r.cls] += 1;
+        out->ms[r.cls] += ms;
+        out->work[r.cls] += r.work;
+        g_prof.pool.push_back(r.a);
+        g_prof.pool.push_back(r.b);
+    }
+    g_prof.recs.clear();
     return HALO_OK;
 }

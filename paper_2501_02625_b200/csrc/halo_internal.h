@@ -35,4 +35,16 @@ void run_plain(const void* in, int in_dtype, int64_t n, int mode, int fmt, unsig
 int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
              int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st);
 
+// production K1/K2/K4 kernels for blocks <= 256 (fwht2.cu); false = not handled
+bool rows_v2(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
+             uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
+bool cols_v2(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
+             unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, float* out,
+             int64_t rows_out, unsigned* err, float* sro, float* spo, cudaStream_t st);
+
+// elementwise glue (glue.cu)
+void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);
+void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void* dU, int64_t n, cudaStream_t st);
+void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st);
+
 }  // namespace halo_b200

@@ -27,6 +27,7 @@
 
 #include <stdint.h>
 #include <math.h>
+#include <string.h>
 
 #if defined(__CUDACC__)
 #define HALO_HD __host__ __device__ __forceinline__
@@ -35,6 +36,25 @@
 #endif
 
 namespace halo_b200 {
+
+HALO_HD uint32_t f2u(float f) {
+#if defined(__CUDA_ARCH__)
+    return __float_as_uint(f);
+#else
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+#endif
+}
+HALO_HD float u2f(uint32_t u) {
+#if defined(__CUDA_ARCH__)
+    return __uint_as_float(u);
+#else
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+#endif
+}
 
 // ---------------------------------------------------------------- INT8 ----
 // quantize.hpp:154-161: nearbyint, clamp to +-127 (-128 never produced).
@@ -122,6 +142,67 @@ HALO_HD uint8_t quant_e4m3(float x, float s, float inv_s) {
     if (q > 448.0f) q = 448.0f;
     const uint8_t mag = e4m3_bits_pos(q);
     return (mag != 0 && x < 0.0f) ? (uint8_t)(mag | 0x80) : mag;
+}
+
+// ------------------------------------------------------------ fast paths --
+// Same functions, cheaper common case.  y = x * inv is within 2^-22
+// (relative) of the true quotient; when y's distance to the rounded grid
+// value is below 0.4999 steps the true quotient is strictly nearer to that
+// grid value than to any other (margin 1e-4 >> 2^-22 * 16), so the candidate
+// is the exact RNE result.  Near a midpoint (~0.02% of inputs) the exact
+// fma-checked path above decides.  Rounding to an integer uses the
+// 1.5 * 2^23 trick: y + 12582912 rounds y to nearest-even in fp32.
+constexpr float kRoundMagic = 12582912.0f;
+
+HALO_HD int8_t quant_int8_fast(float x, float s, float inv_s) {
+    const float y = x * inv_s;
+    const float t = y + kRoundMagic;
+    const float q = t - kRoundMagic;
+    if (fabsf(y - q) < 0.4999f && fabsf(q) <= 127.0f) return (int8_t)(int)q;
+    return quant_int8(x, s, inv_s);
+}
+
+HALO_HD uint8_t quant_e4m3_fast(float x, float s, float inv_s) {
+    const float a = fabsf(x);
+    const float y = a * inv_s;
+    uint8_t code;
+    if (y >= 448.0f) {
+        code = 0x7E;  // every quotient >= 448*(1-2^-22) rounds (or saturates) to 448
+    } else {
+        // binade of y (normal fp32 here), clamped to the E4M3 minimum -6
+        int e = (y >= 0.015625f) ? (int)((f2u(y) >> 23) & 0xFF) - 127 : -6;
+        const float z = y * u2f((uint32_t)(127 + 3 - e) << 23);  // exact: y / step, in [0, 16)
+        const float t = z + kRoundMagic;
+        const float qz = t - kRoundMagic;
+        if (!(fabsf(z - qz) < 0.4999f)) return quant_e4m3(x, s, inv_s);
+        code = (uint8_t)(((e + 7) << 3) + (int)qz - 8);  // also right when qz == 16 (next binade)
+    }
+    return (code != 0 && x < 0.0f) ? (uint8_t)(code | 0x80) : code;
+}
+
+// Branch-free candidates for the vectorised kernels: return the fast-path
+// code and flag inputs that need the exact path.  Kernels collect the flags
+// into a mask and take the (rare, warp-uniform) exact loop only when a flag
+// is set, which keeps the hot loop free of per-element branches.
+HALO_HD uint8_t quant_int8_try(float x, float inv_s, uint32_t& slow) {
+    const float y = x * inv_s;
+    const float t = y + kRoundMagic;
+    const float q = t - kRoundMagic;
+    slow = (uint32_t)!(fabsf(y - q) < 0.4999f && fabsf(q) <= 127.0f);
+    return (uint8_t)(f2u(t) & 0xFFu);  // two's complement low byte of the integer q
+}
+
+HALO_HD uint8_t quant_e4m3_try(float x, float inv_s, uint32_t& slow) {
+    const float a = fabsf(x);
+    const float y = a * inv_s;
+    const bool sat = y >= 448.0f;
+    const int e = (y >= 0.015625f) ? (int)((f2u(y) >> 23) & 0xFF) - 127 : -6;
+    const float z = sat ? 0.0f : y * u2f((uint32_t)(127 + 3 - e) << 23);
+    const float t = z + kRoundMagic;
+    const float qz = t - kRoundMagic;
+    slow = (uint32_t)(!sat && !(fabsf(z - qz) < 0.4999f));
+    const uint32_t code = sat ? 0x7Eu : (uint32_t)(((e + 7) << 3) + (int)qz - 8);
+    return (uint8_t)((code != 0 && x < 0.0f) ? (code | 0x80u) : code);
 }
 
 // decode for the dequantize / epilogue paths

@@ -199,9 +199,12 @@ class SavedContext:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _lib._lib is not None:
-            _lib._lib.halo_ctx_destroy(h)
-            self._h = None
+        try:
+            if h and _lib._lib is not None:
+                _lib._lib.halo_ctx_destroy(h)
+        except Exception:  # interpreter shutdown
+            pass
+        self._h = None
 
     def saved(self, layer: "HaloLinearLayer"):
         """Views of (xq, sx, wq, sw) as torch tensors (copies)."""
@@ -274,9 +277,12 @@ class HaloLinearLayer:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _lib._lib is not None:
-            _lib._lib.halo_linear_destroy(h)
-            self._h = None
+        try:
+            if h and _lib._lib is not None:
+                _lib._lib.halo_linear_destroy(h)
+        except Exception:  # interpreter shutdown
+            pass
+        self._h = None
 
     @property
     def in_features(self):

@@ -1,0 +1,72 @@
+"""Llama-3 MLP block over three HALO linears (cfg2 of BASELINE.json).
+
+    y = down( silu(gate(x)) * up(x) )
+
+The three projections are ``HaloLinearLayer`` instances (halo_linear.hpp
+semantics, HALO-0/1/2, INT8 or FP8); the SwiGLU glue and the residual-style
+add of the two input gradients are sm_100a kernels of the same library.
+This is the reference's block pattern (model.hpp:159-176: norm -> fc1 ->
+silu -> fc2, backward in reverse :179-209) with the Llama gate added.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import halo
+from ._lib import DTYPE_BF16, check, lib
+
+
+class HaloMLP:
+    def __init__(self, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor, scheme):
+        hidden, model = w_gate.shape
+        if tuple(w_up.shape) != (hidden, model) or tuple(w_down.shape) != (model, hidden):
+            raise ValueError("HaloMLP: weight shapes must be gate/up (I x H) and down (H x I)")
+        bf = torch.bfloat16
+        self.gate = halo.HaloLinearLayer(w_gate, scheme, out_dtype=bf)
+        self.up = halo.HaloLinearLayer(w_up, scheme, out_dtype=bf)
+        self.down = halo.HaloLinearLayer(w_down, scheme, out_dtype=bf)
+        self.ctx = [halo.SavedContext() for _ in range(3)]
+        self._act = None
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        g = self.gate.forward(x, self.ctx[0])
+        u = self.up.forward(x, self.ctx[1])
+        h = torch.empty_like(g)
+        check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
+        self._act = (g, u)
+        return self.down.forward(h, self.ctx[2])
+
+    def backward(self, dy: torch.Tensor, need_grad_w: bool = True):
+        """Returns (dx, (dW_gate, dW_up, dW_down))."""
+        g, u = self._act
+        bd = self.down.backward(self.ctx[2], dy, need_grad_w)
+        dg = torch.empty_like(g)
+        du = torch.empty_like(u)
+        check(lib().halo_swiglu_backward(halo._ptr(bd.e_x), halo._ptr(g), halo._ptr(u), halo._ptr(dg),
+                                         halo._ptr(du), g.numel(), halo._stream()))
+        bg = self.gate.backward(self.ctx[0], dg, need_grad_w)
+        bu = self.up.backward(self.ctx[1], du, need_grad_w)
+        dx = torch.empty_like(bg.e_x)
+        check(lib().halo_add(halo._ptr(bg.e_x), halo._ptr(bu.e_x), halo._ptr(dx), DTYPE_BF16, dx.numel(),
+                             halo._stream()))
+        return dx, (bg.grad_w, bu.grad_w, bd.grad_w)
+
+    def gemm_ops(self, tokens: int) -> float:
+        """Integer ops of the three quantized GEMM triples: 6*b*m*n each."""
+        ops = 0.0
+        for l in (self.gate, self.up, self.down):
+            ops += 6.0 * tokens * l.in_features * l.out_features
+        return ops
+
+
+def profile_enable(on: bool = True):
+    check(lib().halo_profile_enable(1 if on else 0))
+
+
+def profile_read() -> dict:
+    from ._lib import Profile
+    p = Profile()
+    check(lib().halo_profile_read(C.byref(p)))
+    return p.as_dict()

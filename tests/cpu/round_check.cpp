@@ -18,11 +18,25 @@ static void check(float x, float s, int fmt) {
     ++total;
     if (fmt == ORC_INT8) {
         const int8_t got = quant_int8(x, s, inv);
-        if ((double)got != want) { if (bad < 5) printf("int8 x=%a s=%a got %d want %g\n", x, s, got, want); ++bad; }
+        uint32_t sl;
+        int8_t fast = (int8_t)quant_int8_try(x, inv, sl);
+        if (sl) fast = quant_int8(x, s, inv);
+        if (quant_int8_fast(x, s, inv) != fast) fast = 99;
+        if ((double)got != want || (double)fast != want) {
+            if (bad < 5) printf("int8 x=%a s=%a got %d fast %d want %g\n", x, s, got, fast, want);
+            ++bad;
+        }
     } else {
         const uint8_t got = quant_e4m3(x, s, inv);
+        uint32_t sl;
+        uint8_t fast = quant_e4m3_try(x, inv, sl);
+        if (sl) fast = quant_e4m3(x, s, inv);
+        if (quant_e4m3_fast(x, s, inv) != fast) fast = 0xFF;
         float wf = (float)want; uint8_t wb; orc_codes_to_e4m3(&wf, 1, &wb);
-        if (got != wb) { if (bad < 5) printf("e4m3 x=%a s=%a got %02x want %02x (%g)\n", x, s, got, wb, want); ++bad; }
+        if (got != wb || fast != wb) {
+            if (bad < 5) printf("e4m3 x=%a s=%a got %02x fast %02x want %02x (%g)\n", x, s, got, fast, wb, want);
+            ++bad;
+        }
     }
 }
 
