@@ -54,7 +54,12 @@ static void fwht_segment(float* row, int64_t B) {
     for (int64_t j = 0; j < B; ++j) row[j] *= norm;
 }
 
+/* Only power-of-two blocks are restated (the base-12/20 Kronecker factors of
+ * hadamard.hpp:20-58 are outside this path); other sizes leave A untouched. */
+static int pow2(int64_t b) { return b > 0 && (b & (b - 1)) == 0; }
+
 void orc_fwht_rows(float* a, int64_t rows, int64_t cols, int64_t block) {
+    if (!pow2(block) || cols % block) return;
     for (int64_t r = 0; r < rows; ++r)
         for (int64_t s = 0; s < cols; s += block)
             fwht_segment(a + r * cols + s, block);
@@ -63,6 +68,7 @@ void orc_fwht_rows(float* a, int64_t rows, int64_t cols, int64_t block) {
 /* hadamard.hpp:205-216: left = transpose(right(transpose(A))).  For a
  * power-of-two block the H^T / H variants coincide (base_dim 1). */
 void orc_fwht_cols(float* a, int64_t rows, int64_t cols, int64_t block) {
+    if (!pow2(block) || rows % block) return;
     float* col = (float*)malloc(sizeof(float) * (size_t)block);
     for (int64_t s = 0; s < rows; s += block) {
         for (int64_t c = 0; c < cols; ++c) {

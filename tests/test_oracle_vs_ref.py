@@ -1,0 +1,62 @@
+"""The C restatement against the reference compiled from /root/reference
+(oracle/_ref/libhalo_ref.so): bit-exact on randomized cases.  Skipped where
+the prebuilt reference library is absent."""
+import numpy as np
+import pytest
+
+
+@pytest.fixture(scope="module")
+def O(orc):
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    return orc
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("block,b,m,n", [(0, 64, 128, 32), (32, 96, 64, 48), (16, 30, 32, 16), (0, 60, 64, 16)])
+def test_layer_bitexact(O, level, fmt, block, b, m, n):
+    seed = 1000 + 7 * level + 3 * fmt + b
+    X = O.bf16_round(O.ref_randn(b, m, seed))
+    X[:, 1] *= 40
+    W = O.bf16_round(O.ref_randn(n, m, seed + 1, 1 / np.sqrt(m)))
+    E = O.bf16_round(O.ref_randn(b, n, seed + 2, 1e-3))
+    r = O.ref_linear(level, fmt, block, X, W, E)
+    o = O.linear(level, fmt, block, X, W, E)
+    for k in ("Y", "EX", "GW", "xq", "wq"):
+        assert np.array_equal(r[k], o[k]), k
+    assert r["sx"] == o["sx"] and r["sw"] == o["sw"]
+
+
+@pytest.mark.parametrize("block", [2, 8, 64, 256, 1024])
+def test_transforms(O, block):
+    a = O.ref_randn(8, 1024, block)
+    assert np.array_equal(O.fwht_rows(a, block), O.ref_fwht_rows(a, block))
+    assert np.array_equal(O.fwht_rows(a, block), O.ref_fwht_rows(a, block, ht=True))  # H == H^T for 2^n
+    c = O.ref_randn(1024, 8, block + 1)
+    assert np.array_equal(O.fwht_cols(c, block), O.ref_fwht_cols(c, block))
+
+
+def test_round_code_random(O):
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.normal(0, 60, 20000), np.arange(-130, 130) + 0.5, rng.normal(0, 300, 20000)])
+    for fmt in (0, 1):
+        for x in xs:
+            assert O.orc().orc_round_code(float(x), fmt) == O.ref_round_code(float(x), fmt)
+
+
+def test_fsdp_gather_matches_single_process(O):
+    # test_hqfsdp.cpp:98-125 semantics: 50 random weights per world size
+    rng = np.random.default_rng(11)
+    for world in (1, 2, 4, 8):
+        for rep in range(10):
+            rows = 3 + int(rng.integers(0, 38))
+            cols = 16 if rep % 2 == 0 else 32
+            W = O.ref_randn(rows, cols, 50 * world + rep)
+            fmt = 1 if rep % 5 == 0 else 0
+            codes, scale, _ = O.ref_fsdp_gather(world, W, fmt, rep % 4 != 3)
+            padded = (rows + world - 1) // world * world
+            P = np.zeros((padded, cols), np.float32)
+            P[:rows] = W
+            want, s = O.quantize(O.fwht_rows(P, cols) if rep % 4 != 3 else P, fmt)
+            assert np.array_equal(codes, want) and scale == s[0]
