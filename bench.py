@@ -11,9 +11,11 @@ quantized GEMMs per step / step time (TOPS).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 (torchrun, one rank per GPU): every rank runs the block on its own 8192
-tokens (weak scaling); the weight gradients are reduce-scattered over NCCL
-(the HQ-FSDP gradient exchange, hqfsdp.hpp:271-300) inside the timed step.
+N > 1 (torchrun, one rank per GPU): HQ-FSDP (hqfsdp.hpp) — every rank owns a
+row shard of each weight and runs the block on its own 8192 tokens (weak
+scaling); per step the INT8 (WH)_Q codes are all-gathered for the forward,
+regathered under the saved scale for the backward, and dW is reduce-scattered,
+all over NCCL inside the timed step.
 `--impl reference` times the reference's own CPU implementation (the
 unmodified headers compiled into oracle/_ref) on a bounded sample.
 """
@@ -142,6 +144,7 @@ def main():
     ap.add_argument("--fmt", default="int8", choices=["int8", "fp8"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fsdp", action="store_true", help="HQ-FSDP path even at N=1 (always on for N>1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -166,33 +169,32 @@ def main():
 
     fmt = halo.INT8 if args.fmt == "int8" else halo.FP8_E4M3
     b = args.tokens
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    g = torch.Generator(device=dev).manual_seed(1234)  # weights: identical on every rank
     bf = torch.bfloat16
     # random-init Llama-3-8B MLP weights (std 1/sqrt(fan_in), model.hpp:146-149) and
     # synthetic activations with outlier channels
     wg = (torch.randn(INTER, HIDDEN, generator=g, device=dev) / HIDDEN ** 0.5).to(bf)
     wu = (torch.randn(INTER, HIDDEN, generator=g, device=dev) / HIDDEN ** 0.5).to(bf)
     wd = (torch.randn(HIDDEN, INTER, generator=g, device=dev) / INTER ** 0.5).to(bf)
+    g = torch.Generator(device=dev).manual_seed(4321 + rank)  # per-rank tokens
     x = torch.randn(b, HIDDEN, generator=g, device=dev)
     x[:, [2, 9, 16, 27]] *= 40
     x = x.to(bf)
     dy = (torch.randn(b, HIDDEN, generator=g, device=dev) * 1e-3).to(bf)
     scheme = halo.halo2(fmt, args.block)
-    mlp = HaloMLP(wg, wu, wd, scheme)
+    use_fsdp = world > 1 or args.fsdp
+    if use_fsdp:
+        # HQ-FSDP: weights row-sharded over the ranks, INT8 (WH)_Q gathered for
+        # the forward, regathered for the backward, dW reduce-scattered
+        from paper_2501_02625_b200.fsdp import FsdpHaloMLP
+        mlp = FsdpHaloMLP(wg, wu, wd, scheme)
+    else:
+        mlp = HaloMLP(wg, wu, wd, scheme)
     ops_step = mlp.gemm_ops(b)
-
-    # reduce-scatter buffers for the FSDP gradient exchange (N > 1)
-    def grad_exchange(grads):
-        if world == 1:
-            return
-        for gw in grads:
-            shard = torch.empty((gw.shape[0] // world, gw.shape[1]), dtype=gw.dtype, device=dev)
-            dist.reduce_scatter_tensor(shard, gw, op=dist.ReduceOp.AVG)
 
     def step(inp, grad):
         mlp.forward(inp)
-        dx, grads = mlp.backward(grad)
-        grad_exchange(grads)
+        dx, _ = mlp.backward(grad)
         return dx
 
     flush = torch.empty(int(512 * 2 ** 20) // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -303,7 +305,8 @@ def main():
             "vs_baseline": None, "dtype": "int8" if fmt == halo.INT8 else "fp8_e4m3", "data": "synthetic",
             "config": {"workload": CONFIG_NAME, "global_batch": b * world, "seq_len": None,
                        "tokens_per_gpu": b, "hadamard_block": args.block,
-                       "parallelism": f"dp{world}" + (" + NCCL reduce-scatter of dW" if world > 1 else ""),
+                       "parallelism": (f"hq-fsdp{world} (INT8 weight all-gather + regather, bf16 dW "
+                                       f"reduce-scatter over NCCL)" if use_fsdp else "single GPU"),
                        "l2": "512 MiB buffer written between timed steps (outside the step events); "
                              "per-step working set ~2 GB > 126 MB L2"},
             "tokens_per_s": world * b * args.steps / (ms / 1e3),

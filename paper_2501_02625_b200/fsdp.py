@@ -1,0 +1,288 @@
+"""HQ-FSDP (hqfsdp.hpp) on real ranks: one process per GPU, NCCL over NVLink.
+
+The reference simulates the protocol with logical ranks in one process
+(hqfsdp.hpp:3-10).  Here every rank owns a contiguous row shard of each
+linear weight (rows zero-padded to a multiple of the world size,
+hqfsdp.hpp:131-148) and the collectives are real:
+
+  forward gather   (hqfsdp.hpp:204-237)  local rotate + absmax (K1 phase A on
+                   the shard) -> all-gather of the per-rank absmax (max is
+                   order-insensitive) -> shared scale float(max/fmax) ->
+                   local quantize under that scale (K1 phase B) ->
+                   all-gather of the INT8/E4M3 codes
+  backward regather (:243-266)           same codes under the SAVED scale, no
+                   scale traffic; optional stale-weight check
+  reduce-scatter   (:271-300)            dW summed over ranks and scattered
+                   by row range, divided by the world size
+
+Because per-tensor scales are shared, the gathered codes equal a
+single-process quantization of the rotated padded weight bit for bit
+(test_hqfsdp.cpp:98-125); the gradient mean is fp32 in NCCL order instead of
+the reference's double rank-order sum (tolerance parity).
+
+The byte ledger (:36-103) is kept so the reference's compression ratios
+(INT8 gather = 0.5 x BF16) can be reported.  Device work goes through an
+``ops`` object: the default is the CUDA path of this package; the CPU
+multi-process tests inject a checker implementation.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from ._lib import HaloLogicError
+
+INT8, FP8_E4M3 = 0, 1
+_FMAX = {INT8: 127.0, FP8_E4M3: 448.0}
+K_SCALE_BYTES = 4  # hqfsdp.hpp:55
+
+
+# ------------------------------------------------------------ byte model --
+
+def code_payload_bytes(fmt: int, elems: int) -> int:
+    """hqfsdp.hpp:36-49 (INT8/FP8 one byte per code)."""
+    if fmt in (INT8, FP8_E4M3):
+        return elems
+    raise ValueError("only int8 / fp8_e4m3 payloads are on the device path")
+
+
+@dataclass
+class CollectiveStat:  # hqfsdp.hpp:57-61
+    payload: int = 0
+    transferred: int = 0
+    count: int = 0
+
+
+@dataclass
+class CommLedger:  # hqfsdp.hpp:65-79
+    gather: CollectiveStat = field(default_factory=CollectiveStat)
+    scale_reduce: CollectiveStat = field(default_factory=CollectiveStat)
+    reduce_scatter: CollectiveStat = field(default_factory=CollectiveStat)
+    bf16_gather_payload: int = 0
+    backward_gathers: int = 0
+    backward_consumers: int = 0
+
+    def record(self, c: CollectiveStat, payload: int, world: int):
+        c.payload += payload
+        c.transferred += payload * (world - 1) // world
+        c.count += 1
+
+
+@dataclass
+class CommReport:  # hqfsdp.hpp:81-103
+    gather_payload: int
+    gather_transferred: int
+    scale_reduce_payload: int
+    scale_reduce_transferred: int
+    reduce_scatter_payload: int
+    reduce_scatter_transferred: int
+    gather_ratio_vs_bf16: float
+
+
+def comm_report(ledger: CommLedger) -> CommReport:
+    ratio = ledger.gather.payload / ledger.bf16_gather_payload if ledger.bf16_gather_payload else 1.0
+    return CommReport(ledger.gather.payload, ledger.gather.transferred, ledger.scale_reduce.payload,
+                      ledger.scale_reduce.transferred, ledger.reduce_scatter.payload,
+                      ledger.reduce_scatter.transferred, ratio)
+
+
+# --------------------------------------------------------------- devices --
+
+class CudaOps:
+    """The B200 kernels (K1 phase A / phase B) behind the protocol."""
+
+    def absmax(self, a: torch.Tensor, had_block: int, rotate: bool) -> torch.Tensor:
+        from . import halo
+        return halo.rotate_absmax(a, had_block, rotate)
+
+    def quantize(self, a: torch.Tensor, had_block: int, fmt: int, scale: torch.Tensor, rotate: bool):
+        from . import halo
+        codes, _ = halo.rotate_quantize(a, had_block, fmt, scale=scale, rotate=rotate)
+        return codes
+
+
+# ------------------------------------------------------------- sharding --
+
+@dataclass
+class WorldConfig:  # hqfsdp.hpp:26-30
+    world_size: int = 1
+    shard_linear: bool = True
+    replicate_norms: bool = True
+
+
+@dataclass
+class ShardedParam:  # hqfsdp.hpp:107-120
+    master: torch.Tensor          # this rank's rows of the padded weight
+    full_rows: int
+    pad_rows: int
+    world: int
+    rank: int
+    shard_rows: int
+    cols: int
+    format: int = INT8
+    local_absmax: torch.Tensor | None = None  # one per rank, over the rotated shard
+    global_scale: torch.Tensor | None = None
+    scales_valid: bool = False
+
+
+def row_range(p: ShardedParam, rank: int):
+    """hqfsdp.hpp:122-125"""
+    return rank * p.shard_rows, (rank + 1) * p.shard_rows
+
+
+def shard(w: torch.Tensor, world: WorldConfig, fmt: int, rank: int) -> ShardedParam:
+    """hqfsdp.hpp:131-148: rows padded with zeros to a multiple of the world
+    size; rank r keeps rows [r*shard_rows, (r+1)*shard_rows)."""
+    if world.world_size < 1:
+        raise ValueError("shard: world_size must be at least 1")
+    rows, cols = w.shape
+    padded = (rows + world.world_size - 1) // world.world_size * world.world_size
+    shard_rows = padded // world.world_size
+    local = torch.zeros((shard_rows, cols), dtype=w.dtype, device=w.device)
+    lo = rank * shard_rows
+    hi = min(rows, lo + shard_rows)
+    if hi > lo:
+        local[: hi - lo] = w[lo:hi]
+    return ShardedParam(local, rows, padded - rows, world.world_size, rank, shard_rows, cols, fmt)
+
+
+def scale_from_absmax(m: torch.Tensor, fmt: int) -> torch.Tensor:
+    """hqfsdp.hpp:172-177 / quantize.hpp:234: float(double(m)/fmax), 1 if 0."""
+    s = (m.double() / _FMAX[fmt]).float()
+    return torch.where(m == 0, torch.ones_like(s), s)
+
+
+def _gather(t: torch.Tensor, group, out: torch.Tensor | None = None) -> torch.Tensor:
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    shape = (world * t.shape[0],) + tuple(t.shape[1:])
+    if out is None:
+        out = torch.empty(shape, dtype=t.dtype, device=t.device)
+    elif tuple(out.shape) != shape or out.dtype != t.dtype:
+        raise ValueError("gather: output buffer shape/dtype mismatch")
+    if world == 1:
+        out.copy_(t)
+    elif dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    else:
+        dist.all_gather(list(out.chunk(world, 0)), t.contiguous(), group=group)
+    return out
+
+
+def quantized_all_gather(p: ShardedParam, apply_hadamard: bool, ledger: CommLedger, had_block: int = 0,
+                         group=None, ops=None, out: torch.Tensor | None = None):
+    """Forward gather (hqfsdp.hpp:204-237).  Returns (codes, scale): the
+    (rows_padded x cols) codes and the shared per-tensor scale, identical on
+    every rank."""
+    ops = ops or CudaOps()
+    am = ops.absmax(p.master, had_block, apply_hadamard).reshape(1).float()
+    all_am = _gather(am, group)  # every rank's local absmax, kept (on device) for the stale check
+    p.local_absmax = all_am
+    g = all_am.max().reshape(1)
+    p.global_scale = scale_from_absmax(g, p.format)
+    p.scales_valid = True
+    ledger.record(ledger.scale_reduce, K_SCALE_BYTES, p.world)
+    return _gather_with_scale(p, apply_hadamard, ledger, had_block, group, ops, out)
+
+
+def _gather_with_scale(p, apply_hadamard, ledger, had_block, group, ops, out=None):
+    """hqfsdp.hpp:184-196: quantize the local rotated rows under the agreed
+    scale, gather the codes, book the bytes."""
+    codes = ops.quantize(p.master, had_block, p.format, p.global_scale, apply_hadamard)
+    full = _gather(codes, group, out)
+    elems = full.numel()
+    ledger.record(ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
+    ledger.bf16_gather_payload += 2 * elems
+    return full, p.global_scale
+
+
+def backward_regather(p: ShardedParam, apply_hadamard: bool, ledger: CommLedger, check_stale: bool = True,
+                      had_block: int = 0, group=None, ops=None, out: torch.Tensor | None = None):
+    """Backward gather under the saved forward scale (hqfsdp.hpp:243-266)."""
+    if not p.scales_valid:
+        raise HaloLogicError("backward_regather: no saved forward scales")
+    ops = ops or CudaOps()
+    if check_stale:
+        am = float(ops.absmax(p.master, had_block, apply_hadamard).reshape(-1)[0])
+        stale = torch.tensor([1.0 if am != float(p.local_absmax[p.rank]) else 0.0])
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            stale = stale.to(p.master.device)
+            dist.all_reduce(stale, op=dist.ReduceOp.MAX, group=group)
+        if float(stale) != 0.0:
+            raise HaloLogicError("backward_regather: saved scales are stale (weights changed since the forward gather)")
+    ledger.backward_gathers += 1
+    return _gather_with_scale(p, apply_hadamard, ledger, had_block, group, ops, out)
+
+
+def reduce_scatter_grads(grad: torch.Tensor, p: ShardedParam, ledger: CommLedger, group=None) -> torch.Tensor:
+    """hqfsdp.hpp:271-300: mean over ranks, scattered by row range.  `grad`
+    is this rank's full (rows x cols) gradient; padding rows are zero and the
+    returned shard has shard_rows rows (rows past full_rows stay zero)."""
+    if tuple(grad.shape) != (p.full_rows, p.cols):
+        raise ValueError("reduce_scatter_grads: gradient shape mismatch")
+    padded = torch.zeros((p.shard_rows * p.world, p.cols), dtype=grad.dtype, device=grad.device)
+    padded[: p.full_rows] = grad
+    out = torch.empty((p.shard_rows, p.cols), dtype=grad.dtype, device=grad.device)
+    world = p.world
+    if world == 1:
+        out.copy_(padded)
+    elif dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
+        out.div_(world)
+    else:  # gloo has no reduce_scatter: all-reduce then slice
+        dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(padded[p.rank * p.shard_rows:(p.rank + 1) * p.shard_rows])
+        out.div_(world)
+    ledger.record(ledger.reduce_scatter, 2 * padded.numel(), world)
+    return out
+
+
+class FsdpHaloMLP:
+    """Llama MLP block (mlp.HaloMLP) with HQ-FSDP weights: each rank keeps a
+    row shard of gate/up/down; every step gathers the INT8 (WH)_Q codes for
+    the forward, regathers them for the backward under the saved scale, and
+    reduce-scatters the weight gradients (the loop of hqfsdp.hpp:361-411)."""
+
+    def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16):
+        from .mlp import HaloMLP
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.fmt = scheme.format_w
+        self.block = scheme.had_block
+        self.rotate = bool(scheme.F.middle)
+        self.check_stale = check_stale
+        self.params = [shard(w, WorldConfig(self.world), self.fmt, self.rank) for w in (w_gate, w_up, w_down)]
+        self.mlp = HaloMLP(w_gate, w_up, w_down, scheme)
+        for layer in self.layers:
+            layer.grad_dtype = grad_dtype
+        code_dt = torch.int8 if self.fmt == INT8 else torch.uint8
+        self.buffers = [torch.empty((p.shard_rows * p.world, p.cols), dtype=code_dt, device=p.master.device)
+                        for p in self.params]
+        self.ledger = CommLedger()
+
+    @property
+    def layers(self):
+        return (self.mlp.gate, self.mlp.up, self.mlp.down)
+
+    def _install(self, layer, codes, scale, rows):
+        layer.set_qweight(codes[:rows], scale)
+
+    def forward(self, x):
+        for layer, p, buf in zip(self.layers, self.params, self.buffers):
+            codes, scale = quantized_all_gather(p, self.rotate, self.ledger, self.block, self.group, out=buf)
+            self._install(layer, codes, scale, p.full_rows)
+        return self.mlp.forward(x)
+
+    def backward(self, dy):
+        for layer, p, buf in zip(self.layers, self.params, self.buffers):
+            codes, scale = backward_regather(p, self.rotate, self.ledger, self.check_stale, self.block, self.group,
+                                             out=buf)
+            self.ledger.backward_consumers += 1
+        dx, grads = self.mlp.backward(dy)
+        shards = [reduce_scatter_grads(g, p, self.ledger, self.group) for g, p in zip(grads, self.params)]
+        return dx, shards
+
+    def gemm_ops(self, tokens):
+        return self.mlp.gemm_ops(tokens)
