@@ -1,0 +1,120 @@
+// halo_b200.hpp — header-only C++ object API over the C ABI (halo_b200.h),
+// restoring the reference's operator surface (halo_linear.hpp:227-462):
+//
+//   halo_b200::HaloLinearLayer layer(w, n, m, halo_b200::halo2(INT8, 256));
+//   halo_b200::SavedContext ctx;
+//   layer.forward(x, b, y, ctx, stream);                 // forward(x, ctx)
+//   layer.backward(ctx, e_y, e_x, grad_w, stream);       // backward(ctx, e_y)
+//   layer.counters();                                    // QuantCallCounters
+//
+// Tensors are device pointers (row-major, caller-owned).  Status codes are
+// rethrown as the reference's exception types: std::invalid_argument,
+// halo_b200::numeric_error (== halo::numeric_error, tensor.hpp:22-24),
+// std::logic_error, and std::runtime_error for CUDA failures.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "halo_b200.h"
+
+namespace halo_b200 {
+
+struct numeric_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(halo_status s) {
+    switch (s) {
+    case HALO_OK: return;
+    case HALO_ERR_INVALID_ARGUMENT: throw std::invalid_argument(halo_last_error());
+    case HALO_ERR_NUMERIC: throw numeric_error(halo_last_error());
+    case HALO_ERR_LOGIC: throw std::logic_error(halo_last_error());
+    default: throw std::runtime_error(std::string("halo_b200: ") + halo_last_error());
+    }
+}
+
+// halo_linear.hpp:81-152
+inline halo_scheme scheme_from_string(const std::string& id, halo_format f = HALO_FMT_INT8, int64_t had_block = 0) {
+    halo_scheme s;
+    check(halo_scheme_from_string(id.c_str(), f, had_block, &s));
+    return s;
+}
+inline halo_scheme halo0(halo_format f = HALO_FMT_INT8, int64_t had_block = 0) { return scheme_from_string("halo0", f, had_block); }
+inline halo_scheme halo1(halo_format f = HALO_FMT_INT8, int64_t had_block = 0) { return scheme_from_string("halo1", f, had_block); }
+inline halo_scheme halo2(halo_format f = HALO_FMT_INT8, int64_t had_block = 0) { return scheme_from_string("halo2", f, had_block); }
+
+inline std::string to_string(const halo_scheme& s) {  // halo_linear.hpp:154-159
+    if (s.name[0]) return s.name;
+    auto p = [](const halo_placement& q) {
+        std::string r;
+        if (q.left) r += 'L';
+        if (q.middle) r += 'M';
+        if (q.right) r += 'R';
+        return r.empty() ? std::string("O") : r;
+    };
+    return "F:" + p(s.F) + ";E:" + p(s.E) + ";G:" + p(s.G);
+}
+
+// SavedContextT (halo_linear.hpp:207-216): device-resident (XH)_Q, (WH)_Q
+class SavedContext {
+public:
+    SavedContext() { check(halo_ctx_create(&h_)); }
+    ~SavedContext() { halo_ctx_destroy(h_); }
+    SavedContext(const SavedContext&) = delete;
+    SavedContext& operator=(const SavedContext&) = delete;
+    halo_ctx* get() const { return h_; }
+    void check_numeric(halo_stream_t st = nullptr) { check(halo_ctx_check(h_, st)); }
+
+private:
+    halo_ctx* h_ = nullptr;
+};
+
+class HaloLinearLayer {
+public:
+    // HaloLinearLayerT(W, scheme), halo_linear.hpp:230-234 (W: n x m, device)
+    HaloLinearLayer(const void* w, int64_t out_features, int64_t in_features, const halo_scheme& scheme,
+                    halo_dtype w_dtype = HALO_DTYPE_BF16)
+        : n_(out_features), m_(in_features), scheme_(scheme) {
+        check(halo_linear_create(&scheme_, w, w_dtype, out_features, in_features, &h_));
+    }
+    ~HaloLinearLayer() { halo_linear_destroy(h_); }
+    HaloLinearLayer(const HaloLinearLayer&) = delete;
+    HaloLinearLayer& operator=(const HaloLinearLayer&) = delete;
+
+    int64_t in_features() const { return m_; }
+    int64_t out_features() const { return n_; }
+    const halo_scheme& scheme() const { return scheme_; }
+
+    void set_weight(const void* w, halo_dtype dt = HALO_DTYPE_BF16) { check(halo_linear_set_weight(h_, w, dt)); }
+    void set_qweight(const uint8_t* codes, const float* scale) { check(halo_linear_set_qweight(h_, codes, scale)); }
+
+    // forward(x, ctx) -> y  (halo_linear.hpp:267-303)
+    void forward(const void* x, int64_t batch, void* y, SavedContext& ctx, halo_stream_t st = nullptr,
+                 halo_dtype x_dtype = HALO_DTYPE_BF16, halo_dtype y_dtype = HALO_DTYPE_BF16) {
+        check(halo_linear_forward(h_, x, x_dtype, batch, y, y_dtype, ctx.get(), st));
+    }
+    // backward(ctx, e_y) -> {e_x, grad_w}  (halo_linear.hpp:305-439)
+    void backward(const SavedContext& ctx, const void* e_y, void* e_x, void* grad_w, halo_stream_t st = nullptr,
+                  halo_dtype e_dtype = HALO_DTYPE_BF16, halo_dtype ex_dtype = HALO_DTYPE_BF16,
+                  halo_dtype gw_dtype = HALO_DTYPE_F32) {
+        check(halo_linear_backward(h_, ctx.get(), e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, st));
+    }
+    // export_inference_weights (halo_linear.hpp:332-338)
+    void export_inference_weights(uint8_t* codes, float* scale, halo_stream_t st = nullptr) {
+        check(halo_linear_export_inference_weights(h_, codes, scale, st));
+    }
+    halo_counters counters() const {
+        halo_counters c;
+        check(halo_linear_counters(h_, &c));
+        return c;
+    }
+    void reset_counters() { check(halo_linear_reset_counters(h_)); }
+
+private:
+    int64_t n_, m_;
+    halo_scheme scheme_;
+    halo_linear* h_ = nullptr;
+};
+
+}  // namespace halo_b200
