@@ -27,6 +27,8 @@
 #include "common.cuh"
 #include "halo_internal.h"
 
+#include <type_traits>
+
 namespace halo_b200 {
 
 enum : int { V2_ABSMAX = 0, V2_QUANT = 1, V2_XFORM = 2 };
@@ -229,7 +231,7 @@ struct Raw2<float> {
 };
 
 template <typename InT, int FMT, int MODE>
-__global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64_t rows_pad, int64_t cols, int lb,
+__global__ void __launch_bounds__(256, 2) k_cols_v2(const InT* in, int64_t b, int64_t rows_pad, int64_t cols, int lb,
                                                  float norm, int fold, unsigned* amax_r, unsigned* amax_p,
                                                  const float* sup_r, const float* sup_p, uint8_t* __restrict__ codes_r,
                                                  uint8_t* __restrict__ codes_p, float* out, int64_t rows_out,
@@ -246,26 +248,28 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
     float am_r = 0.f, am_p = 0.f;
     bool ok = true;
     const int64_t ct = (cols + C_COLS - 1) / C_COLS, rt = (rows_pad + 255) / 256;
-    Raw2<InT> raw[32];
-    auto load_tile = [&](int64_t tl) {
-        const int64_t r0_ = (tl / ct) * 256, c0_ = (tl % ct) * C_COLS;
-        const int64_t gc_ = c0_ + 2 * l;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int64_t gr = r0_ + 32 * w + i;
-            if (tl < ct * rt && gc_ < cols && gr < b) raw[i].load(in + gr * cols + gc_);
-            else raw[i].zero();
-        }
-    };
-    for (int64_t tile = blockIdx.x; tile < ct * rt; tile += gridDim.x) {
-        load_tile(tile);  // 32 independent requests per thread, issued back to back
-        const int64_t r0 = (tile / ct) * 256, c0 = (tile % ct) * C_COLS;
+    // One tile = 256 rows x 64 columns.  Interior tiles (the common case:
+    // b, rows_pad multiples of 256, cols a multiple of 64) run without any
+    // bounds checks; edge tiles take the checked instantiation.
+    auto run = [&](auto edge_tag, int64_t r0, int64_t c0) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
         const int64_t gc = c0 + 2 * l;
-        const bool cok = gc < cols;
-        // ---- phase 1: rows r0 + 32w + i, stages 1..16 in registers
+        const bool cok = !EDGE || gc < cols;
+        const int64_t row1 = r0 + 32 * w;  // first phase-1 row of this warp
+        // ---- phase 1: rows row1 + i, stages 1..16 in registers
         float a[32], bb[32];
+        {
+            Raw2<InT> raw[32];
+            const InT* p = in + row1 * cols + gc;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) raw[i].get(a[i], bb[i]);
+            for (int i = 0; i < 32; ++i) {
+                if (!EDGE || (cok && row1 + i < b)) raw[i].load(p);
+                else raw[i].zero();
+                p += cols;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) raw[i].get(a[i], bb[i]);
+        }
         if constexpr (MODE == V2_ABSMAX) {
             uint32_t bad = 0;
 #pragma unroll
@@ -275,27 +279,28 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
             }
             ok = ok & (bad == 0);
         } else if constexpr (MODE == V2_QUANT) {
-            // codes of the un-rotated E_Y (the G operand).  The warp vote is
-            // outside every lane-dependent branch.
+            // codes of the un-rotated E_Y (the G operand); the warp vote is
+            // outside every lane-dependent branch
             uint32_t ma = 0, mb = 0;
-            if (codes_p && cok) {
+            if (codes_p) {
+                uint8_t* q = codes_p + row1 * cols + gc;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const int64_t gr = r0 + 32 * w + i;
                     uint32_t s1, s2;
                     const uint32_t ca = qtry<FMT>(a[i], i_p, s1);
                     const uint32_t cb2 = qtry<FMT>(bb[i], i_p, s2);
-                    if (gr < b) {
+                    if (!EDGE || (cok && row1 + i < b)) {
                         ma |= s1 << i;
                         mb |= s2 << i;
-                        *reinterpret_cast<uint16_t*>(codes_p + gr * cols + gc) = (uint16_t)(ca | (cb2 << 8));
+                        *reinterpret_cast<uint16_t*>(q) = (uint16_t)(ca | (cb2 << 8));
                     }
+                    q += cols;
                 }
             }
             if (__any_sync(0xffffffffu, (ma | mb) != 0)) {  // rare, warp-uniform exact path
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const int64_t gr = r0 + 32 * w + i;
+                    const int64_t gr = row1 + i;
                     if ((ma >> i) & 1u) codes_p[gr * cols + gc] = qexact<FMT>(a[i], s_p, i_p);
                     if ((mb >> i) & 1u) codes_p[gr * cols + gc + 1] = qexact<FMT>(bb[i], s_p, i_p);
                 }
@@ -313,18 +318,19 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
                     }
             }
         }
+        float* Tw = T + (32 * w) * C_COLS + 2 * l;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-            *reinterpret_cast<float2*>(&T[(32 * w + i) * C_COLS + 2 * l]) = make_float2(a[i], bb[i]);
+        for (int i = 0; i < 32; ++i) *reinterpret_cast<float2*>(Tw + i * C_COLS) = make_float2(a[i], bb[i]);
         __syncthreads();
         // ---- phase 2: rows r + 32k (r = 4w + g), stages 32, 64, 128
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
             const int rl = 4 * w + g;
             float x[8], y[8];
+            const float* Tr = T + rl * C_COLS + 2 * l;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const float2 f = *reinterpret_cast<const float2*>(&T[(rl + 32 * k) * C_COLS + 2 * l]);
+                const float2 f = *reinterpret_cast<const float2*>(Tr + 32 * k * C_COLS);
                 x[k] = f.x;
                 y[k] = f.y;
             }
@@ -349,6 +355,7 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
                     }
                 }
             }
+            const int64_t row2 = r0 + rl;  // phase-2 rows: row2 + 32k
             if constexpr (MODE == V2_ABSMAX) {
                 if (!done) {
 #pragma unroll
@@ -356,6 +363,7 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
                 }
             } else if constexpr (MODE == V2_QUANT) {
                 uint32_t m = 0;
+                uint8_t* q = codes_r + row2 * cols + gc;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     if (!fold) {
@@ -365,11 +373,11 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
                     uint32_t s1, s2;
                     const uint32_t cx = qtry<FMT>(x[k], i_r, s1);
                     const uint32_t cy = qtry<FMT>(y[k], i_r, s2);
-                    const int64_t gr = r0 + rl + 32 * k;
-                    if (cok && gr < rows_pad) {
+                    if (!EDGE || (cok && row2 + 32 * k < rows_pad)) {
                         m |= (s1 << k) | (s2 << (k + 8));
-                        *reinterpret_cast<uint16_t*>(codes_r + gr * cols + gc) = (uint16_t)(cx | (cy << 8));
+                        *reinterpret_cast<uint16_t*>(q) = (uint16_t)(cx | (cy << 8));
                     }
+                    q += 32 * cols;
                 }
                 if (__any_sync(0xffffffffu, m != 0)) {  // rare: exact path via scratch
                     float* S = scratch + threadIdx.x * 16;
@@ -379,22 +387,30 @@ __global__ void __launch_bounds__(256) k_cols_v2(const InT* in, int64_t b, int64
                         S[k + 8] = y[k];
                     }
                     while (m) {
-                        const int q = __ffs(m) - 1;
+                        const int qq = __ffs(m) - 1;
                         m &= m - 1;
-                        const int64_t gr = r0 + rl + 32 * (q & 7);
-                        codes_r[gr * cols + gc + (q >> 3)] = qexact<FMT>(S[q], s_r, i_r);
+                        const int64_t gr = row2 + 32 * (qq & 7);
+                        codes_r[gr * cols + gc + (qq >> 3)] = qexact<FMT>(S[qq], s_r, i_r);
                     }
                 }
             } else {
+                float* o = out + row2 * cols + gc;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const int64_t gr = r0 + rl + 32 * k;
-                    if (cok && gr < rows_out)
-                        *reinterpret_cast<float2*>(out + gr * cols + gc) = make_float2(x[k] * norm, y[k] * norm);
+                    if (!EDGE || (cok && row2 + 32 * k < rows_out))
+                        *reinterpret_cast<float2*>(o) = make_float2(x[k] * norm, y[k] * norm);
+                    o += 32 * cols;
                 }
             }
         }
         __syncthreads();
+    };
+    for (int64_t tile = blockIdx.x; tile < ct * rt; tile += gridDim.x) {
+        const int64_t r0 = (tile / ct) * 256, c0 = (tile % ct) * C_COLS;
+        const int64_t rlim = MODE == V2_XFORM ? rows_out : (b < rows_pad ? b : rows_pad);
+        const bool interior = (r0 + 256 <= rlim) && (r0 + 256 <= rows_pad) && (c0 + C_COLS <= cols);
+        if (interior) run(std::false_type{}, r0, c0);
+        else run(std::true_type{}, r0, c0);
     }
     if constexpr (MODE == V2_ABSMAX) {
         am_r = warp_max(am_r) * norm;
