@@ -1,0 +1,33 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench, ncu launch list, ncu full captures.
+# Usage (from this container):
+#   gpurun --timeout 2400 -- 'bash tools/gpu_run.sh [tests] [bench] [launches] [full]'
+# Everything lands in gpurun_out/.
+set -u
+mkdir -p gpurun_out
+what="${*:-tests bench launches full}"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt 2>&1
+nproc > gpurun_out/host.txt; lscpu | head -20 >> gpurun_out/host.txt
+for w in $what; do
+  case $w in
+    tests)
+      timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+      echo "smoke rc=$?" >> gpurun_out/smoke.log ;;
+    bench)
+      timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log ;;
+    bench_fast)
+      timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log ;;
+    launches)
+      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/launches.csv python tools/prof_step.py 2 > gpurun_out/launches.log 2>&1
+      echo "launches rc=$?" >> gpurun_out/launches.log ;;
+    full)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 3 \
+        -f -o gpurun_out/prof_gemm python tools/prof_step.py 1 > gpurun_out/prof_gemm.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_rows|k_cols' -s 0 -c 6 \
+        -f -o gpurun_out/prof_fwht python tools/prof_step.py 1 > gpurun_out/prof_fwht.log 2>&1 ;;
+  esac
+done
+echo done
