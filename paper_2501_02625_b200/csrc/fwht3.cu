@@ -1,0 +1,619 @@
+// fwht3.cu — K1 / K4-right, third generation: right (row) blockwise FWHT for
+// Hadamard blocks B = 2^LB <= 256, fused with absmax (phase A), quantize
+// (phase B) or a plain transformed store (K4-right), sm_100a.
+//
+// Arithmetic is the reference's, bit for bit (hadamard.hpp:136-177): stages
+// len = 1, 2, 4, ... in fp32 add/sub, one normalising multiply by
+// float(1/sqrt(double(B))) (folded exactly into the quantizer scale when
+// B = 4^k).  Codes follow quantize.hpp:244-280 via quant_round.cuh.
+//
+// What changed against fwht2.cu (issue-bound at ~30 thread instructions per
+// element): the block size is a template parameter (no runtime stage
+// branches) and the work is laid out for sm_100a's packed fp32 pipe:
+//   * phase 1: lane holds 32 CONTIGUOUS elements (two 256-bit loads,
+//     LDG.E.ENL2.256); stage 1 is scalar, stages 2..16 are FADD2 pairs;
+//   * one XOR-swizzled, conflict-free smem exchange (8 STS.128 + 8 LDS.128
+//     per lane) turns the 8 lanes of a 256-element segment from
+//     "block p of 32" into "chunk r of 4 contiguous elements of every block";
+//   * phase 2: stages 32..128 as FADD2 pairs across the 8 chunks;
+//   * quantize in pairs: q = RNE(x*inv) by one FFMA2 with the 1.5*2^23
+//     magic, certified by the once-rounded residual x - q*s (FFMA2;
+//     quant_round.cuh quant_int8_try_r); a running FMNMX3 of |residual|
+//     decides the rare exact path once per 32 elements (inputs within ~2^-22
+//     of a rounding midpoint), 4 contiguous codes are packed
+//     with 3 PRMT and written as one 32-bit store (8 lanes x 4 B = full
+//     32 B sectors per segment);
+//   * absmax: the last stage is skipped (max(|u+v|,|u-v|) = |u|+|v|
+//     exactly), a NaN-propagating FMNMX3 carries non-finite inputs into the
+//     absmax word (every FWHT output of a block containing Inf/NaN is
+//     non-finite), so no separate finiteness pass is needed.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "halo_internal.h"
+#include "sm100.cuh"
+
+namespace halo_b200 {
+
+namespace {
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ void bfly2(float2& a, float2& b) {
+    const float2 x = a, y = b;
+    a = add2(x, y);
+    b = sub2(x, y);
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+__device__ __forceinline__ float max3nan(float a, float b, float c) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// 32 contiguous inputs -> 16 float2 (pair k = elements 2k, 2k+1)
+template <typename InT>
+struct Load32;
+template <>
+struct Load32<__nv_bfloat16> {
+    uint32_t r[16];
+    __device__ __forceinline__ void load(const __nv_bfloat16* p, bool lo_ok, bool hi_ok) {
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+        if (lo_ok)
+            asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                         : "l"(q));
+        else
+            for (int i = 0; i < 8; ++i) r[i] = 0;
+        if (hi_ok)
+            asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                           "=r"(r[15])
+                         : "l"(q + 8));
+        else
+            for (int i = 8; i < 16; ++i) r[i] = 0;
+    }
+    __device__ __forceinline__ void get(float2 (&v)[16]) const {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = make_float2(__uint_as_float(r[k] << 16), __uint_as_float(r[k] & 0xFFFF0000u));
+    }
+};
+template <>
+struct Load32<float> {
+    float r[32];
+    __device__ __forceinline__ void ld8(const float* p, int o) {
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[o]), "=f"(r[o + 1]), "=f"(r[o + 2]), "=f"(r[o + 3]), "=f"(r[o + 4]), "=f"(r[o + 5]),
+                       "=f"(r[o + 6]), "=f"(r[o + 7])
+                     : "l"(p));
+    }
+    __device__ __forceinline__ void load(const float* p, bool lo_ok, bool hi_ok) {
+        if (lo_ok) {
+            ld8(p, 0);
+            ld8(p + 8, 8);
+        } else {
+            for (int i = 0; i < 16; ++i) r[i] = 0.f;
+        }
+        if (hi_ok) {
+            ld8(p + 16, 16);
+            ld8(p + 24, 24);
+        } else {
+            for (int i = 16; i < 32; ++i) r[i] = 0.f;
+        }
+    }
+    __device__ __forceinline__ void get(float2 (&v)[16]) const {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = make_float2(r[2 * k], r[2 * k + 1]);
+    }
+};
+
+// 4 codes (low bytes of the magic-rounded fp32 words) -> one word
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+}  // namespace
+
+template <int FMT>
+__device__ __noinline__ uint32_t exact4(float2 a, float2 b, float s, float inv) {
+    if constexpr (FMT == FMT_INT8)
+        return pack4((uint8_t)quant_int8(a.x, s, inv), (uint8_t)quant_int8(a.y, s, inv), (uint8_t)quant_int8(b.x, s, inv),
+                     (uint8_t)quant_int8(b.y, s, inv));
+    else
+        return pack4(quant_e4m3(a.x, s, inv), quant_e4m3(a.y, s, inv), quant_e4m3(b.x, s, inv), quant_e4m3(b.y, s, inv));
+}
+
+// does any of these 4 elements need the exact path?  (re-derived in the
+// rare slow branch with the same criteria as the hot loop)
+template <int FMT, bool SUP>
+__device__ __forceinline__ bool group_slow(float2 a, float2 b, float s, float inv, float h) {
+    const float x[4] = {a.x, a.y, b.x, b.y};
+    bool slow = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t sl;
+        if constexpr (FMT == FMT_INT8) (void)quant_int8_try_r(x[i], s, inv, h, sl);
+        else (void)quant_e4m3_try(x[i], inv, sl);
+        slow |= sl != 0;
+    }
+    return slow;
+}
+
+enum : int { V3_ABSMAX = 0, V3_QUANT = 1, V3_XFORM = 2 };
+
+
+// ------------------------------------------------------------------ core
+// One warp iteration = one chunk of 1024 elements = 4 segments of 256; lane
+// l = (segment k = l>>3, part p = l&7) enters with the 32 contiguous inputs
+// base + 256k + 32p + 0..31 (pair i = elements 2i, 2i+1).  B <= 32: every
+// stage runs in phase 1 and the lane owns those 32 outputs; B >= 64: the
+// exchange gives the lane chunk p (4 contiguous elements) of every 32-block
+// of its segment.
+template <int LB, int FMT, int MODE, bool SUP, typename OutT>
+struct RowsCore {
+    static constexpr bool FOLD = (LB % 2) == 0;  // norm = 2^-LB/2 folds into the scale
+    static constexpr int P1 = LB < 5 ? LB : 5;   // stages in phase 1
+    static constexpr bool X2 = LB > 5;           // phase 2 needed
+    static constexpr int P2 = X2 ? LB - 5 : 0;   // stages in phase 2
+
+    float s = 1.f, inv = 1.f, norm = 1.f, amax = 0.f;
+    float thr = 0.5f;  // slow-path threshold on the running residual maximum
+    float2 inv2, magic2, norm2, nsm2;
+
+    __device__ __forceinline__ void init(const unsigned* absmax, const float* supplied, float nrm, unsigned* err,
+                                         float* scale_out) {
+        norm = nrm;
+        if constexpr (MODE == V3_QUANT) {
+            resolve_scale(absmax, supplied, FMT, &s, &inv);
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                if (scale_out) *scale_out = s;
+                if (!SUP && (*absmax >= 0x7f800000u)) atomicOr(err, ERRF_NONFINITE);
+            }
+            if (FOLD) {
+                s = s / norm;  // exact power-of-two rescale
+                inv = inv * norm;
+            }
+        }
+        inv2 = make_float2(inv, inv);
+        magic2 = make_float2(kRoundMagic, kRoundMagic);
+        nsm2 = make_float2(-s, -s);
+        if (FMT == FMT_INT8) thr = half_margin(s);
+        norm2 = make_float2(norm, norm);
+    }
+
+    // phase 1: stages len = 1 .. min(B, 32)/2 in registers
+    __device__ __forceinline__ void phase1(float2 (&v)[16]) {
+        if constexpr (P1 >= 1) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (MODE == V3_ABSMAX && LB == 1) {
+                    amax = max3nan(amax, fabsf(v[i].x) + fabsf(v[i].y), 0.f);
+                } else {
+                    const float a = v[i].x, b = v[i].y;
+                    v[i] = make_float2(a + b, a - b);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 1; t < P1; ++t) {
+            const int h = 1 << (t - 1);  // pair-index distance for len = 2^t
+            const bool last = (MODE == V3_ABSMAX) && !X2 && (t == LB - 1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if ((i & h) == 0) {
+                    if (last) amax = max3nan(amax, fabsf(v[i].x) + fabsf(v[i + h].x), fabsf(v[i].y) + fabsf(v[i + h].y));
+                    else bfly2(v[i], v[i + h]);
+                }
+            }
+        }
+        if constexpr (MODE == V3_ABSMAX && LB == 0) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) amax = max3nan(amax, fabsf(v[i].x), fabsf(v[i].y));
+        }
+    }
+
+    // 4 contiguous outputs (a = elements 0,1; c = 2,3) -> code word; running
+    // fast-path residual maximum in dmax
+    __device__ __forceinline__ uint32_t quant4(float2& a, float2& c, float& dmax) const {
+        if (!FOLD) {
+            a = mul2(a, norm2);
+            c = mul2(c, norm2);
+        }
+        if constexpr (FMT == FMT_INT8) {
+            // candidate q = RNE(x*inv) by the magic add, certified by the
+            // once-rounded residual x - q*s (quant_int8_try_r)
+            const float2 ta = __ffma2_rn(a, inv2, magic2), tc = __ffma2_rn(c, inv2, magic2);
+            const float2 qa = sub2(ta, magic2), qc = sub2(tc, magic2);
+            const float2 ra = __ffma2_rn(qa, nsm2, a), rc = __ffma2_rn(qc, nsm2, c);
+            dmax = fmax3(fmax3(dmax, fabsf(ra.x), fabsf(ra.y)), fabsf(rc.x), fabsf(rc.y));
+            if (SUP)  // |q| <= 127 (the clamp) maps below thr, |q| >= 128 above it
+                dmax = fmaxf(dmax, fmax3(fmax3(0.f, fabsf(qa.x), fabsf(qa.y)), fabsf(qc.x), fabsf(qc.y)) *
+                                       (thr / 127.5f));
+            return pack4(__float_as_uint(ta.x), __float_as_uint(ta.y), __float_as_uint(tc.x), __float_as_uint(tc.y));
+        } else {
+            uint32_t s0, s1, s2, s3;
+            const uint32_t w = pack4(quant_e4m3_try(a.x, inv, s0), quant_e4m3_try(a.y, inv, s1),
+                                     quant_e4m3_try(c.x, inv, s2), quant_e4m3_try(c.y, inv, s3));
+            dmax = fmaxf(dmax, (float)(s0 | s1 | s2 | s3));
+            return w;
+        }
+    }
+
+    // everything after phase 1 (all 32 lanes of the warp call this together)
+    __device__ __forceinline__ void finish(float2 (&v)[16], int64_t base, int64_t n, int k, int p, float4* S,
+                                           uint8_t* __restrict__ codes, OutT* __restrict__ out) {
+        if constexpr (!X2) {
+            const int64_t e0 = base + k * 256 + p * 32;
+            if constexpr (MODE == V3_QUANT) {
+                float dmax = 0.f;
+                uint32_t wd[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) wd[q] = quant4(v[2 * q], v[2 * q + 1], dmax);
+                if (__any_sync(0xffffffffu, !(dmax < thr))) {
+                    if (!(dmax < thr)) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (group_slow<FMT, SUP>(v[2 * q], v[2 * q + 1], s, inv, thr))
+                                wd[q] = exact4<FMT>(v[2 * q], v[2 * q + 1], s, inv);
+                    }
+                }
+                if (e0 < n) {
+                    uint32_t* d = reinterpret_cast<uint32_t*>(codes + e0);
+                    if (e0 + 32 <= n) {
+                        asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(wd[0]),
+                                     "r"(wd[1]), "r"(wd[2]), "r"(wd[3]), "r"(wd[4]), "r"(wd[5]), "r"(wd[6]), "r"(wd[7])
+                                     : "memory");
+                    } else {
+                        *reinterpret_cast<uint4*>(d) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                    }
+                }
+            } else if constexpr (MODE == V3_XFORM) {
+                if (e0 < n) {
+                    const int cnt = (e0 + 32 <= n) ? 4 : 2;  // 8-element groups
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        if (g < cnt) {
+                            float2 o[4];
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) o[m] = mul2(v[4 * g + m], norm2);
+                            if constexpr (sizeof(OutT) == 4) {
+                                float4* d = reinterpret_cast<float4*>(out + e0 + 8 * g);
+                                d[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+                                d[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+                            } else {
+                                *reinterpret_cast<uint4*>(out + e0 + 8 * g) =
+                                    make_uint4(pack_bf16x2(o[0].x, o[0].y), pack_bf16x2(o[1].x, o[1].y),
+                                               pack_bf16x2(o[2].x, o[2].y), pack_bf16x2(o[3].x, o[3].y));
+                            }
+                        }
+                    }
+                }
+            }
+        } else {
+            // ---------------- exchange: (block p, chunk q) -> slot 8p + (q ^ p) of segment k
+            float4* T = S + k * 64;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                T[p * 8 + (q ^ p)] = make_float4(v[2 * q].x, v[2 * q].y, v[2 * q + 1].x, v[2 * q + 1].y);
+            __syncwarp();
+            float2 u[8][2];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const float4 f = T[b * 8 + (p ^ b)];
+                u[b][0] = make_float2(f.x, f.y);
+                u[b][1] = make_float2(f.z, f.w);
+            }
+            __syncwarp();
+            // ---------------- phase 2: len = 32 << t  <->  block-index bit t
+#pragma unroll
+            for (int t = 0; t < P2; ++t) {
+                const int h = 1 << t;
+                const bool last = (MODE == V3_ABSMAX) && (t == P2 - 1);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if ((b & h) == 0) {
+                        if (last) {
+                            amax = max3nan(amax, fabsf(u[b][0].x) + fabsf(u[b + h][0].x),
+                                           fabsf(u[b][0].y) + fabsf(u[b + h][0].y));
+                            amax = max3nan(amax, fabsf(u[b][1].x) + fabsf(u[b + h][1].x),
+                                           fabsf(u[b][1].y) + fabsf(u[b + h][1].y));
+                        } else {
+                            bfly2(u[b][0], u[b + h][0]);
+                            bfly2(u[b][1], u[b + h][1]);
+                        }
+                    }
+                }
+            }
+            // lane's outputs: elements base + 256k + 32b + 4p + 0..3
+            const int64_t e0 = base + k * 256 + 4 * p;
+            if constexpr (MODE == V3_QUANT) {
+                float dmax = 0.f;
+                uint32_t* dst = reinterpret_cast<uint32_t*>(codes + e0);
+                if (base + 1024 <= n) {  // interior chunk: no per-group bounds
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) dst[8 * b] = quant4(u[b][0], u[b][1], dmax);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const uint32_t wd = quant4(u[b][0], u[b][1], dmax);
+                        if (e0 + 32 * b < n) dst[8 * b] = wd;
+                    }
+                }
+                if (__any_sync(0xffffffffu, !(dmax < thr))) {
+                    if (!(dmax < thr)) {
+                        // rare: re-store the groups the fast path cannot certify
+#pragma unroll
+                        for (int b = 0; b < 8; ++b)
+                            if (group_slow<FMT, SUP>(u[b][0], u[b][1], s, inv, thr) && e0 + 32 * b < n)
+                                *reinterpret_cast<uint32_t*>(codes + e0 + 32 * b) = exact4<FMT>(u[b][0], u[b][1], s, inv);
+                    }
+                }
+            } else if constexpr (MODE == V3_XFORM) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if (e0 + 32 * b < n) {
+                        const float2 a = mul2(u[b][0], norm2), c = mul2(u[b][1], norm2);
+                        if constexpr (sizeof(OutT) == 4) {
+                            *reinterpret_cast<float4*>(out + e0 + 32 * b) = make_float4(a.x, a.y, c.x, c.y);
+                        } else {
+                            *reinterpret_cast<uint2*>(out + e0 + 32 * b) =
+                                make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(c.x, c.y));
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    __device__ __forceinline__ void reduce(unsigned* absmax, unsigned* err) {
+        if constexpr (MODE == V3_ABSMAX) {
+            // warp max (NaN-propagating), then the normalising multiply once:
+            // max(fl(|x| * norm)) == fl(max|x| * norm) (monotone rounding)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) amax = max3nan(amax, __shfl_xor_sync(0xffffffffu, amax, o), 0.f);
+            amax *= norm;
+            if ((threadIdx.x & 31) == 0) {
+                atomic_absmax(absmax, fabsf(amax));
+                if (!(amax <= 3.402823466e38f)) atomicOr(err, ERRF_NONFINITE);
+            }
+        }
+    }
+};
+
+// ------------------------------------------------ v3: direct 256-bit loads
+template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
+__global__ void __launch_bounds__(256) k_rows_v3(const InT* __restrict__ in, int64_t n, float norm, unsigned* absmax,
+                                                 const float* supplied, uint8_t* __restrict__ codes,
+                                                 OutT* __restrict__ out, unsigned* err, float* scale_out) {
+    __shared__ __align__(16) float4 xs[8][4 * 64];  // per warp: 4 segments x 64 float4 slots
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int k = l >> 3, p = l & 7;
+    RowsCore<LB, FMT, MODE, SUP, OutT> core;
+    core.init(absmax, supplied, norm, err, scale_out);
+    const int64_t nchunks = (n + 1023) >> 10;
+    const int64_t cstride = (int64_t)gridDim.x * 8;
+    const int lane_off = k * 256 + p * 32;
+    Load32<InT> cur, nxt;
+    auto load_chunk = [&](Load32<InT>& r, int64_t cc) {
+        const int64_t e0 = (cc << 10) + lane_off;
+        r.load(in + e0, e0 < n, e0 + 16 < n);
+    };
+    const int64_t c0 = (int64_t)blockIdx.x * 8 + w;
+    if (c0 < nchunks) load_chunk(cur, c0);
+    for (int64_t c = c0; c < nchunks; c += cstride) {
+        float2 v[16];
+        cur.get(v);
+        if (c + cstride < nchunks) load_chunk(nxt, c + cstride);
+        core.phase1(v);
+        core.finish(v, c << 10, n, k, p, xs[w], codes, out);
+        cur = nxt;
+    }
+    core.reduce(absmax, err);
+}
+
+// ------------------------------------- v4: TMA-staged (128 B swizzled) input
+// Each warp streams its chunks through a private S-deep ring of smem stages
+// filled by cp.async.bulk.tensor (one elected lane, mbarrier complete_tx), so
+// the bytes in flight do not cost registers: 4 warps/CTA x S stages x 2 KB.
+// The tensor map views the input as rows of 128 B; the 128 B swizzle makes
+// the lanes' 16 B reads conflict-free.
+template <typename InT>
+struct V4Cfg {
+    static constexpr int ROW_ELEMS = 128 / sizeof(InT);       // 64 bf16 / 32 fp32
+    static constexpr int CHUNK_ROWS = 1024 / ROW_ELEMS;       // 16 / 32
+    static constexpr int STAGE_BYTES = 1024 * sizeof(InT);    // 2 / 4 KB
+    static constexpr int STAGES = sizeof(InT) == 2 ? 4 : 3;
+    static constexpr int WARPS = 4;
+    static constexpr int XCH_BYTES = 4096;                    // exchange, per warp
+    static constexpr size_t SMEM = 1024 + (size_t)WARPS * (STAGES * STAGE_BYTES + XCH_BYTES) + WARPS * STAGES * 8;
+};
+
+template <typename InT>
+__device__ __forceinline__ void v4_read(const uint8_t* stage, int k, int p, float2 (&v)[16]) {
+    if constexpr (sizeof(InT) == 2) {
+        const int row = 4 * k + (p >> 1);
+        const uint8_t* r = stage + row * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint4 q = *reinterpret_cast<const uint4*>(r + ((((p & 1) * 4 + j) ^ (row & 7)) << 4));
+            const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+                v[4 * j + m] = make_float2(__uint_as_float(wv[m] << 16), __uint_as_float(wv[m] & 0xFFFF0000u));
+        }
+    } else {
+        const int row = 8 * k + p;
+        const uint8_t* r = stage + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 q = *reinterpret_cast<const float4*>(r + ((j ^ (row & 7)) << 4));
+            v[2 * j] = make_float2(q.x, q.y);
+            v[2 * j + 1] = make_float2(q.z, q.w);
+        }
+    }
+}
+
+template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
+__global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtensorMap tm, int64_t n, float norm,
+                                                 unsigned* absmax, const float* supplied,
+                                                 uint8_t* __restrict__ codes, OutT* __restrict__ out, unsigned* err,
+                                                 float* scale_out) {
+    using C = V4Cfg<InT>;
+    extern __shared__ uint8_t smem_raw[];
+    // 1024 B alignment for the 128 B swizzle, by pointer arithmetic on the
+    // __shared__ array so every access stays an LDS/STS (not a generic LD/ST)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int k = l >> 3, p = l & 7;
+    uint8_t* stages = smem + w * C::STAGES * C::STAGE_BYTES;
+    float4* xch = reinterpret_cast<float4*>(smem + C::WARPS * C::STAGES * C::STAGE_BYTES + w * C::XCH_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::WARPS * (C::STAGES * C::STAGE_BYTES + C::XCH_BYTES)) +
+                     w * C::STAGES;
+
+    const int64_t nchunks = (n + 1023) >> 10;
+    const int64_t G = (int64_t)gridDim.x * C::WARPS;
+    const int64_t c0 = (int64_t)blockIdx.x * C::WARPS + w;
+    if (l == 0) {
+        if (w == 0) tma_prefetch_desc(&tm);
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < C::STAGES; ++s) {
+            const int64_t c = c0 + s * G;
+            if (c < nchunks) {
+                mbar_expect_tx(&bars[s], C::STAGE_BYTES);
+                tma_load_2d(stages + s * C::STAGE_BYTES, &tm, &bars[s], 0, (int)(c * C::CHUNK_ROWS));
+            }
+        }
+    }
+    __syncwarp();
+    RowsCore<LB, FMT, MODE, SUP, OutT> core;
+    core.init(absmax, supplied, norm, err, scale_out);
+    int i = 0;
+    for (int64_t c = c0; c < nchunks; c += G, ++i) {
+        const int s = i % C::STAGES;
+        mbar_wait(&bars[s], (uint32_t)(i / C::STAGES) & 1u);
+        float2 v[16];
+        v4_read<InT>(stages + s * C::STAGE_BYTES, k, p, v);
+        core.phase1(v);  // consumes every loaded value: the stage's reads are complete
+        __syncwarp();
+        if (l == 0) {
+            const int64_t cn = c + C::STAGES * G;
+            if (cn < nchunks) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&bars[s], C::STAGE_BYTES);
+                tma_load_2d(stages + s * C::STAGE_BYTES, &tm, &bars[s], 0, (int)(cn * C::CHUNK_ROWS));
+            }
+        }
+        core.finish(v, c << 10, n, k, p, xch, codes, out);
+    }
+    core.reduce(absmax, err);
+}
+
+// ============================================================ launcher
+
+namespace {
+
+template <typename K>
+unsigned v3_grid(K kern, int64_t n) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int64_t want = ((n + 1023) / 1024 + 7) / 8;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    if (want > cap) want = cap;
+    if (want < 1) want = 1;
+    return (unsigned)want;
+}
+
+}  // namespace
+
+int k1_version() {
+    static const int ver = [] {
+        const char* e = getenv("HALO_K1_VERSION");
+        return e ? atoi(e) : 4;
+    }();
+    return ver;
+}
+
+namespace {
+
+template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
+void launch_v3(const InT* in, int64_t n, unsigned* amax, const float* sup, uint8_t* codes, OutT* out, unsigned* err,
+               float* sout, cudaStream_t st) {
+    const float norm = hadamard_norm(int64_t(1) << LB);
+    using C = V4Cfg<InT>;
+    if (k1_version() >= 4 && n % C::ROW_ELEMS == 0 && (uintptr_t)in % 16 == 0) {
+        CUtensorMap tm;
+        if (encode_2d_sw128(&tm, sizeof(InT) == 4 ? 0 : 1, in, C::ROW_ELEMS, n / C::ROW_ELEMS, C::CHUNK_ROWS)) {
+            auto kern = k_rows_v4<LB, InT, FMT, MODE, SUP, OutT>;
+            static int per_sm = 0;
+            if (!per_sm) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C::WARPS, C::SMEM);
+                if (per_sm < 1) per_sm = 1;
+            }
+            int64_t want = ((n + 1023) / 1024 + C::WARPS - 1) / C::WARPS;
+            const int64_t cap = (int64_t)num_sms() * per_sm;
+            if (want > cap) want = cap;
+            kern<<<(unsigned)(want < 1 ? 1 : want), 32 * C::WARPS, C::SMEM, st>>>(tm, n, norm, amax, sup, codes, out,
+                                                                              err, sout);
+            return;
+        }
+    }
+    auto kern = k_rows_v3<LB, InT, FMT, MODE, SUP, OutT>;
+    kern<<<v3_grid(kern, n), 256, 0, st>>>(in, n, norm, amax, sup, codes, out, err, sout);
+}
+
+template <int LB>
+void dispatch_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, unsigned* amax, const float* sup,
+                 uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
+    using bf = __nv_bfloat16;
+    if (mode == V3_XFORM) {
+        const float* p = static_cast<const float*>(in);
+        if (out_dtype == DT_BF16) launch_v3<LB, float, 0, V3_XFORM, false, bf>(p, n, amax, sup, codes, static_cast<bf*>(out), err, sout, st);
+        else launch_v3<LB, float, 0, V3_XFORM, false, float>(p, n, amax, sup, codes, static_cast<float*>(out), err, sout, st);
+        return;
+    }
+#define HALO_V3(T)                                                                                                       \
+    {                                                                                                                    \
+        auto p = static_cast<const T*>(in);                                                                              \
+        if (mode == V3_ABSMAX) launch_v3<LB, T, 0, V3_ABSMAX, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st); \
+        else if (fmt == FMT_INT8) {                                                                                      \
+            if (sup) launch_v3<LB, T, FMT_INT8, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);  \
+            else launch_v3<LB, T, FMT_INT8, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);     \
+        } else {                                                                                                         \
+            if (sup) launch_v3<LB, T, FMT_E4M3, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);  \
+            else launch_v3<LB, T, FMT_E4M3, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);     \
+        }                                                                                                                \
+    }
+    if (in_dtype == DT_BF16) HALO_V3(bf) else HALO_V3(float)
+#undef HALO_V3
+}
+
+}  // namespace
+
+// B = 2^lb with lb in [0, 8]; n a multiple of 16 (and of B).
+bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
+             uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
+    if (n % 16 || B < 1 || B > 256 || (B & (B - 1))) return false;
+    if (mode == V3_XFORM && in_dtype != DT_F32) return false;
+    int lb = 0;
+    while ((int64_t(1) << lb) < B) ++lb;
+    switch (lb) {
+    case 0: dispatch_v3<0>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 1: dispatch_v3<1>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 2: dispatch_v3<2>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 3: dispatch_v3<3>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 4: dispatch_v3<4>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 5: dispatch_v3<5>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 6: dispatch_v3<6>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 7: dispatch_v3<7>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    default: dispatch_v3<8>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    }
+    return true;
+}
+
+}  // namespace halo_b200

@@ -25,6 +25,8 @@
 // The production kernels for 8 <= B <= 256 (rows) and B <= 256 (columns)
 // live in fwht2.cu; this file keeps the warp-shuffle row kernel for B < 8
 // and a CTA-per-segment shared-memory kernel for B > 256 (parity / sweep).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "halo_internal.h"
 
@@ -369,8 +371,15 @@ static void cols_dispatch(int mode, int fmt, const InT* in, int64_t b, int64_t r
 void run_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t B, int mode, int fmt,
               unsigned* amax, const float* sup, uint8_t* codes, void* out, int out_dtype, unsigned* err,
               float* scale_out, cudaStream_t st) {
-    // production kernels (fwht2.cu) for 8 <= B <= 256; this file keeps the
-    // generic paths for the remaining block sizes
+    // production kernels: fwht3.cu (B <= 256; TMA-staged v4, or v3 with
+    // direct loads), then fwht2.cu (8 <= B <= 256); this file keeps the
+    // generic paths for the remaining block sizes.  HALO_K1_VERSION=2 / 3
+    // pins an older kernel (A/B measurements).
+    const int ver = k1_version();
+    const bool aligned = ((uintptr_t)in % 32 == 0) && ((uintptr_t)codes % 32 == 0) && ((uintptr_t)out % 16 == 0);
+    if (ver >= 3 && aligned &&
+        rows_v3(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))
+        return;
     if (rows_v2(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))
         return;
     if (mode != MODE_XFORM) {
@@ -388,6 +397,10 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
               unsigned* amax_rot, unsigned* amax_plain, const float* sup_rot, const float* sup_plain,
               uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
               float* scale_rot_out, float* scale_plain_out, cudaStream_t st) {
+    if (mode != MODE_XFORM && k1_version() >= 3 &&
+        cols_v3(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
+                codes_plain, err, scale_rot_out, scale_plain_out, st))
+        return;
     if (cols_v2(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
                 codes_plain, out, rows_out, err, scale_rot_out, scale_plain_out, st))
         return;

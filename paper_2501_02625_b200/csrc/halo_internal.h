@@ -2,6 +2,7 @@
 // (halo_capi.cpp) and the kernels (fwht_quant.cu, gemm_sm100.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,6 +42,22 @@ bool rows_v2(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
 bool cols_v2(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
              unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, float* out,
              int64_t rows_out, unsigned* err, float* sro, float* spo, cudaStream_t st);
+
+// 2-D 128B-swizzled TMA descriptor (gemm_sm100.cu); dtype 0 f32, 1 bf16, 2 u8
+bool encode_2d_sw128(CUtensorMap* map, int dtype, const void* base, uint64_t inner, uint64_t outer,
+                     uint32_t box_outer);
+
+// K1 kernel generation (HALO_K1_VERSION, default 4)
+int k1_version();
+
+// third-generation K1 / K4-right (fwht3.cu): B = 2^k <= 256, FADD2 butterflies
+bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
+             uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
+
+// third-generation K2 (fwht_cols3.cu): absmax / quantize, B = 2^k <= 256
+bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
+             unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
+             float* sro, float* spo, cudaStream_t st);
 
 // elementwise glue (glue.cu)
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);

@@ -145,20 +145,29 @@ HALO_HD uint8_t quant_e4m3(float x, float s, float inv_s) {
 }
 
 // ------------------------------------------------------------ fast paths --
-// Same functions, cheaper common case.  y = x * inv is within 2^-22
-// (relative) of the true quotient; when y's distance to the rounded grid
-// value is below 0.4999 steps the true quotient is strictly nearer to that
-// grid value than to any other (margin 1e-4 >> 2^-22 * 16), so the candidate
-// is the exact RNE result.  Near a midpoint (~0.02% of inputs) the exact
-// fma-checked path above decides.  Rounding to an integer uses the
+// Same functions, cheaper common case: when y = x * inv sits closer than
+// kFastMargin (below) to the rounded grid value, the true quotient is
+// strictly nearer to that grid value than to any other, so the candidate is
+// the exact RNE result.  Near a midpoint the exact fma-checked path above
+// decides.  Rounding to an integer uses the
 // 1.5 * 2^23 trick: y + 12582912 rounds y to nearest-even in fp32.
 constexpr float kRoundMagic = 12582912.0f;
+
+// Fast-path acceptance margin, in grid steps.  The candidate q is certified
+// when |y - q| < kFastMargin.  Error budget of y against the true quotient
+// Q = x/s (|Q| <= 127.5 for INT8, the scaled E4M3 mantissa z < 16): inv =
+// RN(1/s) contributes |Q| * 2^-24 <= 7.6e-6, the rounding of y = RN(x*inv)
+// (absent when ptxas contracts it into an FFMA) another 7.6e-6 and the
+// residual y - q 2^-25; 0.5 - 0.49998 = 2e-5 covers the sum, so |Q - q| < 0.5
+// and q = RNE(Q).  Inputs within 2e-5 steps of a midpoint (4e-5 of them)
+// take the exact fma-checked path.
+constexpr float kFastMargin = 0.49998f;
 
 HALO_HD int8_t quant_int8_fast(float x, float s, float inv_s) {
     const float y = x * inv_s;
     const float t = y + kRoundMagic;
     const float q = t - kRoundMagic;
-    if (fabsf(y - q) < 0.4999f && fabsf(q) <= 127.0f) return (int8_t)(int)q;
+    if (fabsf(y - q) < kFastMargin && fabsf(q) <= 127.0f) return (int8_t)(int)q;
     return quant_int8(x, s, inv_s);
 }
 
@@ -174,7 +183,7 @@ HALO_HD uint8_t quant_e4m3_fast(float x, float s, float inv_s) {
         const float z = y * u2f((uint32_t)(127 + 3 - e) << 23);  // exact: y / step, in [0, 16)
         const float t = z + kRoundMagic;
         const float qz = t - kRoundMagic;
-        if (!(fabsf(z - qz) < 0.4999f)) return quant_e4m3(x, s, inv_s);
+        if (!(fabsf(z - qz) < kFastMargin)) return quant_e4m3(x, s, inv_s);
         code = (uint8_t)(((e + 7) << 3) + (int)qz - 8);  // also right when qz == 16 (next binade)
     }
     return (code != 0 && x < 0.0f) ? (uint8_t)(code | 0x80) : code;
@@ -188,7 +197,7 @@ HALO_HD uint8_t quant_int8_try(float x, float inv_s, uint32_t& slow) {
     const float y = x * inv_s;
     const float t = y + kRoundMagic;
     const float q = t - kRoundMagic;
-    slow = (uint32_t)!(fabsf(y - q) < 0.4999f && fabsf(q) <= 127.0f);
+    slow = (uint32_t)!(fabsf(y - q) < kFastMargin && fabsf(q) <= 127.0f);
     return (uint8_t)(f2u(t) & 0xFFu);  // two's complement low byte of the integer q
 }
 
@@ -200,9 +209,26 @@ HALO_HD uint8_t quant_e4m3_try(float x, float inv_s, uint32_t& slow) {
     const float z = sat ? 0.0f : y * u2f((uint32_t)(127 + 3 - e) << 23);
     const float t = z + kRoundMagic;
     const float qz = t - kRoundMagic;
-    slow = (uint32_t)(!sat && !(fabsf(z - qz) < 0.4999f));
+    slow = (uint32_t)(!sat && !(fabsf(z - qz) < kFastMargin));
     const uint32_t code = sat ? 0x7Eu : (uint32_t)(((e + 7) << 3) + (int)qz - 8);
     return (uint8_t)((code != 0 && x < 0.0f) ? (code | 0x80u) : code);
+}
+
+// Residual-certified INT8 candidate (the vectorised kernels' fast path).
+// q is any integer near x/s (here RNE of x*inv, however y was rounded); the
+// residual r = fma(-q, s, x) is x - q*s rounded once, so |r| < h with
+// h = half_margin(s) = RN(0.5 * s * (1 - 2^-22)) proves |x - q*s| < s/2,
+// i.e. q = RNE(x/s) with no tie.  Only inputs within ~2^-22 of a midpoint
+// (plus |q| > 127, which needs the clamp) fall to the exact path: ~100x
+// fewer than the |y - q| < kFastMargin test above.
+HALO_HD float half_margin(float s) { return (0.5f * s) * (1.0f - 2.384185791015625e-07f); }
+
+HALO_HD uint8_t quant_int8_try_r(float x, float s, float inv_s, float h, uint32_t& slow) {
+    const float t = x * inv_s + kRoundMagic;
+    const float q = t - kRoundMagic;
+    const float r = fmaf(-q, s, x);
+    slow = (uint32_t)!(fabsf(r) < h && fabsf(q) <= 127.0f);
+    return (uint8_t)(f2u(t) & 0xFFu);
 }
 
 // decode for the dequantize / epilogue paths

@@ -22,6 +22,10 @@ static void check(float x, float s, int fmt) {
         int8_t fast = (int8_t)quant_int8_try(x, inv, sl);
         if (sl) fast = quant_int8(x, s, inv);
         if (quant_int8_fast(x, s, inv) != fast) fast = 99;
+        uint32_t sr;
+        int8_t fr = (int8_t)quant_int8_try_r(x, s, inv, half_margin(s), sr);
+        if (sr) fr = quant_int8(x, s, inv);
+        if (fr != fast) fast = 98;
         if ((double)got != want || (double)fast != want) {
             if (bad < 5) printf("int8 x=%a s=%a got %d fast %d want %g\n", x, s, got, fast, want);
             ++bad;

@@ -1,0 +1,91 @@
+"""Kernel microbenchmarks (cfg2 shapes): K1 rotate+quantize (phase A + B),
+K2 left rotate+quantize, K4 transforms, K3 GEMMs.  CUDA events on the
+launching stream, L2 flushed (512 MiB write) before every timed launch,
+median of N.  Prints one JSON line per op.
+
+  python tools/bench_kernels.py [k1 k2 k4 gemm] [--reps 10]
+"""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2501_02625_b200 import halo  # noqa: E402
+
+reps = 10
+args = [a for a in sys.argv[1:]]
+if "--reps" in args:
+    i = args.index("--reps")
+    reps = int(args[i + 1])
+    del args[i:i + 2]
+what = set(args or ["k1", "k2", "k4", "gemm"])
+dev = torch.device("cuda", 0)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "MEASURED_PEAKS.json"))) if os.path.exists("MEASURED_PEAKS.json") else {}
+hbm = peaks.get("hbm_gbs", 6650.0)
+
+
+def timeit(fn, nbytes=None, ops=None, name="", warm=3, **extra):
+    for _ in range(warm):
+        fn()
+    ts = []
+    st = torch.cuda.current_stream()
+    for _ in range(reps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    rec = {"op": name, "ms": round(ms, 4), **extra}
+    if nbytes:
+        rec["GBps"] = round(nbytes / ms / 1e6, 1)
+        rec["frac_hbm"] = round(nbytes / ms / 1e6 / hbm, 3)
+    if ops:
+        rec["TOPS"] = round(ops / ms / 1e9, 1)
+    print(json.dumps(rec), flush=True)
+    return ms
+
+
+g = torch.Generator(device=dev).manual_seed(0)
+bf = torch.bfloat16
+B = 256
+shapes = {"X": (8192, 4096), "W_gate": (14336, 4096), "W_down": (4096, 14336), "H": (8192, 14336)}
+if "k1" in what:
+    for nm, (r, c) in shapes.items():
+        a = torch.randn(r, c, generator=g, device=dev).to(bf)
+        n = r * c
+        timeit(lambda: halo.rotate_absmax(a, B), nbytes=2 * n, name=f"k1_absmax[{nm} {r}x{c}]")
+        timeit(lambda: halo.rotate_quantize(a, B), nbytes=3 * n, name=f"k1_quant_AB[{nm} {r}x{c}]",
+               note="bytes counted: one bf16 read + int8 write (algorithmic)")
+        del a
+if "k2" in what:
+    for nm, (r, c) in {"dY": (8192, 4096), "dG": (8192, 14336)}.items():
+        e = (torch.randn(r, c, generator=g, device=dev) * 1e-3).to(bf)
+        n = r * c
+        timeit(lambda: halo.left_rotate_quantize(e, B), nbytes=4 * n, name=f"k2_left_quant_AB[{nm} {r}x{c}]")
+        del e
+if "k4" in what:
+    for nm, (r, c) in {"dX_gate": (8192, 4096), "dX_down": (8192, 14336), "dW": (14336, 4096)}.items():
+        p = torch.randn(r, c, generator=g, device=dev)
+        n = r * c
+        timeit(lambda: halo.transform_right(p, B, out_dtype=bf), nbytes=6 * n, name=f"k4_right_bf16[{nm} {r}x{c}]")
+        timeit(lambda: halo.transform_left(p, B), nbytes=8 * n, name=f"k4_left_f32[{nm} {r}x{c}]")
+        del p
+if "gemm" in what:
+    b, H, I = 8192, 4096, 14336
+    one = torch.ones(1, device=dev)
+    xq = torch.randint(-127, 128, (b, H), dtype=torch.int8, device=dev, generator=g)
+    wq = torch.randint(-127, 128, (I, H), dtype=torch.int8, device=dev, generator=g)
+    eq = torch.randint(-127, 128, (b, I), dtype=torch.int8, device=dev, generator=g)
+    timeit(lambda: halo.qmatmul(xq, wq, one, one, out="bf16"), ops=2 * b * H * I, name="gemm_F[8192x14336x4096 NT bf16]")
+    timeit(lambda: halo.qmatmul(eq, wq, one, one, b_kmajor=False, out="f32"), ops=2 * b * H * I,
+           name="gemm_E[8192x4096x14336 K/MN f32]")
+    timeit(lambda: halo.qmatmul(eq, xq, one, one, a_kmajor=False, b_kmajor=False, out="f32"), ops=2 * b * H * I,
+           name="gemm_G[14336x4096x8192 MN/MN f32]")

@@ -19,6 +19,16 @@ for w in $what; do
       timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log ;;
     bench_fast)
       timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log ;;
+    kern)
+      timeout 600 python tools/bench_kernels.py > gpurun_out/kern.log 2>&1; echo "kern rc=$?" >> gpurun_out/kern.log ;;
+    kern_v2)
+      HALO_K1_VERSION=2 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/kern_v2.log 2>&1 ;;
+    prof_k1)
+      timeout 600 ncu --set full --clock-control none -k regex:k_rows_v -s 4 -c 2 \
+        -f -o gpurun_out/prof_k1 python tools/bench_kernels.py k1 --reps 1 > gpurun_out/prof_k1.log 2>&1 ;;
+    prof_k2)
+      timeout 600 ncu --set full --clock-control none -k regex:k_cols_v -s 8 -c 2 \
+        -f -o gpurun_out/prof_k2 python tools/bench_kernels.py k2 --reps 1 > gpurun_out/prof_k2.log 2>&1 ;;
     launches)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python tools/prof_step.py 2 > gpurun_out/launches.log 2>&1
@@ -29,5 +39,11 @@ for w in $what; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_rows|k_cols' -s 0 -c 6 \
         -f -o gpurun_out/prof_fwht python tools/prof_step.py 1 > gpurun_out/prof_fwht.log 2>&1 ;;
   esac
+done
+# keep reps small enough to travel back (64 MiB cap): export raw CSV, drop big reps
+for r in gpurun_out/*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  if [ $(stat -c %s "$r") -gt 25000000 ]; then rm -f "$r"; fi
 done
 echo done
