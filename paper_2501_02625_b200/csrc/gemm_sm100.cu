@@ -55,6 +55,15 @@ struct GemmArgs {
     const float* sa;
     const float* sb;
     void* out;
+    // fused epilogue Hadamard (K4): blockwise FWHT of block 2^xf_lb along N
+    // (the tile's 256 columns hold whole blocks), reference stage order, then
+    // one multiply by xf_norm.  0 = none.
+    int xf_lb;
+    float xf_norm;
+    // transposed store: out is [n_valid][M] row-major (C^T), rows >= n_valid
+    // of C^T (N-index) are dropped (take_rows after the left transform)
+    int out_trans;
+    int n_valid;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -91,6 +100,78 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+        "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+        "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void ep_bfly(float& a, float& b) {
+    const float x = a, y = b;
+    a = x + y;
+    b = x - y;
+}
+__device__ __forceinline__ void ep_bfly2(float& a0, float& a1, float& b0, float& b1) {
+    const float2 x = make_float2(a0, a1), y = make_float2(b0, b1);
+    const float2 s = __fadd2_rn(x, y), d = __fadd2_rn(x, make_float2(-y.x, -y.y));
+    a0 = s.x;
+    a1 = s.y;
+    b0 = d.x;
+    b1 = d.y;
+}
+
+// store 8 consecutive N-columns (col0..col0+7) of one C row
+__device__ __forceinline__ void ep_store8(const GemmArgs& p, int row, int col0, const float (&v)[8]) {
+    if (!p.out_trans) {
+        if (row >= p.M || col0 >= p.N) return;
+        if (p.out_kind == 0) {
+            float* o = static_cast<float*>(p.out) + (int64_t)row * p.N + col0;
+            if (col0 + 8 <= p.N && (p.N % 4) == 0) {
+                reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(o)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            } else {
+                
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (col0 + j < p.N) o[j] = v[j];
+            }
+        } else {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.N + col0;
+            if (col0 + 8 <= p.N && (p.N % 8) == 0) store8(o, v);
+            else
+                {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (col0 + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+            }
+        }
+    } else {
+        // C^T[col][row]: consecutive lanes = consecutive rows -> 128 B per store
+        if (row >= p.M) return;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = col0 + j;
+            if (c < p.n_valid) {
+                if (p.out_kind == 0) static_cast<float*>(p.out)[(int64_t)c * p.M + row] = v[j];
+                else static_cast<__nv_bfloat16*>(p.out)[(int64_t)c * p.M + row] = __float2bfloat16_rn(v[j]);
+            }
+        }
+    }
 }
 
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
@@ -243,6 +324,86 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tc_fence_after();
             const int row = mb * BM + ew * 32 + lane;
             const bool row_ok = row < p.M;
+            const uint32_t tacc = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+            if (p.xf_lb > 0) {
+                // ---- fused FWHT along N (hadamard.hpp:136-177 order): pass 1
+                // runs stages len = 1..16 on each 32-column chunk and parks the
+                // fp32 result back in TMEM; pass 2 gathers 8 columns from each
+                // chunk (tcgen05.ld x8) for stages len = 32, 64, 128.
+                const int B = 1 << p.xf_lb;
+                const bool two_pass = B > 32;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tacc + c * 32, r);
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if constexpr (FMT == FMT_INT8) v[j] = (float)((double)(int32_t)r[j] * ss);
+                        else v[j] = __uint_as_float(r[j]) * ssf;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) ep_bfly(v[j], v[j + 1]);  // len 1 (B >= 2)
+#pragma unroll
+                    for (int t = 1; t < 5; ++t) {
+                        const int len = 1 << t;
+                        if (len < B) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 2)
+                                if ((j & len) == 0) ep_bfly2(v[j], v[j + 1], v[j + len], v[j + len + 1]);
+                        }
+                    }
+                    if (two_pass) {
+                        tmem_st32(tacc + c * 32, v);
+                    } else {
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            float o[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) o[j] = v[8 * g + j] * p.xf_norm;
+                            ep_store8(p, row, nb * BN + c * 32 + 8 * g, o);
+                        }
+                    }
+                }
+                if (two_pass) {
+                    tmem_wait_st();
+#pragma unroll 1
+                    for (int g = 0; g < 4; ++g) {
+                        float u[8][8];
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            uint32_t r[8];
+                            tmem_ld8(tacc + c * 32 + g * 8, r);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) u[c][j] = __uint_as_float(r[j]);
+                        }
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) {
+                            const int h = 1 << t;
+                            if ((32 << t) < B) {
+#pragma unroll
+                                for (int c = 0; c < 8; ++c)
+                                    if ((c & h) == 0)
+#pragma unroll
+                                        for (int j = 0; j < 8; j += 2)
+                                            ep_bfly2(u[c][j], u[c][j + 1], u[c + h][j], u[c + h][j + 1]);
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            float o[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) o[j] = u[c][j] * p.xf_norm;
+                            ep_store8(p, row, nb * BN + c * 32 + 8 * g, o);
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                continue;
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
@@ -257,7 +418,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         for (int j = 0; j < 32; j += 4)
                             *reinterpret_cast<int4*>(o + j) = make_int4(r[j], r[j + 1], r[j + 2], r[j + 3]);
                     } else {
-                        for (int j = 0; j < 32 && col0 + j < p.N; ++j) o[j] = (int32_t)r[j];
+                        
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) o[j] = (int32_t)r[j];
                     }
                     continue;
                 }
@@ -274,7 +438,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         for (int j = 0; j < 32; j += 4)
                             *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     } else {
-                        for (int j = 0; j < 32 && col0 + j < p.N; ++j) o[j] = v[j];
+                        
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) o[j] = v[j];
                     }
                 } else {
                     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.N + col0;
@@ -282,7 +449,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < 32; j += 8) store8(o + j, v + j);
                     } else {
-                        for (int j = 0; j < 32 && col0 + j < p.N; ++j) o[j] = __float2bfloat16_rn(v[j]);
+                        
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
                     }
                 }
             }
@@ -353,6 +523,14 @@ static bool encode_map(CUtensorMap* map, const void* base, uint64_t inner, uint6
 
 int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
              int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st) {
+    return run_gemm_x(fmt, A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, out, out_kind, 0, 1.0f, 0, N, st);
+}
+
+int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+               int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int xf_lb, float xf_norm,
+               int out_trans, int64_t n_valid, cudaStream_t st) {
+    if (xf_lb < 0 || xf_lb > 8) return -1;  // the 256-column tile must hold whole blocks
+    if ((xf_lb > 0 || out_trans) && out_kind == 2) return -1;
     if (M <= 0 || N <= 0 || K <= 0) return -1;
     if (M > INT32_MAX / 2 || N > INT32_MAX / 2 || K > INT32_MAX / 2) return -1;
     // TMA: global strides must be multiples of 16 bytes
@@ -362,7 +540,8 @@ int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, 
     const bool ok_a = a_kmajor ? encode_map(&ma, A, K, M, BM) : encode_map(&ma, A, M, K, BK);
     const bool ok_b = b_kmajor ? encode_map(&mb, B, K, N, BN) : encode_map(&mb, B, N, K, BK);
     if (!ok_a || !ok_b) return -2;
-    GemmArgs args{(int)M, (int)N, (int)K, a_kmajor, b_kmajor, fmt, out_kind, sa, sb, out};
+    GemmArgs args{(int)M, (int)N, (int)K, a_kmajor, b_kmajor, fmt, out_kind, sa, sb, out,
+                  xf_lb, xf_norm, out_trans, (int)(n_valid < N ? n_valid : N)};
     const int tiles = (int)(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
     const int grid = tiles < num_sms() ? tiles : num_sms();
     if (fmt == FMT_INT8) {

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -174,7 +175,29 @@ static int prof_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int
     return run_gemm(fmt, A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, out, out_kind, st);
 }
 
-// ================================================================ helpers
+static int prof_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+                       int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int64_t xf_block,
+                       int out_trans, int64_t n_valid, cudaStream_t st) {
+    ProfScope ps(PC_GEMM, 2.0 * (double)M * (double)N * (double)K, st);
+    int lb = 0;
+    while ((int64_t(1) << lb) < xf_block) ++lb;
+    return run_gemm_x(fmt, A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, out, out_kind, lb, hadamard_norm(xf_block),
+                      out_trans, n_valid, st);
+}
+
+// the GEMM epilogue can apply a block-B transform along its 256-column tile
+static bool fusable_block(int64_t B) { return B >= 2 && B <= 256 && (B & (B - 1)) == 0; }
+
+// HALO_FUSE_K4=0 keeps the un-rotation in separate K4 kernels (A/B runs)
+static bool fuse_k4() {
+    static const bool on = [] {
+        const char* e = getenv("HALO_FUSE_K4");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// ================================================================= helpers
 
 extern "C" int halo_abi_version(void) { return HALO_B200_ABI_VERSION; }
 extern "C" const char* halo_last_error(void) { return g_err.c_str(); }
@@ -596,13 +619,23 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         if (r != HALO_OK) return r;
         l->ce += 2;
         float* P = c->scratch.as<float>();
-        // prod = qmatmul(eq, wq)  (:401): B operand (n x m) is MN-major
-        int gr = prof_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
-        if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
-        // prod = transform_left(prod); take_rows(b)  (:405-409), in place
-        ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
-        run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, P,
-                 b, nullptr, nullptr, nullptr, st);
+        if (fuse_k4() && fusable_block(Bb)) {
+            // prod^T = wq^T ehq^T (:401, transposed: M = in-features,
+            // N = padded tokens); the epilogue applies transform_left over
+            // the token axis (:405-408) and stores take_rows(b) of prod
+            // (:409) row-major.  ss = sw * s_ehq: same exact double product.
+            int gr = prof_gemm_x(fmt, wq, c->ehq.as<uint8_t>(), m, b_pad, n, 0, 1, sw, &d->scale[SEH], P, 0, Bb, 1, b,
+                                 st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
+        } else {
+            // prod = qmatmul(eq, wq)  (:401): B operand (n x m) is MN-major
+            int gr = prof_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
+            // prod = transform_left(prod); take_rows(b)  (:405-409), in place
+            ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
+            run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     P, b, nullptr, nullptr, nullptr, st);
+        }
         // prod = transform_right_ht(prod)  (:410-411)
         finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st);
     } else {
@@ -611,7 +644,13 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
                                                    &d->amax[SE], &d->scale[SE], &d->err, st);
         if (r != HALO_OK) return r;
         l->ce += 1;
-        if (s.E.right) {
+        if (s.E.right && fuse_k4() && fusable_block(Bm)) {
+            // E_X = (E_Y)_Q (WH)_Q H^T (:410-411) with the right transform in
+            // the GEMM epilogue
+            int gr = prof_gemm_x(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
+                                 ex_dtype == HALO_DTYPE_F32 ? 0 : 1, Bm, 0, m, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
+        } else if (s.E.right) {
             if (c->scratch.ensure((size_t)(b * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
             float* P = c->scratch.as<float>();
             int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
@@ -627,7 +666,13 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     // ---- gradient path (:418-439): G = (E_Y^T)_Q (XH)_Q [H^T]
     if (grad_w) {
         const uint8_t* xq = c->xq.as<uint8_t>();
-        if (s.G.right) {
+        if (s.G.right && fuse_k4() && fusable_block(Bm)) {
+            // grad_w = (E_Y^T)_Q (XH)_Q H^T (:433-437), the right transform in
+            // the GEMM epilogue
+            int gr = prof_gemm_x(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], grad_w,
+                                 gw_dtype == HALO_DTYPE_F32 ? 0 : 1, Bm, 0, m, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
+        } else if (s.G.right) {
             if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
             float* G = c->gscratch.as<float>();
             int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], G, 0, st);

@@ -35,6 +35,13 @@ void run_plain(const void* in, int in_dtype, int64_t n, int mode, int fmt, unsig
 // Returns 0 on success, else a cudaError_t / -1 for unsupported shapes.
 int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
              int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st);
+// K3 + fused K4: as run_gemm, then a blockwise FWHT (block 2^xf_lb <= 256,
+// reference stage order, final multiply by xf_norm) along N inside the
+// epilogue; out_trans stores C^T ([n_valid][M], rows of C^T beyond n_valid
+// dropped).  out_kind 0/1 only.
+int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+               int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int xf_lb, float xf_norm,
+               int out_trans, int64_t n_valid, cudaStream_t st);
 
 // production K1/K2/K4 kernels for blocks <= 256 (fwht2.cu); false = not handled
 bool rows_v2(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
