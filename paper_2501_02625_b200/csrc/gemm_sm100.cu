@@ -30,6 +30,8 @@
 //               through the double-buffered accumulator.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -39,13 +41,29 @@
 
 namespace halo_b200 {
 
-constexpr int BM = 128, BN = 256, BK = 128, STAGES = 4;
+// Per-CTA tile: 128 rows (TMEM lanes) x 256 columns.  CG = 2 pairs two CTAs
+// of a cluster on one 256 x 256 tile with cta_group::2 MMAs: each CTA loads
+// its 128 rows of A and HALF of B (128 of the 256 N-rows), so the L2->SM
+// operand traffic per MAC drops by a third (48 -> 32 KB per CTA per k-block).
+constexpr int BM = 128, BN = 256, BK = 128;
 constexpr int A_STAGE_BYTES = BM * BK;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK;  // 32 KB
-constexpr int GEMM_THREADS = 256;
+template <int CG>
+struct GemmCfg {
+    static constexpr int B_ROWS = BN / CG;                       // B rows loaded per CTA
+    static constexpr int B_STAGE_BYTES = B_ROWS * BK;            // 32 / 16 KB
+    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int TILE_M = BM * CG;                       // rows per (pair) tile
+};
+constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 16;  // tile raster: 16 M-tiles share each B panel in L2
-constexpr size_t GEMM_SMEM = 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256;
+constexpr int EPI_WARPS = 8;
+constexpr int STG_BYTES = EPI_WARPS * 32 * 32 * 4;  // epilogue staging: 32 rows x 32 fp32 per warp
+template <int CG>
+constexpr size_t gemm_smem() {
+    return 1024 /*align slack*/ + GemmCfg<CG>::STAGES * (A_STAGE_BYTES + GemmCfg<CG>::B_STAGE_BYTES) + STG_BYTES + 256;
+}
+static_assert(gemm_smem<1>() <= 232448 && gemm_smem<2>() <= 232448, "smem budget");
 
 struct GemmArgs {
     int M, N, K;
@@ -64,6 +82,8 @@ struct GemmArgs {
     // of C^T (N-index) are dropped (take_rows after the left transform)
     int out_trans;
     int n_valid;
+    int dbg_skip_epi;  // HALO_GEMM_DEBUG_SKIP_EPI=1: epilogue only releases TMEM (timing experiments)
+    int tma_store;     // C written by TMA boxes of 32 rows x 128 B (tmC); else coalesced STG flush
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -72,9 +92,61 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-template <int FMT>
+__device__ __forceinline__ void tc_commit_mc2(uint64_t* bar) {
+    // arrive on the barrier at this offset in BOTH CTAs of the pair
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-CTA TMA: data lands in this CTA's smem, completion bytes go to the
+// leader CTA's mbarrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int FMT, int CG>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
+    if constexpr (CG == 2) {
+        if constexpr (FMT == FMT_INT8) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+                : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+                : "memory");
+        }
+        return;
+    }
     if constexpr (FMT == FMT_INT8) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -102,6 +174,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// split form: issue now, consume after tmem_wait32 (which ties the registers
+// to the wait so the compiler cannot read them early)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])::"memory");
+}
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -118,6 +212,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
         "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
         "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
         : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -174,6 +273,56 @@ __device__ __forceinline__ void ep_store8(const GemmArgs& p, int row, int col0, 
     }
 }
 
+// ---- epilogue staging: a warp's 32 rows x 32 fp32 columns (4 KB), the
+// 16 B chunks XOR-swizzled by row so that both the row-per-lane writes and
+// the chunk-per-lane reads are bank-conflict free; the flush then writes
+// whole sectors (8 lanes cover one 128 B row of fp32 per instruction)
+// instead of one scattered 16 B piece per lane and row.
+__device__ __forceinline__ int stg_phys(int row, int k) { return k ^ (row & 7); }
+
+// 8 values = staged chunks 2*seg, 2*seg+1 of this lane's row
+__device__ __forceinline__ void stg_put(float* S, int lane, int seg, const float* v8) {
+    float4* R = reinterpret_cast<float4*>(S + lane * 32);
+    R[stg_phys(lane, 2 * seg)] = make_float4(v8[0], v8[1], v8[2], v8[3]);
+    R[stg_phys(lane, 2 * seg + 1)] = make_float4(v8[4], v8[5], v8[6], v8[7]);
+}
+
+// staged (row r, chunk k) -> C[row0 + r][col_base + (k>>1)*cstride + (k&1)*4 .. +3]
+__device__ __forceinline__ void stg_flush(const GemmArgs& p, const float* S, int lane, int row0, int col_base,
+                                          int cstride) {
+    const int k = lane & 7;
+    const int col = col_base + (k >> 1) * cstride + (k & 1) * 4;
+    const bool full = col + 4 <= p.N && (p.N % 4) == 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int r = 4 * t + (lane >> 3);
+        const float4 a = reinterpret_cast<const float4*>(S + r * 32)[stg_phys(r, k)];
+        const int row = row0 + r;
+        if (row >= p.M || col >= p.N) continue;
+        const int64_t off = (int64_t)row * p.N + col;
+        const float v[4] = {a.x, a.y, a.z, a.w};
+        if (p.out_kind == 1) {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + off;
+            if (full) {
+                *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (col + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
+            }
+        } else {  // fp32, or raw s32 bits
+            float* o = static_cast<float*>(p.out) + off;
+            if (full) {
+                *reinterpret_cast<float4*>(o) = a;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (col + j < p.N) o[j] = v[j];
+            }
+        }
+    }
+}
+
 // UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
 //   K-major : SBO = 1024 B (8 rows x 128 B), LBO unused
 //   MN-major: LBO = stride between 128-element MN chunks, SBO = 1024 B
@@ -207,14 +356,23 @@ __device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int&
     nb = r / gsize;
 }
 
-template <int FMT>
+template <int FMT, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmC, GemmArgs p) {
+    using C = GemmCfg<CG>;
+    constexpr int STAGES = C::STAGES;
+    constexpr int B_STAGE_BYTES = C::B_STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024 B alignment (128 B swizzle atoms) by pointer arithmetic on the
+    // __shared__ array, so generic-pointer accesses stay LDS/STS (identical
+    // offsets in both CTAs of a pair, as cta_group::2 requires)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+    // epilogue staging (1 KB aligned: 128 B-swizzled TMA-store boxes), then barriers
+    float* stg = reinterpret_cast<float*>(sB + STAGES * B_STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES + STG_BYTES);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
@@ -222,7 +380,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mt = (p.M + BM - 1) / BM, nt = (p.N + BN - 1) / BN;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // pair (cluster) index
+    const int mt = (p.M + C::TILE_M - 1) / C::TILE_M, nt = (p.N + BN - 1) / BN;
     const int ntiles = mt * nt;
     const int nkb = (p.K + BK - 1) / BK;
 
@@ -235,55 +396,76 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
+            mbar_init(&tempty[s], EPI_WARPS * CG);  // every epilogue warp of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ============================ TMA producer
+        // ============================ TMA producer (both CTAs of a pair)
         if (lane == 0) {
+            // pair mode: bytes of BOTH CTAs complete on the leader's barrier,
+            // which alone carries the expect_tx
+            const uint32_t full_leader0 = CG == 2 ? mapa_rank(&full[0], 0) : 0u;
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int t = cid; t < ntiles; t += ncl) {
                 int mb, nb;
                 tile_coords(t, mt, nt, mb, nb);
-                const int m0 = mb * BM, n0 = nb * BN;
+                const int m0 = mb * C::TILE_M + (int)rank * BM, n0 = nb * BN + (int)rank * C::B_ROWS;
                 for (int kb = 0; kb < nkb; ++kb) {
                     const int k0 = kb * BK;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
                     uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
                     uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
-                    if (p.a_kmajor) tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
-                    else tma_load_2d(a_dst, &tmA, &full[stage], m0, k0);
-                    if (p.b_kmajor) {
-                        tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+                    if constexpr (CG == 2) {
+                        if (leader) mbar_expect_tx(&full[stage], 2 * (A_STAGE_BYTES + B_STAGE_BYTES));
+                        const uint32_t fb = full_leader0 + stage * 8;
+                        if (p.a_kmajor) tma_load_2d_2sm(a_dst, &tmA, fb, k0, m0);
+                        else tma_load_2d_2sm(a_dst, &tmA, fb, m0, k0);
+                        if (p.b_kmajor) tma_load_2d_2sm(b_dst, &tmB, fb, k0, n0);
+                        else tma_load_2d_2sm(b_dst, &tmB, fb, n0, k0);
                     } else {
-                        tma_load_2d(b_dst, &tmB, &full[stage], n0, k0);
-                        tma_load_2d(b_dst + B_STAGE_BYTES / 2, &tmB, &full[stage], n0 + 128, k0);
+                        mbar_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+                        if (p.a_kmajor) tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+                        else tma_load_2d(a_dst, &tmA, &full[stage], m0, k0);
+                        if (p.b_kmajor) {
+                            tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+                        } else {
+                            tma_load_2d(b_dst, &tmB, &full[stage], n0, k0);
+                            tma_load_2d(b_dst + B_STAGE_BYTES / 2, &tmB, &full[stage], n0 + 128, k0);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ============================ MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc = make_idesc(FMT, !p.a_kmajor, !p.b_kmajor, BM, BN);
+        // ============================ MMA issuer (the leader CTA of a pair)
+        if (lane == 0 && leader) {
+            const uint32_t idesc = make_idesc(FMT, !p.a_kmajor, !p.b_kmajor, C::TILE_M, BN);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+            for (int t = cid; t < ntiles; t += ncl, ++local) {
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -300,53 +482,175 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         const uint64_t ad = p.a_kmajor ? make_desc(a_addr + k * 32, 16, 1024)
                                                        : make_desc(a_addr + k * 4096, A_STAGE_BYTES, 1024);
                         const uint64_t bd = p.b_kmajor ? make_desc(b_addr + k * 32, 16, 1024)
-                                                       : make_desc(b_addr + k * 4096, B_STAGE_BYTES / 2, 1024);
-                        tc_mma<FMT>(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                                                       : make_desc(b_addr + k * 4096, 128 * BK, 1024);
+                        tc_mma<FMT, CG>(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
-                    tc_commit(&empty[stage]);  // smem stage free once these MMAs retire
+                    // smem stage free (in both CTAs) once these MMAs retire
+                    if constexpr (CG == 2) tc_commit_mc2(&empty[stage]);
+                    else tc_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(&tfull[acc]);  // accumulator complete
+                if constexpr (CG == 2) tc_commit_mc2(&tfull[acc]);  // accumulator complete (both halves)
+                else tc_commit(&tfull[acc]);
             }
         }
     } else if (warp >= 4) {
-        // ============================ epilogue
-        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
-        const double ss = (double)(*p.sa) * (double)(*p.sb);
+        // ============================ epilogue (8 warps)
+        // warp w reads TMEM lanes 32*(w%4).. (its row quadrant q) and owns the
+        // column half h of the 256-column accumulator
+        const int ew = warp - 4;
+        const int q = ew & 3, h = ew >> 2;
+        float* S = stg + ew * (32 * 32);
+        const float sa = *p.sa, sb = *p.sb;
+        const double ss = (double)sa * (double)sb;
         const float ssf = (float)ss;
+        // ss = s_hi + s_lo exactly (a product of two floats has <= 48 bits)
+        const float s_hi = __fmul_rn(sa, sb), s_lo = __fmaf_rn(sa, sb, -s_hi);
+        // raw accumulator -> output value.  INT8: the reference's
+        // float(double(acc) * (double(sa) * double(sb))) (quantize.hpp:356-370)
+        // on the fp32 pipe: for |acc| < 2^24, P = acc*s_hi + acc*s_lo as p + t
+        // (t's rounding error <= 2^-47 |p|), c = RN(p + t), certified when the
+        // residual P - c lies more than 2^-16 half-ulps inside the rounding
+        // interval (then neither the fp32 rounding nor the reference's
+        // intermediate fp64 rounding, 2^-53, can land elsewhere).  A lane
+        // with an uncertified element (about 2^-16 of them, |acc| >= 2^24, or
+        // acc == 0) redoes its 32 values with the fp64 formula.
+        auto cvt = [&](const uint32_t (&r)[32], float (&v)[32]) {
+            if (p.out_kind == 2) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                return;
+            }
+            if constexpr (FMT == FMT_INT8) {
+                int viol = -1;  // max over (|residual| - threshold) and |acc| - (2^24 - 1), as ints
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int A = (int)r[j];
+                    const float af = __int2float_rn(A);
+                    const float pp = __fmul_rn(af, s_hi);
+                    const float t = __fmaf_rn(af, s_lo, __fmaf_rn(af, s_hi, -pp));
+                    const float c = __fadd_rn(pp, t);
+                    const float rr = __fadd_rn(__fadd_rn(pp, -c), t);  // pp - c is exact (Sterbenz)
+                    const int thr = (int)(__float_as_uint(c) & 0x7F800000u) - (24 << 23) - 0x100;
+                    viol = max(viol, max((int)(__float_as_uint(rr) & 0x7FFFFFFFu) - thr, abs(A) - 0xFFFFFF));
+                    v[j] = c;
+                }
+                if (viol >= 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = (float)((double)(int32_t)r[j] * ss);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ssf;
+            }
+        };
+        // 32 final values of this lane's row, columns col0..col0+31 (chunk c
+        // of the tile) -> C.  TMA path: stage a 32-row x 128 B box (fp32: one
+        // chunk; bf16: chunks c, c+1 side by side) 128 B-swizzled, then one
+        // elected lane issues the bulk tensor store.
+        auto store_chunk = [&](const float (&v)[32], int c, int row0_, int col0) {
+            if (p.tma_store) {
+                uint4* R = reinterpret_cast<uint4*>(S) + lane * 8;
+                if (p.out_kind == 1) {
+                    if ((c & 1) == 0) {
+                        if (lane == 0) bulk_wait_read0();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        R[(4 * (c & 1) + g) ^ (lane & 7)] =
+                            make_uint4(pack_bf16x2(v[8 * g], v[8 * g + 1]), pack_bf16x2(v[8 * g + 2], v[8 * g + 3]),
+                                       pack_bf16x2(v[8 * g + 4], v[8 * g + 5]), pack_bf16x2(v[8 * g + 6], v[8 * g + 7]));
+                    if (c & 1) {
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmC, S, col0 - 32, row0_);
+                            bulk_commit();
+                        }
+                    }
+                } else {
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        R[k ^ (lane & 7)] = make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                                                       __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmC, S, col0, row0_);
+                        bulk_commit();
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) stg_put(S, lane, g, v + 8 * g);
+                __syncwarp();
+                stg_flush(p, S, lane, row0_, col0, 8);
+                __syncwarp();
+            }
+        };
+        const uint32_t tempty_leader0 = CG == 2 ? mapa_rank(&tempty[0], 0) : 0u;
         int local = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        for (int t = cid; t < ntiles; t += ncl, ++local) {
             int mb, nb;
             tile_coords(t, mt, nt, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = mb * BM + ew * 32 + lane;
-            const bool row_ok = row < p.M;
-            const uint32_t tacc = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-            if (p.xf_lb > 0) {
-                // ---- fused FWHT along N (hadamard.hpp:136-177 order): pass 1
-                // runs stages len = 1..16 on each 32-column chunk and parks the
-                // fp32 result back in TMEM; pass 2 gathers 8 columns from each
-                // chunk (tcgen05.ld x8) for stages len = 32, 64, 128.
-                const int B = 1 << p.xf_lb;
-                const bool two_pass = B > 32;
+            const int row0 = mb * C::TILE_M + (int)rank * BM + q * 32;
+            const int row = row0 + lane;
+            const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+            if (p.dbg_skip_epi == 1) {
+            } else if (p.dbg_skip_epi == 4) {
+                // timing experiment: TMEM loads + conversion, no stores
+                uint32_t x = 0;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = 4 * h; c < 4 * h + 4; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tacc + c * 32, r);
+                    float v[32];
+                    cvt(r, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) x ^= __float_as_uint(v[j]);
+                }
+                if (x == 0x9E3779B9u) static_cast<int*>(p.out)[0] = 1;
+            } else if (p.dbg_skip_epi == 5) {
+                // timing experiment: TMEM loads + staging + stores of the raw bits, no conversion
+#pragma unroll 1
+                for (int c = 4 * h; c < 4 * h + 4; ++c) {
                     uint32_t r[32];
                     tmem_ld32(tacc + c * 32, r);
                     float v[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if constexpr (FMT == FMT_INT8) v[j] = (float)((double)(int32_t)r[j] * ss);
-                        else v[j] = __uint_as_float(r[j]) * ssf;
-                    }
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) stg_put(S, lane, g, v + 8 * g);
+                    __syncwarp();
+                    stg_flush(p, S, lane, row0, nb * BN + c * 32, 8);
+                    __syncwarp();
+                }
+            } else if (p.xf_lb > 0) {
+                // ---- fused FWHT along N (hadamard.hpp:136-177 order): pass 1
+                // runs stages len = 1..16 on each 32-column chunk (this warp's
+                // 4 chunks) and parks the fp32 result back in TMEM; pass 2
+                // gathers 8 columns from each of the 8 chunks (tcgen05.ld x8;
+                // this warp's 2 of the 4 column groups) for len = 32, 64, 128.
+                const int B = 1 << p.xf_lb;
+                const bool two_pass = B > 32;
+#pragma unroll 1
+                for (int c = 4 * h; c < 4 * h + 4; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tacc + c * 32, r);
+                    float v[32];
+                    cvt(r, v);
 #pragma unroll
                     for (int j = 0; j < 32; j += 2) ep_bfly(v[j], v[j + 1]);  // len 1 (B >= 2)
 #pragma unroll
-                    for (int t = 1; t < 5; ++t) {
-                        const int len = 1 << t;
+                    for (int tt = 1; tt < 5; ++tt) {
+                        const int len = 1 << tt;
                         if (len < B) {
 #pragma unroll
                             for (int j = 0; j < 32; j += 2)
@@ -357,18 +661,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         tmem_st32(tacc + c * 32, v);
                     } else {
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            float o[8];
+                        for (int j = 0; j < 32; ++j) v[j] *= p.xf_norm;
+                        if (p.out_trans) {
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) o[j] = v[8 * g + j] * p.xf_norm;
-                            ep_store8(p, row, nb * BN + c * 32 + 8 * g, o);
+                            for (int g = 0; g < 4; ++g) {
+                                float o[8];
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) o[j] = v[8 * g + j];
+                                ep_store8(p, row, nb * BN + c * 32 + 8 * g, o);
+                            }
+                        } else {
+                            store_chunk(v, c, row0, nb * BN + c * 32);
                         }
                     }
                 }
                 if (two_pass) {
                     tmem_wait_st();
+                    // both column halves of this row quadrant must be in TMEM
+                    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
 #pragma unroll 1
-                    for (int g = 0; g < 4; ++g) {
+                    for (int g = 2 * h; g < 2 * h + 2; ++g) {
                         float u[8][8];
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
@@ -379,94 +691,74 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         }
                         tmem_wait_ld();
 #pragma unroll
-                        for (int t = 0; t < 3; ++t) {
-                            const int h = 1 << t;
-                            if ((32 << t) < B) {
+                        for (int tt = 0; tt < 3; ++tt) {
+                            const int hh = 1 << tt;
+                            if ((32 << tt) < B) {
 #pragma unroll
                                 for (int c = 0; c < 8; ++c)
-                                    if ((c & h) == 0)
+                                    if ((c & hh) == 0)
 #pragma unroll
                                         for (int j = 0; j < 8; j += 2)
-                                            ep_bfly2(u[c][j], u[c][j + 1], u[c + h][j], u[c + h][j + 1]);
+                                            ep_bfly2(u[c][j], u[c][j + 1], u[c + hh][j], u[c + hh][j + 1]);
                             }
                         }
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            float o[8];
+                        for (int c = 0; c < 8; ++c)
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) o[j] = u[c][j] * p.xf_norm;
-                            ep_store8(p, row, nb * BN + c * 32 + 8 * g, o);
+                            for (int j = 0; j < 8; ++j) u[c][j] *= p.xf_norm;
+                        if (p.out_trans) {
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) ep_store8(p, row, nb * BN + c * 32 + 8 * g, u[c]);
+                        } else {
+                            // final values back into TMEM; pass 3 stores whole chunks
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) tmem_st8(tacc + c * 32 + g * 8, u[c]);
+                        }
+                    }
+                    if (!p.out_trans) {
+                        tmem_wait_st();
+                        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+#pragma unroll 1
+                        for (int c = 4 * h; c < 4 * h + 4; ++c) {
+                            uint32_t r[32];
+                            tmem_ld32(tacc + c * 32, r);
+                            float v[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                            store_chunk(v, c, row0, nb * BN + c * 32);
                         }
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
-                continue;
-            }
+            } else {
+                // ---- plain epilogue: this warp's 4 chunks of 32 columns
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
-                const int col0 = nb * BN + c * 32;
-                if (!row_ok || col0 >= p.N) continue;
-                const bool full_chunk = (col0 + 32 <= p.N) && (p.N % 8 == 0);  // 16 B aligned rows
-                if (p.out_kind == 2) {
-                    int32_t* o = static_cast<int32_t*>(p.out) + (int64_t)row * p.N + col0;
-                    if (full_chunk) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<int4*>(o + j) = make_int4(r[j], r[j + 1], r[j + 2], r[j + 3]);
-                    } else {
-                        
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j < p.N) o[j] = (int32_t)r[j];
-                    }
-                    continue;
-                }
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if constexpr (FMT == FMT_INT8) v[j] = (float)((double)(int32_t)r[j] * ss);
-                    else v[j] = __uint_as_float(r[j]) * ssf;
-                }
-                if (p.out_kind == 0) {
-                    float* o = static_cast<float*>(p.out) + (int64_t)row * p.N + col0;
-                    if (full_chunk) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    } else {
-                        
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j < p.N) o[j] = v[j];
-                    }
-                } else {
-                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + (int64_t)row * p.N + col0;
-                    if (full_chunk) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 8) store8(o + j, v + j);
-                    } else {
-                        
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j < p.N) o[j] = __float2bfloat16_rn(v[j]);
-                    }
+                for (int c = 4 * h; c < 4 * h + 4; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tacc + c * 32, r);
+                    float v[32];
+                    cvt(r, v);
+                    store_chunk(v, c, row0, nb * BN + c * 32);
                 }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+                else mbar_arrive(&tempty[acc]);
+            }
         }
+        if (lane == 0) bulk_wait0();  // staged boxes fully written before the CTA leaves
     }
 
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
     tc_fence_after();
     if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        if constexpr (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
     }
 }
 
@@ -536,28 +828,79 @@ int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     // TMA: global strides must be multiples of 16 bytes
     if ((a_kmajor ? K : M) % 16 != 0 || (b_kmajor ? K : N) % 16 != 0) return -1;
     if (out_kind == 2 && fmt != FMT_INT8) return -1;
-    CUtensorMap ma, mb;
-    const bool ok_a = a_kmajor ? encode_map(&ma, A, K, M, BM) : encode_map(&ma, A, M, K, BK);
-    const bool ok_b = b_kmajor ? encode_map(&mb, B, K, N, BN) : encode_map(&mb, B, N, K, BK);
-    if (!ok_a || !ok_b) return -2;
     GemmArgs args{(int)M, (int)N, (int)K, a_kmajor, b_kmajor, fmt, out_kind, sa, sb, out,
-                  xf_lb, xf_norm, out_trans, (int)(n_valid < N ? n_valid : N)};
-    const int tiles = (int)(((M + BM - 1) / BM) * ((N + BN - 1) / BN));
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    if (fmt == FMT_INT8) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_gemm<FMT_INT8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
-            attr = true;
-        }
-        k_gemm<FMT_INT8><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ma, mb, args);
+                  xf_lb, xf_norm, out_trans, (int)(n_valid < N ? n_valid : N), 0};
+    static const int dbg = [] {
+        const char* e = getenv("HALO_GEMM_DEBUG_SKIP_EPI");
+        return e ? atoi(e) : 0;
+    }();
+    args.dbg_skip_epi = dbg;
+    // HALO_GEMM_CG=1 pins the single-CTA kernel (A/B runs)
+    static const int cg_env = [] {
+        const char* e = getenv("HALO_GEMM_CG");
+        return e ? atoi(e) : 2;
+    }();
+    const int cg = (cg_env == 1 || num_sms() < 2) ? 1 : 2;
+    CUtensorMap ma, mb;
+    const int b_box = BN / cg;
+    const bool ok_a = a_kmajor ? encode_map(&ma, A, K, M, BM) : encode_map(&ma, A, M, K, BK);
+    const bool ok_b = b_kmajor ? encode_map(&mb, B, K, N, b_box) : encode_map(&mb, B, N, K, BK);
+    if (!ok_a || !ok_b) return -2;
+    // C via TMA stores when the row pitch is a multiple of 16 B (HALO_GEMM_TMA_STORE=0 disables)
+    static const int tma_store_env = [] {
+        const char* e = getenv("HALO_GEMM_TMA_STORE");
+        return e ? atoi(e) : 1;
+    }();
+    CUtensorMap mc;
+    std::memset(&mc, 0, sizeof(mc));
+    const int esz = out_kind == 1 ? 2 : 4;
+    args.tma_store = 0;
+    if (tma_store_env && !out_trans && ((int64_t)N * esz) % 16 == 0 && (uintptr_t)out % 16 == 0) {
+        auto enc = get_encode();
+        const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+        const cuuint64_t strides[1] = {(cuuint64_t)N * esz};
+        const cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUtensorMapDataType dt = out_kind == 1   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                       : out_kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        if (enc && enc(&mc, dt, 2, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            args.tma_store = 1;
+    }
+    const int64_t tile_m = (int64_t)BM * cg;
+    const int tiles = (int)(((M + tile_m - 1) / tile_m) * ((N + BN - 1) / BN));
+    if (cg == 1) {
+        const int grid = tiles < num_sms() ? tiles : num_sms();
+        auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 1> : k_gemm<FMT_E4M3, 1>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<1>());
+        kern<<<grid, GEMM_THREADS, gemm_smem<1>(), st>>>(ma, mb, mc, args);
     } else {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_gemm<FMT_E4M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
-            attr = true;
+        auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 2> : k_gemm<FMT_E4M3, 2>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<2>());
+        // persistent: as many co-resident pairs as the GPCs can host
+        static int max_pairs[2] = {0, 0};
+        int& mp = max_pairs[fmt == FMT_INT8 ? 0 : 1];
+        cudaLaunchConfig_t cfg = {};
+        cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = gemm_smem<2>();
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (!mp) {
+            cfg.gridDim = dim3(num_sms(), 1, 1);
+            if (cudaOccupancyMaxActiveClusters(&mp, kern, &cfg) != cudaSuccess || mp < 1) mp = num_sms() / 2;
         }
-        k_gemm<FMT_E4M3><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ma, mb, args);
+        const int grid = 2 * (tiles < mp ? tiles : mp);
+        cfg.gridDim = dim3(grid, 1, 1);
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, args);
+        if (le != cudaSuccess) return (int)le;
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : (int)e;

@@ -89,3 +89,27 @@ if "gemm" in what:
            name="gemm_E[8192x4096x14336 K/MN f32]")
     timeit(lambda: halo.qmatmul(eq, xq, one, one, a_kmajor=False, b_kmajor=False, out="f32"), ops=2 * b * H * I,
            name="gemm_G[14336x4096x8192 MN/MN f32]")
+if "gemm_sweep" in what:
+    one = torch.ones(1, device=dev)
+    def cod(r, c):
+        return torch.randint(-127, 128, (r, c), dtype=torch.int8, device=dev, generator=g)
+    for (M, N, K, ak, bk, out) in [(8192, 14336, 4096, 1, 1, "bf16"), (8192, 14336, 4096, 1, 1, "f32"),
+                                   (8192, 14336, 4096, 1, 1, "s32"), (8192, 4096, 14336, 1, 1, "bf16"),
+                                   (8192, 14336, 8192, 1, 1, "bf16"), (16384, 16384, 4096, 1, 1, "bf16"),
+                                   (8192, 8192, 8192, 1, 1, "bf16"), (8192, 4096, 14336, 1, 0, "f32"),
+                                   (14336, 4096, 8192, 0, 0, "f32")]:
+        a = cod(M, K) if ak else cod(K, M)
+        b = cod(N, K) if bk else cod(K, N)
+        timeit(lambda: halo.qmatmul(a, b, one, one, a_kmajor=bool(ak), b_kmajor=bool(bk), out=out), ops=2 * M * N * K,
+               name=f"gemm[{M}x{N}x{K} a{'K' if ak else 'MN'} b{'K' if bk else 'MN'} {out}]")
+        del a, b
+if "gemm_epi" in what:
+    one = torch.ones(1, device=dev)
+    def cod(r, c):
+        return torch.randint(-127, 128, (r, c), dtype=torch.int8, device=dev, generator=g)
+    for (M, N, K, out) in [(8192, 14336, 128, "bf16"), (8192, 14336, 128, "f32"), (8192, 14336, 128, "s32"),
+                           (8192, 14336, 512, "bf16")]:
+        a, b = cod(M, K), cod(N, K)
+        ms = timeit(lambda: halo.qmatmul(a, b, one, one, out=out), ops=2 * M * N * K, name=f"gemm_epi[{M}x{N}x{K} {out}]",
+                    tiles=(M // 256) * (N // 256))
+        del a, b

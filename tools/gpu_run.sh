@@ -29,6 +29,9 @@ for w in $what; do
     prof_k2)
       timeout 600 ncu --set full --clock-control none -k regex:k_cols_v -s 8 -c 2 \
         -f -o gpurun_out/prof_k2 python tools/bench_kernels.py k2 --reps 1 > gpurun_out/prof_k2.log 2>&1 ;;
+    prof_gemm)
+      timeout 600 ncu --set full --clock-control none -k regex:k_gemm -s 3 -c 3 \
+        -f -o gpurun_out/prof_gemm python tools/bench_kernels.py gemm --reps 1 > gpurun_out/prof_gemm.log 2>&1 ;;
     launches)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python tools/prof_step.py 2 > gpurun_out/launches.log 2>&1
