@@ -49,28 +49,47 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region (NVML,
+    every 5 ms from a side thread; nvidia-smi when NVML is unavailable)."""
+
+    REASONS = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80)]
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons_bitmask)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if self._nvml is not None:
+                    n = self._nvml
+                    sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+                    mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+                    rs = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                    self.samples.append((float(sm), float(mx), int(rs)))
+                    self._stop.wait(0.005)
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        f = [x.strip() for x in out.split(",")]
+                        self.samples.append((float(f[0]), float(f[1]), int(f[2], 16)))
+                    self._stop.wait(0.05)
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -83,17 +102,15 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         reasons = set()
-        for s in self.samples:
-            for i, nm in enumerate(names):
-                if len(s) > 3 + i and "Active" in s[3 + i] and "Not" not in s[3 + i]:
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        for _, _, bits in self.samples:
+            for name, bit in self.REASONS:
+                if bits & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def cpu_reference_sample(threads):
@@ -136,7 +153,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens", type=int, default=TOKENS)
@@ -256,28 +273,55 @@ def main():
     # -------------------------------------------------------------- end to end
     e2e = None
     if not args.no_e2e:
-        hx = x.cpu().pin_memory()
-        hdy = dy.cpu().pin_memory()
-        hdx = torch.empty((b, HIDDEN), dtype=bf, pin_memory=True)
-        dx_dev = torch.empty_like(x)
-        xs = torch.empty_like(x)
-        dys = torch.empty_like(dy)
-        for _ in range(2):
-            xs.copy_(hx, non_blocking=True)
-            dys.copy_(hdy, non_blocking=True)
-            dx_dev = step(xs, dys)
-            hdx.copy_(dx_dev, non_blocking=True)
+        # Public-API step with host I/O: every step copies its X and dY from
+        # pinned host memory and reads dX back.  The copies run on a side
+        # stream, double-buffered, so step i+1's inputs upload (and step i's
+        # dX downloads) while step i computes - all inside the timed region.
+        cs = torch.cuda.Stream(device=dev)
+        main = torch.cuda.current_stream(dev)
+        hx = [x.cpu().pin_memory() for _ in range(2)]
+        hdy = [dy.cpu().pin_memory() for _ in range(2)]
+        hdx = [torch.empty((b, HIDDEN), dtype=bf, pin_memory=True) for _ in range(2)]
+        xs = [torch.empty_like(x) for _ in range(2)]
+        dys = [torch.empty_like(dy) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        used = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+
+        def upload(k):
+            with torch.cuda.stream(cs):
+                cs.wait_event(used[k])
+                xs[k].copy_(hx[k], non_blocking=True)
+                dys[k].copy_(hdy[k], non_blocking=True)
+                ready[k].record(cs)
+
+        def run_e2e(n):
+            upload(0)
+            for i in range(n):
+                k = i % 2
+                if i + 1 < n:
+                    upload(1 - k)
+                main.wait_event(ready[k])
+                dx_dev = step(xs[k], dys[k])
+                used[k].record(main)
+                with torch.cuda.stream(cs):
+                    cs.wait_event(used[k])
+                    hdx[k].copy_(dx_dev, non_blocking=True)
+                    dx_dev.record_stream(cs)
+                    done[k].record(cs)
+            main.wait_stream(cs)
+
+        for e in used:
+            e.record(main)
+        run_e2e(2)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
-        ev0.record()
-        for _ in range(args.steps):
-            xs.copy_(hx, non_blocking=True)
-            dys.copy_(hdy, non_blocking=True)
-            dx_dev = step(xs, dys)
-            hdx.copy_(dx_dev, non_blocking=True)
-        ev1.record()
+        torch.cuda.synchronize()
+        ev0.record(main)
+        run_e2e(args.steps)
+        ev1.record(main)
         torch.cuda.synchronize()
         e_ms = ev0.elapsed_time(ev1)
         te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
@@ -285,9 +329,10 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = te.item()
         e2e = {"value": world * ops_step * args.steps / (e_ms / 1e3) / 1e12, "unit": "TOPS",
-               "h2d_bytes_per_step": hx.numel() * 2 + hdy.numel() * 2, "d2h_bytes_per_step": hdx.numel() * 2,
+               "h2d_bytes_per_step": hx[0].numel() * 2 + hdy[0].numel() * 2, "d2h_bytes_per_step": hdx[0].numel() * 2,
                "ms_per_step": e_ms / args.steps,
-               "api": "paper_2501_02625_b200.mlp.HaloMLP over the C ABI (halo_linear_forward/backward)"}
+               "api": "paper_2501_02625_b200.mlp.HaloMLP over the C ABI (halo_linear_forward/backward); "
+                      "H2D/D2H on a side stream, double-buffered, overlapping the previous/next step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
