@@ -44,9 +44,12 @@ def launches(tag):
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name")
     tot, cnt = collections.defaultdict(float), collections.Counter()
     seq = []
     for r in rows[hdr + 1:]:
+        if r[mi] != "gpu__time_duration.sum":
+            continue
         name = r[ki].split("(")[0][:100]
         v = float(r[vi].replace(",", ""))
         v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
@@ -71,10 +74,11 @@ def launches(tag):
 def full(tag):
     lines = []
     for fn in sorted(os.listdir(OUT)):
-        if not (fn.startswith("prof") and fn.endswith(".ncu-rep")):
+        if not (fn.startswith("prof") and fn.endswith(".raw.csv")):
             continue
-        raw = subprocess.run(["ncu", "-i", os.path.join(OUT, fn), "--page", "raw", "--csv"], capture_output=True,
-                             text=True).stdout
+        raw = open(os.path.join(OUT, fn)).read() if fn.endswith(".csv") else \
+            subprocess.run(["ncu", "-i", os.path.join(OUT, fn), "--page", "raw", "--csv"], capture_output=True,
+                           text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
         if len(rows) < 3:
             continue
