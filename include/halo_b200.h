@@ -139,6 +139,17 @@ HALO_API halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_km
                          int64_t M, int64_t N, int64_t K, const float* scale_a, const float* scale_b, void* out,
                          int32_t out_kind, halo_stream_t stream);
 
+/* qmatmul followed by transform_right along N (block had_block, 0 = N), the
+ * reference's qmatmul -> transform_right_ht composition of the backward
+ * (halo_linear.hpp:410-411, 433-437), with the transform fused into the
+ * GEMM epilogue (had_block <= 256).  out_transposed != 0 stores C^T
+ * ([n_valid][M], rows of C^T at or beyond n_valid dropped: the E path's
+ * take_rows after transform_left, :405-409).  out_kind F32 / BF16. */
+HALO_API halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int32_t a_kmajor, const uint8_t* b,
+                                int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
+                                const float* scale_b, void* out, int32_t out_kind, int64_t had_block,
+                                int32_t out_transposed, int64_t n_valid, halo_stream_t stream);
+
 /* ----------------------------------------------------------------- layer */
 
 typedef struct halo_linear halo_linear; /* HaloLinearLayerT, halo_linear.hpp:227 */

@@ -433,6 +433,26 @@ extern "C" halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_
     return HALO_OK;
 }
 
+extern "C" halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int32_t a_kmajor, const uint8_t* b,
+                                           int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
+                                           const float* scale_b, void* out, int32_t out_kind, int64_t had_block,
+                                           int32_t out_transposed, int64_t n_valid, halo_stream_t stream) {
+    if (!a || !b || !out || !scale_a || !scale_b) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_rotate: null pointer");
+    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_rotate: bad format");
+    if (out_kind != 0 && out_kind != 1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_rotate: out kind must be f32 or bf16");
+    int64_t B;
+    if (resolve_block(N, had_block, &B, "qmatmul_rotate") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    if (!fusable_block(B))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_rotate: the fused transform needs a block of 2..256");
+    if (n_valid < 0 || n_valid > N) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_rotate: bad n_valid");
+    const int r = prof_gemm_x(format, a, b, M, N, K, a_kmajor, b_kmajor, scale_a, scale_b, out, out_kind, B,
+                              out_transposed ? 1 : 0, out_transposed ? n_valid : N, (cudaStream_t)stream);
+    if (r == -1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_rotate: unsupported shape (strides must be multiples of 16 B)");
+    if (r == -2) return fail(HALO_ERR_CUDA, "qmatmul_rotate: cuTensorMapEncodeTiled failed");
+    if (r != 0) return fail(HALO_ERR_CUDA, std::string("qmatmul_rotate: ") + cudaGetErrorString((cudaError_t)r));
+    return HALO_OK;
+}
+
 // ================================================================= layer
 
 static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {

@@ -167,8 +167,10 @@ def transform_left(a: torch.Tensor, had_block: int = 0, rows_out: int | None = N
 
 
 def qmatmul(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: torch.Tensor, *,
-            a_kmajor: bool = True, b_kmajor: bool = True, fmt: int = INT8, out: str = "f32") -> torch.Tensor:
-    """``qmatmul`` (quantize.hpp:339-380) on device codes.
+            a_kmajor: bool = True, b_kmajor: bool = True, fmt: int = INT8, out: str = "f32",
+            had_block: int | None = None, transposed: bool = False, n_valid: int | None = None) -> torch.Tensor:
+    """``qmatmul`` (quantize.hpp:339-380) on device codes; with ``had_block``
+    the result is also right-transformed along N in the GEMM epilogue.
 
     A is ``[M, K]`` (a_kmajor) or ``[K, M]``; B is ``[N, K]`` (b_kmajor, the
     reference's transpose_b) or ``[K, N]``.  out: "f32", "bf16" or "s32"
@@ -180,9 +182,17 @@ def qmatmul(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: to
         raise ValueError("qmatmul: inner dimensions disagree")
     kind = {"f32": OUT_F32, "bf16": OUT_BF16, "s32": OUT_S32}[out]
     dt = {OUT_F32: torch.float32, OUT_BF16: torch.bfloat16, OUT_S32: torch.int32}[kind]
-    c = torch.empty((M, N), dtype=dt, device=a.device)
-    check(lib().halo_qmatmul(fmt, _ptr(a), int(a_kmajor), _ptr(b), int(b_kmajor), M, N, K, _ptr(scale_a),
-                             _ptr(scale_b), _ptr(c), kind, _stream()))
+    if had_block is None:
+        c = torch.empty((M, N), dtype=dt, device=a.device)
+        check(lib().halo_qmatmul(fmt, _ptr(a), int(a_kmajor), _ptr(b), int(b_kmajor), M, N, K, _ptr(scale_a),
+                                 _ptr(scale_b), _ptr(c), kind, _stream()))
+        return c
+    # qmatmul -> transform_right along N, fused in the GEMM epilogue;
+    # transposed: C^T[:n_valid] (the HALO-2 error path's layout)
+    nv = N if n_valid is None else n_valid
+    c = torch.empty((nv, M) if transposed else (M, N), dtype=dt, device=a.device)
+    check(lib().halo_qmatmul_rotate(fmt, _ptr(a), int(a_kmajor), _ptr(b), int(b_kmajor), M, N, K, _ptr(scale_a),
+                                    _ptr(scale_b), _ptr(c), kind, had_block, int(transposed), nv, _stream()))
     return c
 
 
