@@ -69,7 +69,7 @@ typedef struct halo_placement {
 typedef struct halo_scheme {
     halo_placement F, E, G;
     int32_t format_x, format_w, format_e; /* halo_format */
-    int32_t granularity;                  /* 0 = tensor (the only device path) */
+    int32_t granularity;                  /* HALO_GRAN_TENSOR, or HALO_GRAN_ROW: forward only (see halo_linear_forward) */
     int32_t quantize_f, quantize_e, quantize_g;
     int32_t peft;
     int64_t had_block; /* 0 = full dimension (reference) */
@@ -149,6 +149,30 @@ HALO_API halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int32
                                 int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
                                 const float* scale_b, void* out, int32_t out_kind, int64_t had_block,
                                 int32_t out_transposed, int64_t n_valid, halo_stream_t stream);
+
+/* Granularity (quantize.hpp:65-87): per tensor, or one scale per row
+ * (per token for X / E_Y, per output channel for W).  Column, block and MX
+ * granularities are not on the device path. */
+#define HALO_GRAN_TENSOR 0
+#define HALO_GRAN_ROW 1
+
+/* quantize(transform_right(a, block), fmt, Granularity::row()): one scale per
+ * row (compute_scales per group, quantize.hpp:202-239); codes bit-exact.
+ * cols must be a multiple of 256; scales_out holds `rows` floats. */
+HALO_API halo_status halo_rotate_quantize_rows(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                      int64_t had_block, int32_t format, uint8_t* codes, float* scales_out,
+                                      halo_stream_t stream);
+
+/* qmatmul with row-granularity operands whose scales sit on non-contracted
+ * dims: a_per_row != 0 -> scale_a has M entries (rows of C), b_per_row != 0
+ * -> scale_b has N entries (columns of C); C = float(double(acc) *
+ * (double(sa_i) * double(sb_j))).  The reference dequantizes and multiplies
+ * in double for non-tensor scales (quantize.hpp:345-349, 377-379): parity
+ * within the tolerance stated in the tests.  out_kind F32 / BF16. */
+HALO_API halo_status halo_qmatmul_scaled(int32_t format, const uint8_t* a, int32_t a_kmajor, const uint8_t* b,
+                                int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
+                                int32_t a_per_row, const float* scale_b, int32_t b_per_row, void* out,
+                                int32_t out_kind, halo_stream_t stream);
 
 /* ----------------------------------------------------------------- layer */
 

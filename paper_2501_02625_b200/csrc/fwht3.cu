@@ -140,7 +140,13 @@ __device__ __forceinline__ bool group_slow(float2 a, float2 b, float s, float in
     return slow;
 }
 
-enum : int { V3_ABSMAX = 0, V3_QUANT = 1, V3_XFORM = 2 };
+enum : int { V3_ABSMAX = 0, V3_QUANT = 1, V3_XFORM = 2, V3_ABSMAX_ROWS = 3, V3_QUANT_ROWS = 4 };
+// per-row scale modes (Granularity::row, quantize.hpp:73-132): one absmax
+// word / scale per row of `cols` elements (cols a multiple of 256, so every
+// 256-element segment of a lane lies in one row)
+template <int MODE> __host__ __device__ constexpr bool v3_abs() { return MODE == V3_ABSMAX || MODE == V3_ABSMAX_ROWS; }
+template <int MODE> __host__ __device__ constexpr bool v3_q() { return MODE == V3_QUANT || MODE == V3_QUANT_ROWS; }
+template <int MODE> __host__ __device__ constexpr bool v3_rows() { return MODE == V3_ABSMAX_ROWS || MODE == V3_QUANT_ROWS; }
 
 
 // ------------------------------------------------------------------ core
@@ -160,6 +166,40 @@ struct RowsCore {
     float s = 1.f, inv = 1.f, norm = 1.f, amax = 0.f;
     float thr = 0.5f;  // slow-path threshold on the running residual maximum
     float2 inv2, magic2, norm2, nsm2;
+    int64_t cols = 0;                  // row length (per-row modes)
+    unsigned* amax_rows = nullptr;     // V3_ABSMAX_ROWS: one absmax word per row
+    const float* row_scale = nullptr;  // V3_QUANT_ROWS: per-row scales (k_row_scales)
+
+    // per-row modes: the scale of the row holding element e0
+    __device__ __forceinline__ void row_setup(int64_t e0) {
+        if constexpr (MODE == V3_QUANT_ROWS) {
+            s = __ldg(row_scale + e0 / cols);
+            // any inv near 1/s works: candidates are certified against s
+            inv = FMT == FMT_INT8 ? __fdividef(1.0f, s) : __frcp_rn(s);
+            if (FOLD) {
+                s = s / norm;
+                inv = inv * norm;
+            }
+            inv2 = make_float2(inv, inv);
+            nsm2 = make_float2(-s, -s);
+            if (FMT == FMT_INT8) thr = half_margin(s);
+        }
+    }
+    // per-row absmax: reduce the lane's segment maximum over the 8 lanes of
+    // the segment (lanes 8k..8k+7), one atomic per segment and chunk
+    __device__ __forceinline__ void row_flush(int64_t e0, unsigned* err) {
+        if constexpr (MODE == V3_ABSMAX_ROWS) {
+            float m = amax;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) m = max3nan(m, __shfl_xor_sync(0xffffffffu, m, o), 0.f);
+            m *= norm;
+            if ((threadIdx.x & 7) == 0) {
+                atomic_absmax(amax_rows + e0 / cols, fabsf(m));
+                if (!(m <= 3.402823466e38f)) atomicOr(err, ERRF_NONFINITE);
+            }
+            amax = 0.f;
+        }
+    }
 
     __device__ __forceinline__ void init(const unsigned* absmax, const float* supplied, float nrm, unsigned* err,
                                          float* scale_out) {
@@ -187,7 +227,7 @@ struct RowsCore {
         if constexpr (P1 >= 1) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                if (MODE == V3_ABSMAX && LB == 1) {
+                if (v3_abs<MODE>() && LB == 1) {
                     amax = max3nan(amax, fabsf(v[i].x) + fabsf(v[i].y), 0.f);
                 } else {
                     const float a = v[i].x, b = v[i].y;
@@ -198,7 +238,7 @@ struct RowsCore {
 #pragma unroll
         for (int t = 1; t < P1; ++t) {
             const int h = 1 << (t - 1);  // pair-index distance for len = 2^t
-            const bool last = (MODE == V3_ABSMAX) && !X2 && (t == LB - 1);
+            const bool last = v3_abs<MODE>() && !X2 && (t == LB - 1);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 if ((i & h) == 0) {
@@ -207,7 +247,7 @@ struct RowsCore {
                 }
             }
         }
-        if constexpr (MODE == V3_ABSMAX && LB == 0) {
+        if constexpr (v3_abs<MODE>() && LB == 0) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) amax = max3nan(amax, fabsf(v[i].x), fabsf(v[i].y));
         }
@@ -245,7 +285,7 @@ struct RowsCore {
                                            uint8_t* __restrict__ codes, OutT* __restrict__ out) {
         if constexpr (!X2) {
             const int64_t e0 = base + k * 256 + p * 32;
-            if constexpr (MODE == V3_QUANT) {
+            if constexpr (v3_q<MODE>()) {
                 float dmax = 0.f;
                 uint32_t wd[8];
 #pragma unroll
@@ -309,7 +349,7 @@ struct RowsCore {
 #pragma unroll
             for (int t = 0; t < P2; ++t) {
                 const int h = 1 << t;
-                const bool last = (MODE == V3_ABSMAX) && (t == P2 - 1);
+                const bool last = v3_abs<MODE>() && (t == P2 - 1);
 #pragma unroll
                 for (int b = 0; b < 8; ++b) {
                     if ((b & h) == 0) {
@@ -327,7 +367,7 @@ struct RowsCore {
             }
             // lane's outputs: elements base + 256k + 32b + 4p + 0..3
             const int64_t e0 = base + k * 256 + 4 * p;
-            if constexpr (MODE == V3_QUANT) {
+            if constexpr (v3_q<MODE>()) {
                 float dmax = 0.f;
                 uint32_t* dst = reinterpret_cast<uint32_t*>(codes + e0);
                 if (base + 1024 <= n) {  // interior chunk: no per-group bounds
@@ -383,14 +423,17 @@ struct RowsCore {
 
 // ------------------------------------------------ v3: direct 256-bit loads
 template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
-__global__ void __launch_bounds__(256) k_rows_v3(const InT* __restrict__ in, int64_t n, float norm, unsigned* absmax,
-                                                 const float* supplied, uint8_t* __restrict__ codes,
+__global__ void __launch_bounds__(256) k_rows_v3(const InT* __restrict__ in, int64_t n, int64_t cols, float norm,
+                                                 unsigned* absmax, const float* supplied, uint8_t* __restrict__ codes,
                                                  OutT* __restrict__ out, unsigned* err, float* scale_out) {
     __shared__ __align__(16) float4 xs[8][4 * 64];  // per warp: 4 segments x 64 float4 slots
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int k = l >> 3, p = l & 7;
     RowsCore<LB, FMT, MODE, SUP, OutT> core;
     core.init(absmax, supplied, norm, err, scale_out);
+    core.cols = cols;
+    core.amax_rows = absmax;
+    core.row_scale = supplied;
     const int64_t nchunks = (n + 1023) >> 10;
     const int64_t cstride = (int64_t)gridDim.x * 8;
     const int lane_off = k * 256 + p * 32;
@@ -405,8 +448,11 @@ __global__ void __launch_bounds__(256) k_rows_v3(const InT* __restrict__ in, int
         float2 v[16];
         cur.get(v);
         if (c + cstride < nchunks) load_chunk(nxt, c + cstride);
+        const int64_t seg0 = (c << 10) + k * 256;  // this lane's 256-element segment
+        core.row_setup(seg0);
         core.phase1(v);
         core.finish(v, c << 10, n, k, p, xs[w], codes, out);
+        core.row_flush(seg0, err);
         cur = nxt;
     }
     core.reduce(absmax, err);
@@ -455,7 +501,7 @@ __device__ __forceinline__ void v4_read(const uint8_t* stage, int k, int p, floa
 }
 
 template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
-__global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtensorMap tm, int64_t n, float norm,
+__global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtensorMap tm, int64_t n, int64_t cols, float norm,
                                                  unsigned* absmax, const float* supplied,
                                                  uint8_t* __restrict__ codes, OutT* __restrict__ out, unsigned* err,
                                                  float* scale_out) {
@@ -489,12 +535,17 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
     __syncwarp();
     RowsCore<LB, FMT, MODE, SUP, OutT> core;
     core.init(absmax, supplied, norm, err, scale_out);
+    core.cols = cols;
+    core.amax_rows = absmax;
+    core.row_scale = supplied;
     int i = 0;
     for (int64_t c = c0; c < nchunks; c += G, ++i) {
         const int s = i % C::STAGES;
         mbar_wait(&bars[s], (uint32_t)(i / C::STAGES) & 1u);
         float2 v[16];
         v4_read<InT>(stages + s * C::STAGE_BYTES, k, p, v);
+        const int64_t seg0 = (c << 10) + k * 256;  // this lane's 256-element segment
+        core.row_setup(seg0);
         core.phase1(v);  // consumes every loaded value: the stage's reads are complete
         __syncwarp();
         if (l == 0) {
@@ -506,6 +557,7 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
             }
         }
         core.finish(v, c << 10, n, k, p, xch, codes, out);
+        core.row_flush(seg0, err);
     }
     core.reduce(absmax, err);
 }
@@ -542,7 +594,7 @@ namespace {
 
 template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
 void launch_v3(const InT* in, int64_t n, unsigned* amax, const float* sup, uint8_t* codes, OutT* out, unsigned* err,
-               float* sout, cudaStream_t st) {
+               float* sout, cudaStream_t st, int64_t cols = 256) {
     const float norm = hadamard_norm(int64_t(1) << LB);
     using C = V4Cfg<InT>;
     if (k1_version() >= 4 && n % C::ROW_ELEMS == 0 && (uintptr_t)in % 16 == 0) {
@@ -558,13 +610,13 @@ void launch_v3(const InT* in, int64_t n, unsigned* amax, const float* sup, uint8
             int64_t want = ((n + 1023) / 1024 + C::WARPS - 1) / C::WARPS;
             const int64_t cap = (int64_t)num_sms() * per_sm;
             if (want > cap) want = cap;
-            kern<<<(unsigned)(want < 1 ? 1 : want), 32 * C::WARPS, C::SMEM, st>>>(tm, n, norm, amax, sup, codes, out,
-                                                                              err, sout);
+            kern<<<(unsigned)(want < 1 ? 1 : want), 32 * C::WARPS, C::SMEM, st>>>(tm, n, cols, norm, amax, sup, codes,
+                                                                              out, err, sout);
             return;
         }
     }
     auto kern = k_rows_v3<LB, InT, FMT, MODE, SUP, OutT>;
-    kern<<<v3_grid(kern, n), 256, 0, st>>>(in, n, norm, amax, sup, codes, out, err, sout);
+    kern<<<v3_grid(kern, n), 256, 0, st>>>(in, n, cols, norm, amax, sup, codes, out, err, sout);
 }
 
 template <int LB>
@@ -594,6 +646,60 @@ void dispatch_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, uns
 }
 
 }  // namespace
+
+namespace {
+
+template <int LB>
+void dispatch_rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t cols, unsigned* amax_rows,
+                      const float* row_scales, uint8_t* codes, unsigned* err, cudaStream_t st) {
+#define HALO_VR(T)                                                                                                 \
+    {                                                                                                              \
+        auto p = static_cast<const T*>(in);                                                                        \
+        if (mode == 0) launch_v3<LB, T, 0, V3_ABSMAX_ROWS, false, float>(p, n, amax_rows, nullptr, nullptr, nullptr, err, nullptr, st, cols); \
+        else if (fmt == FMT_INT8) launch_v3<LB, T, FMT_INT8, V3_QUANT_ROWS, false, float>(p, n, nullptr, row_scales, codes, nullptr, err, nullptr, st, cols); \
+        else launch_v3<LB, T, FMT_E4M3, V3_QUANT_ROWS, false, float>(p, n, nullptr, row_scales, codes, nullptr, err, nullptr, st, cols); \
+    }
+    if (in_dtype == DT_BF16) HALO_VR(__nv_bfloat16) else HALO_VR(float)
+#undef HALO_VR
+}
+
+__global__ void k_row_scales(const unsigned* amax, int64_t rows, int fmt, float* scales, unsigned* err) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const unsigned w = amax[r];
+    if (w >= 0x7f800000u) atomicOr(err, ERRF_NONFINITE);
+    scales[r] = scale_from_absmax(__uint_as_float(w), fmt);  // compute_scales, quantize.hpp:202-239
+}
+
+}  // namespace
+
+// Granularity::row (one scale per row, quantize.hpp:73-132): phase A
+// per-row rotated absmax words, per-row scales, phase B quantize with the
+// row's scale.  cols a multiple of 256; B = 2^lb <= 256.
+bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, int64_t B,
+                     unsigned* amax_rows, float* row_scales, uint8_t* codes, unsigned* err, cudaStream_t st) {
+    if (cols % 256 || B < 1 || B > 256 || (B & (B - 1))) return false;
+    if ((uintptr_t)in % 32 || (uintptr_t)codes % 32) return false;
+    const int64_t n = rows * cols;
+    int lb = 0;
+    while ((int64_t(1) << lb) < B) ++lb;
+    cudaMemsetAsync(amax_rows, 0, rows * sizeof(unsigned), st);
+    for (int mode = 0; mode < 2; ++mode) {
+        if (mode == 1) k_row_scales<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(amax_rows, rows, fmt, row_scales, err);
+        switch (lb) {
+        case 0: dispatch_rows_v3<0>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 1: dispatch_rows_v3<1>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 2: dispatch_rows_v3<2>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 3: dispatch_rows_v3<3>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 4: dispatch_rows_v3<4>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 5: dispatch_rows_v3<5>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 6: dispatch_rows_v3<6>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        case 7: dispatch_rows_v3<7>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        default: dispatch_rows_v3<8>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
+        }
+    }
+    return true;
+}
 
 // B = 2^lb with lb in [0, 8]; n a multiple of 16 (and of B).
 bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,

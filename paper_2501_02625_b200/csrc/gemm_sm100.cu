@@ -84,6 +84,10 @@ struct GemmArgs {
     int n_valid;
     int dbg_skip_epi;  // HALO_GEMM_DEBUG_SKIP_EPI=1: epilogue only releases TMEM (timing experiments)
     int tma_store;     // C written by TMA boxes of 32 rows x 128 B (tmC); else coalesced STG flush
+    // Granularity::row scales on non-contracted dims (nullptr = per tensor):
+    // sa_vec[M] per row of C, sb_vec[N] per column of C
+    const float* sa_vec;
+    const float* sb_vec;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -515,10 +519,46 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // intermediate fp64 rounding, 2^-53, can land elsewhere).  A lane
         // with an uncertified element (about 2^-16 of them, |acc| >= 2^24, or
         // acc == 0) redoes its 32 values with the fp64 formula.
-        auto cvt = [&](const uint32_t (&r)[32], float (&v)[32]) {
+        auto cvt = [&](const uint32_t (&r)[32], float (&v)[32], int row_, int col0_) {
             if (p.out_kind == 2) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                return;
+            }
+            if (p.sa_vec || p.sb_vec) {
+                // per-row / per-column scales: the same formula with the
+                // element's scale pair, float(double(acc) * (double(sa_i) * double(sb_j)))
+                const float sai = p.sa_vec ? (row_ < p.M ? __ldg(p.sa_vec + row_) : 0.f) : sa;
+                if constexpr (FMT == FMT_INT8) {
+                    int viol = -1;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float sbj = p.sb_vec ? (col0_ + j < p.N ? __ldg(p.sb_vec + col0_ + j) : 0.f) : sb;
+                        const float shi = __fmul_rn(sai, sbj), slo = __fmaf_rn(sai, sbj, -shi);
+                        const int A = (int)r[j];
+                        const float af = __int2float_rn(A);
+                        const float pp = __fmul_rn(af, shi);
+                        const float t = __fmaf_rn(af, slo, __fmaf_rn(af, shi, -pp));
+                        const float c = __fadd_rn(pp, t);
+                        const float rr = __fadd_rn(__fadd_rn(pp, -c), t);
+                        const int thr = (int)(__float_as_uint(c) & 0x7F800000u) - (24 << 23) - 0x100;
+                        viol = max(viol, max((int)(__float_as_uint(rr) & 0x7FFFFFFFu) - thr, abs(A) - 0xFFFFFF));
+                        v[j] = c;
+                    }
+                    if (viol >= 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float sbj = p.sb_vec ? (col0_ + j < p.N ? __ldg(p.sb_vec + col0_ + j) : 0.f) : sb;
+                            v[j] = (float)((double)(int32_t)r[j] * ((double)sai * (double)sbj));
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float sbj = p.sb_vec ? (col0_ + j < p.N ? __ldg(p.sb_vec + col0_ + j) : 0.f) : sb;
+                        v[j] = __uint_as_float(r[j]) * __fmul_rn(sai, sbj);
+                    }
+                }
                 return;
             }
             if constexpr (FMT == FMT_INT8) {
@@ -612,7 +652,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint32_t r[32];
                     tmem_ld32(tacc + c * 32, r);
                     float v[32];
-                    cvt(r, v);
+                    cvt(r, v, row, nb * BN + c * 32);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) x ^= __float_as_uint(v[j]);
                 }
@@ -645,7 +685,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint32_t r[32];
                     tmem_ld32(tacc + c * 32, r);
                     float v[32];
-                    cvt(r, v);
+                    cvt(r, v, row, nb * BN + c * 32);
 #pragma unroll
                     for (int j = 0; j < 32; j += 2) ep_bfly(v[j], v[j + 1]);  // len 1 (B >= 2)
 #pragma unroll
@@ -736,7 +776,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint32_t r[32];
                     tmem_ld32(tacc + c * 32, r);
                     float v[32];
-                    cvt(r, v);
+                    cvt(r, v, row, nb * BN + c * 32);
                     store_chunk(v, c, row0, nb * BN + c * 32);
                 }
             }
@@ -821,6 +861,24 @@ int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, 
 int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int xf_lb, float xf_norm,
                int out_trans, int64_t n_valid, cudaStream_t st) {
+    return run_gemm_v(fmt, A, B, M, N, K, a_kmajor, b_kmajor, sa, nullptr, sb, nullptr, out, out_kind, xf_lb, xf_norm,
+                      out_trans, n_valid, st);
+}
+
+int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+               int b_kmajor, const float* sa, const float* sa_vec, const float* sb, const float* sb_vec, void* out,
+               int out_kind, int xf_lb, float xf_norm, int out_trans, int64_t n_valid, cudaStream_t st) {
+    if ((sa_vec || sb_vec) && (xf_lb > 0 || out_trans || out_kind == 2)) return -1;
+    static const float kOne = 1.0f;
+    static float* d_one = nullptr;
+    if (!sa || !sb) {  // vector-only call: the tensor scale slot still needs a valid device word
+        if (!d_one) {
+            cudaMalloc(&d_one, sizeof(float));
+            cudaMemcpy(d_one, &kOne, sizeof(float), cudaMemcpyHostToDevice);
+        }
+        if (!sa) sa = d_one;
+        if (!sb) sb = d_one;
+    }
     if (xf_lb < 0 || xf_lb > 8) return -1;  // the 256-column tile must hold whole blocks
     if ((xf_lb > 0 || out_trans) && out_kind == 2) return -1;
     if (M <= 0 || N <= 0 || K <= 0) return -1;
@@ -829,7 +887,7 @@ int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     if ((a_kmajor ? K : M) % 16 != 0 || (b_kmajor ? K : N) % 16 != 0) return -1;
     if (out_kind == 2 && fmt != FMT_INT8) return -1;
     GemmArgs args{(int)M, (int)N, (int)K, a_kmajor, b_kmajor, fmt, out_kind, sa, sb, out,
-                  xf_lb, xf_norm, out_trans, (int)(n_valid < N ? n_valid : N), 0};
+                  xf_lb, xf_norm, out_trans, (int)(n_valid < N ? n_valid : N), 0, 0, sa_vec, sb_vec};
     static const int dbg = [] {
         const char* e = getenv("HALO_GEMM_DEBUG_SKIP_EPI");
         return e ? atoi(e) : 0;

@@ -150,12 +150,17 @@ struct halo_ctx {
     int32_t fmt = 0;
     Buffer xq, wq, ehq, eq, wq2, scratch, gscratch;
     Buffer dev;  // DevScalars
+    // Granularity::row: per-token X scales, per-output-channel W scales and
+    // the per-row absmax scratch
+    Buffer xs_rows, ws_rows, amax_rows;
+    bool row_gran = false;
     const uint8_t* wq_codes = nullptr;  // ctx.wq (own buffer or the layer's qweight)
     const float* wq_scale = nullptr;
+    const float* xq_scale = nullptr;
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
         xq.release(); wq.release(); ehq.release(); eq.release(); wq2.release(); scratch.release();
-        gscratch.release(); dev.release();
+        gscratch.release(); dev.release(); xs_rows.release(); ws_rows.release(); amax_rows.release();
     }
 };
 
@@ -312,8 +317,11 @@ static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows,
 namespace {
 // per-thread scratch for the free-function entry points
 struct FreeScratch {
-    Buffer dev;
-    ~FreeScratch() { dev.release(); }
+    Buffer dev, rows;
+    ~FreeScratch() {
+        dev.release();
+        rows.release();
+    }
 };
 thread_local FreeScratch t_scratch;
 DevScalars* free_scalars() {
@@ -453,6 +461,42 @@ extern "C" halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int
     return HALO_OK;
 }
 
+extern "C" halo_status halo_rotate_quantize_rows(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                                 int64_t had_block, int32_t format, uint8_t* codes, float* scales_out,
+                                                 halo_stream_t stream) {
+    if (!a || !codes || !scales_out) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: null pointer");
+    if (!valid_dtype(a_dtype) || !valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: bad dtype/format");
+    if (rows < 0 || cols <= 0 || cols % 256)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: cols must be a positive multiple of 256");
+    if (rows == 0) return HALO_OK;
+    int64_t B = 1;
+    if (had_block >= 0 && resolve_block(cols, had_block, &B, "rotate_quantize_rows") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    if (B > 256) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: Hadamard block must be <= 256");
+    DevScalars* d = free_scalars();
+    if (!d || t_scratch.rows.ensure((size_t)rows * sizeof(unsigned)) != HALO_OK) return HALO_ERR_CUDA;
+    if (!rows_v3_per_row(format, a_dtype, a, rows, cols, B, t_scratch.rows.as<unsigned>(), scales_out, codes, &d->err,
+                         (cudaStream_t)stream))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: operands must be 32 B aligned");
+    return cuda_check("rotate_quantize_rows");
+}
+
+extern "C" halo_status halo_qmatmul_scaled(int32_t format, const uint8_t* a, int32_t a_kmajor, const uint8_t* b,
+                                           int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
+                                           int32_t a_per_row, const float* scale_b, int32_t b_per_row, void* out,
+                                           int32_t out_kind, halo_stream_t stream) {
+    if (!a || !b || !out || !scale_a || !scale_b) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_scaled: null pointer");
+    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_scaled: bad format");
+    if (out_kind != 0 && out_kind != 1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_scaled: out kind must be f32 or bf16");
+    ProfScope ps(PC_GEMM, 2.0 * (double)M * (double)N * (double)K, (cudaStream_t)stream);
+    const int r = run_gemm_v(format, a, b, M, N, K, a_kmajor, b_kmajor, a_per_row ? nullptr : scale_a,
+                             a_per_row ? scale_a : nullptr, b_per_row ? nullptr : scale_b, b_per_row ? scale_b : nullptr,
+                             out, out_kind, 0, 1.0f, 0, N, (cudaStream_t)stream);
+    if (r == -1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul_scaled: unsupported shape (strides must be multiples of 16 B)");
+    if (r == -2) return fail(HALO_ERR_CUDA, "qmatmul_scaled: cuTensorMapEncodeTiled failed");
+    if (r != 0) return fail(HALO_ERR_CUDA, std::string("qmatmul_scaled: ") + cudaGetErrorString((cudaError_t)r));
+    return HALO_OK;
+}
+
 // ================================================================= layer
 
 static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
@@ -460,7 +504,11 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
     if (!s.quantize_f || !s.quantize_e || !s.quantize_g)
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
-    if (s.granularity != 0) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: only tensor-wise scales are on the device path");
+    if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: only tensor and row granularity are on the device path");
+    if (s.granularity == HALO_GRAN_ROW && (m % 256 || (s.had_block ? s.had_block : m) > 256))
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "halo layer: row granularity needs in_features % 256 == 0 and a Hadamard block <= 256");
     if (!valid_format(s.format_x) || s.format_x != s.format_w || s.format_x != s.format_e)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: X/W/E formats must agree and be int8 or fp8_e4m3");
     if (s.F.left || s.F.right) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_F must be O or M (apply_placement engine is not on the device path)");
@@ -568,6 +616,43 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     DevScalars* d = c->d();
     int64_t B = 1;
     if (rot && resolve_block(l->m, s.had_block, &B, "forward") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    c->row_gran = s.granularity == HALO_GRAN_ROW;
+    if (c->row_gran) {
+        // Granularity::row (quantize.hpp:73-132): X per token, W per output
+        // channel -- both on non-contracted dims of F, so the integer GEMM
+        // stays exact and the epilogue applies sx[i] * sw[j]
+        if (l->qcodes) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row granularity with installed qweight codes");
+        const int64_t mx = b > l->n ? b : l->n;
+        if (c->xs_rows.ensure((size_t)b * sizeof(float)) != HALO_OK || c->wq.ensure((size_t)(l->n * l->m)) != HALO_OK ||
+            c->ws_rows.ensure((size_t)l->n * sizeof(float)) != HALO_OK ||
+            c->amax_rows.ensure((size_t)mx * sizeof(unsigned)) != HALO_OK)
+            return HALO_ERR_CUDA;
+        {
+            ProfScope ps(PC_K1, (double)b * l->m * (dt_bytes(x_dtype) + 1), st);
+            if (!rows_v3_per_row(s.format_x, x_dtype, x, b, l->m, B, c->amax_rows.as<unsigned>(), c->xs_rows.as<float>(),
+                                 c->xq.as<uint8_t>(), &d->err, st))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "forward: row-granularity operands must be 32 B aligned");
+        }
+        ++l->cx;
+        {
+            ProfScope ps(PC_K1, (double)l->n * l->m * (dt_bytes(l->w_dtype) + 1), st);
+            if (!rows_v3_per_row(s.format_w, l->w_dtype, l->w, l->n, l->m, B, c->amax_rows.as<unsigned>(),
+                                 c->ws_rows.as<float>(), c->wq.as<uint8_t>(), &d->err, st))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "forward: row-granularity operands must be 32 B aligned");
+        }
+        ++l->cw;
+        c->wq_codes = c->wq.as<uint8_t>();
+        c->wq_scale = c->ws_rows.as<float>();
+        c->xq_scale = c->xs_rows.as<float>();
+        ProfScope ps(PC_GEMM, 2.0 * (double)b * l->n * l->m, st);
+        const int gr = run_gemm_v(s.format_x, c->xq.as<uint8_t>(), c->wq_codes, b, l->n, l->m, 1, 1, nullptr,
+                                  c->xs_rows.as<float>(), nullptr, c->ws_rows.as<float>(), y,
+                                  y_dtype == HALO_DTYPE_F32 ? 0 : 1, 0, 1.0f, 0, l->n, st);
+        if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
+        c->valid = true;
+        return cuda_check("forward");
+    }
+    c->xq_scale = &d->scale[SX];
     // ctx.xq = quantize(XH)  (:292-294)
     halo_status r = rotate_quantize_impl(x, x_dtype, b, l->m, B, rot, s.format_x, nullptr, c->xq.as<uint8_t>(),
                                          &d->amax[SX], &d->scale[SX], &d->err, st);
@@ -604,6 +689,11 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
     if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
+    if (c->row_gran)
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "halo layer: row-granularity backward puts W's / E_Y's row scales on the contracted dim of E / G; "
+                    "the reference dequantizes and multiplies in double there (quantize.hpp:377-379) and the device "
+                    "path has no full-precision fallback");
     if (c->m != l->m || c->n != l->n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
     if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
@@ -714,6 +804,9 @@ extern "C" halo_status halo_linear_export_inference_weights(halo_linear* l, uint
     if (!l->w) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: no weight set");
     int64_t B;
     if (resolve_block(l->m, l->s.had_block, &B, "export") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    if (l->s.granularity == HALO_GRAN_ROW)  // `scale` receives out_features floats
+        return halo_rotate_quantize_rows(l->w, l->w_dtype, l->n, l->m, l->s.had_block, l->s.format_w, codes, scale,
+                                         stream);
     DevScalars* d = free_scalars();
     if (!d) return HALO_ERR_CUDA;
     return rotate_quantize_impl(l->w, l->w_dtype, l->n, l->m, B, true, l->s.format_w, nullptr, codes, &d->amax[SW],
@@ -740,7 +833,7 @@ extern "C" halo_status halo_ctx_saved(const halo_ctx* c, const uint8_t** xq, con
                                       const float** sw, int64_t* batch_rows) {
     if (!c || !c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: no forward context");
     if (xq) *xq = c->xq.as<uint8_t>();
-    if (sx) *sx = &c->d()->scale[SX];
+    if (sx) *sx = c->xq_scale ? c->xq_scale : &c->d()->scale[SX];
     if (wq) *wq = c->wq_codes;
     if (sw) *sw = c->wq_scale;
     if (batch_rows) *batch_rows = c->b;

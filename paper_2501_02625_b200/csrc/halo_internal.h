@@ -42,6 +42,11 @@ int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, 
 int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int xf_lb, float xf_norm,
                int out_trans, int64_t n_valid, cudaStream_t st);
+// as run_gemm_x with optional per-row (sa_vec[M]) / per-column (sb_vec[N])
+// scales (Granularity::row on the non-contracted dims); no transform then.
+int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+               int b_kmajor, const float* sa, const float* sa_vec, const float* sb, const float* sb_vec, void* out,
+               int out_kind, int xf_lb, float xf_norm, int out_trans, int64_t n_valid, cudaStream_t st);
 
 // production K1/K2/K4 kernels for blocks <= 256 (fwht2.cu); false = not handled
 bool rows_v2(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
@@ -65,6 +70,11 @@ bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
 bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
              unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
              float* sro, float* spo, cudaStream_t st);
+
+// Granularity::row quantization (fwht3.cu): rows*cols input, cols % 256 == 0;
+// amax_rows / row_scales: `rows` words / floats of device scratch / output
+bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, int64_t B,
+                     unsigned* amax_rows, float* row_scales, uint8_t* codes, unsigned* err, cudaStream_t st);
 
 // elementwise glue (glue.cu)
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);

@@ -41,6 +41,9 @@ FP8_E4M3 = FMT_FP8_E4M3
 _DT = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16}
 
 
+GRAN_TENSOR, GRAN_ROW = 0, 1  # halo_b200.h HALO_GRAN_*
+
+
 def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -75,16 +78,22 @@ def scheme_from_string(id: str, fmt: int = INT8, had_block: int = 0) -> Scheme:
     return s
 
 
-def halo0(fmt=INT8, had_block=0):
-    return scheme_from_string("halo0", fmt, had_block)
+def halo0(fmt=INT8, had_block=0, granularity=GRAN_TENSOR):
+    s = scheme_from_string("halo0", fmt, had_block)
+    s.granularity = granularity  # halo_linear.hpp:81-106 take a Granularity
+    return s
 
 
-def halo1(fmt=INT8, had_block=0):
-    return scheme_from_string("halo1", fmt, had_block)
+def halo1(fmt=INT8, had_block=0, granularity=GRAN_TENSOR):
+    s = scheme_from_string("halo1", fmt, had_block)
+    s.granularity = granularity  # halo_linear.hpp:81-106 take a Granularity
+    return s
 
 
-def halo2(fmt=INT8, had_block=0):
-    return scheme_from_string("halo2", fmt, had_block)
+def halo2(fmt=INT8, had_block=0, granularity=GRAN_TENSOR):
+    s = scheme_from_string("halo2", fmt, had_block)
+    s.granularity = granularity  # halo_linear.hpp:81-106 take a Granularity
+    return s
 
 
 def is_supported_hadamard_dim(d: int) -> bool:
@@ -115,6 +124,35 @@ def rotate_quantize(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, scale:
     check(lib().halo_rotate_quantize(_ptr(a), _dt(a), rows, cols, had_block if rotate else -1, fmt,
                                      _ptr(scale), _ptr(codes), _ptr(s_out), _stream()))
     return codes, s_out
+
+
+def rotate_quantize_rows(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, rotate: bool = True):
+    """``quantize(transform_right(a), fmt, Granularity::row())``: codes and one
+    scale per row (``rows`` fp32).  cols must be a multiple of 256."""
+    _need_cuda(a)
+    rows, cols = a.shape
+    codes = torch.empty((rows, cols), dtype=code_dtype(fmt), device=a.device)
+    s_out = torch.empty(rows, dtype=torch.float32, device=a.device)
+    check(lib().halo_rotate_quantize_rows(_ptr(a), _dt(a), rows, cols, had_block if rotate else -1, fmt, _ptr(codes),
+                                          _ptr(s_out), _stream()))
+    return codes, s_out
+
+
+def qmatmul_scaled(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: torch.Tensor, *,
+                   a_kmajor: bool = True, b_kmajor: bool = True, fmt: int = INT8, out: str = "f32") -> torch.Tensor:
+    """qmatmul with per-row scales on the non-contracted dims: ``scale_a`` has 1
+    or M entries (rows of C), ``scale_b`` 1 or N entries (columns of C)."""
+    _need_cuda(a, b, scale_a, scale_b)
+    M, K = a.shape if a_kmajor else a.shape[::-1]
+    N, Kb = b.shape if b_kmajor else b.shape[::-1]
+    if K != Kb:
+        raise ValueError("qmatmul_scaled: inner dimensions disagree")
+    kind = {"f32": OUT_F32, "bf16": OUT_BF16}[out]
+    c = torch.empty((M, N), dtype=torch.float32 if kind == OUT_F32 else torch.bfloat16, device=a.device)
+    check(lib().halo_qmatmul_scaled(fmt, _ptr(a), int(a_kmajor), _ptr(b), int(b_kmajor), M, N, K, _ptr(scale_a),
+                                    int(scale_a.numel() > 1), _ptr(scale_b), int(scale_b.numel() > 1), _ptr(c), kind,
+                                    _stream()))
+    return c
 
 
 def rotate_absmax(a: torch.Tensor, had_block: int = 0, rotate: bool = True) -> torch.Tensor:
@@ -222,10 +260,11 @@ class SavedContext:
         b = C.c_int64()
         check(lib().halo_ctx_saved(self._h, C.byref(xq), C.byref(sx), C.byref(wq), C.byref(sw), C.byref(b)))
         dt = code_dtype(layer.fmt)
+        rows = layer.scheme.granularity == GRAN_ROW
         return (_from_ptr(xq.value, (b.value, layer.in_features), dt),
-                _from_ptr(sx.value, (1,), torch.float32),
+                _from_ptr(sx.value, (b.value if rows else 1,), torch.float32),
                 _from_ptr(wq.value, (layer.out_features, layer.in_features), dt),
-                _from_ptr(sw.value, (1,), torch.float32))
+                _from_ptr(sw.value, (layer.out_features if rows else 1,), torch.float32))
 
     def error_operands(self, layer: "HaloLinearLayer"):
         ehq, seh, eq, se = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
@@ -347,7 +386,8 @@ class HaloLinearLayer:
     def export_inference_weights(self):
         """(WH)_Q codes and scale (halo_linear.hpp:332-338)."""
         codes = torch.empty((self.out_features, self.in_features), dtype=code_dtype(self.fmt), device=self.w.device)
-        scale = torch.empty(1, dtype=torch.float32, device=self.w.device)
+        rows = self.scheme.granularity == GRAN_ROW
+        scale = torch.empty(self.out_features if rows else 1, dtype=torch.float32, device=self.w.device)
         check(lib().halo_linear_export_inference_weights(self._h, _ptr(codes), _ptr(scale), _stream()))
         return codes, scale
 
