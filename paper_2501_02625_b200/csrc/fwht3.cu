@@ -134,7 +134,7 @@ __device__ __forceinline__ bool group_slow(float2 a, float2 b, float s, float in
     for (int i = 0; i < 4; ++i) {
         uint32_t sl;
         if constexpr (FMT == FMT_INT8) (void)quant_int8_try_r(x[i], s, inv, h, sl);
-        else (void)quant_e4m3_try(x[i], inv, sl);
+        else sl = 1;  // E4M3: the bracket test is per word; redo the group exactly
         slow |= sl != 0;
     }
     return slow;
@@ -165,7 +165,7 @@ struct RowsCore {
 
     float s = 1.f, inv = 1.f, norm = 1.f, amax = 0.f;
     float thr = 0.5f;  // slow-path threshold on the running residual maximum
-    float2 inv2, magic2, norm2, nsm2;
+    float2 inv2, magic2, norm2, nsm2, ilo2, ihi2;
     int64_t cols = 0;                  // row length (per-row modes)
     unsigned* amax_rows = nullptr;     // V3_ABSMAX_ROWS: one absmax word per row
     const float* row_scale = nullptr;  // V3_QUANT_ROWS: per-row scales (k_row_scales)
@@ -183,6 +183,7 @@ struct RowsCore {
             inv2 = make_float2(inv, inv);
             nsm2 = make_float2(-s, -s);
             if (FMT == FMT_INT8) thr = half_margin(s);
+            else e4m3_brackets(inv, ilo2, ihi2);
         }
     }
     // per-row absmax: reduce the lane's segment maximum over the 8 lanes of
@@ -219,6 +220,7 @@ struct RowsCore {
         magic2 = make_float2(kRoundMagic, kRoundMagic);
         nsm2 = make_float2(-s, -s);
         if (FMT == FMT_INT8) thr = half_margin(s);
+        else e4m3_brackets(inv, ilo2, ihi2);
         norm2 = make_float2(norm, norm);
     }
 
@@ -266,16 +268,17 @@ struct RowsCore {
             const float2 ta = __ffma2_rn(a, inv2, magic2), tc = __ffma2_rn(c, inv2, magic2);
             const float2 qa = sub2(ta, magic2), qc = sub2(tc, magic2);
             const float2 ra = __ffma2_rn(qa, nsm2, a), rc = __ffma2_rn(qc, nsm2, c);
-            dmax = fmax3(fmax3(dmax, fabsf(ra.x), fabsf(ra.y)), fabsf(rc.x), fabsf(rc.y));
+            float m = fmax3(fmax3(0.f, fabsf(ra.x), fabsf(ra.y)), fabsf(rc.x), fabsf(rc.y));
             if (SUP)  // |q| <= 127 (the clamp) maps below thr, |q| >= 128 above it
-                dmax = fmaxf(dmax, fmax3(fmax3(0.f, fabsf(qa.x), fabsf(qa.y)), fabsf(qc.x), fabsf(qc.y)) *
-                                       (thr / 127.5f));
+                m = fmaxf(m, fmax3(fmax3(0.f, fabsf(qa.x), fabsf(qa.y)), fabsf(qc.x), fabsf(qc.y)) * (thr / 127.5f));
+            // uncertified group (within ~2^-22 of a midpoint, or clamped):
+            // decide its 4 codes exactly right here (divergent but rare)
+            if (!(m < thr)) return exact4<FMT>(a, c, s, inv);
             return pack4(__float_as_uint(ta.x), __float_as_uint(ta.y), __float_as_uint(tc.x), __float_as_uint(tc.y));
         } else {
-            uint32_t s0, s1, s2, s3;
-            const uint32_t w = pack4(quant_e4m3_try(a.x, inv, s0), quant_e4m3_try(a.y, inv, s1),
-                                     quant_e4m3_try(c.x, inv, s2), quant_e4m3_try(c.y, inv, s3));
-            dmax = fmaxf(dmax, (float)(s0 | s1 | s2 | s3));
+            uint32_t bad = 0;
+            const uint32_t w = e4m3x4_fast(a, c, ilo2, ihi2, s, bad);
+            dmax = bad ? 1.0f : dmax;
             return w;
         }
     }

@@ -84,7 +84,7 @@ __device__ __forceinline__ bool c3_group_slow(float2 a, float2 b, float s, float
     for (int i = 0; i < 4; ++i) {
         uint32_t sl;
         if constexpr (FMT == FMT_INT8) (void)quant_int8_try_r(x[i], s, inv, h, sl);
-        else (void)quant_e4m3_try(x[i], inv, sl);
+        else sl = 1;  // E4M3: the bracket test is per word; redo the group exactly
         slow |= sl != 0;
     }
     return slow;
@@ -106,7 +106,7 @@ __device__ __noinline__ void c3_fix(const float4* v, int cnt, uint32_t valid, ui
 template <int FMT, bool SUP>
 struct Quant {
     float s, inv, thr;
-    float2 inv2, nsm2;
+    float2 inv2, nsm2, ilo2, ihi2;
     __device__ __forceinline__ void init(const unsigned* amax, const float* supplied, float fold_norm,
                                          float* scale_out, unsigned* err) {
         resolve_scale(amax, supplied, FMT, &s, &inv);
@@ -119,6 +119,7 @@ struct Quant {
         inv2 = make_float2(inv, inv);
         nsm2 = make_float2(-s, -s);
         thr = FMT == FMT_INT8 ? half_margin(s) : 0.5f;
+        if (FMT != FMT_INT8) e4m3_brackets(inv, ilo2, ihi2);
     }
     // 4 values -> code word; running maximum of the certification residual
     // (INT8: quant_int8_try_r; slow path when it reaches thr)
@@ -128,16 +129,16 @@ struct Quant {
             const float2 ta = __ffma2_rn(a, inv2, m2), tc = __ffma2_rn(c, inv2, m2);
             const float2 qa = c3_sub2(ta, m2), qc = c3_sub2(tc, m2);
             const float2 ra = __ffma2_rn(qa, nsm2, a), rc = __ffma2_rn(qc, nsm2, c);
-            dmax = c3_fmax3(c3_fmax3(dmax, fabsf(ra.x), fabsf(ra.y)), fabsf(rc.x), fabsf(rc.y));
+            float m = c3_fmax3(c3_fmax3(0.f, fabsf(ra.x), fabsf(ra.y)), fabsf(rc.x), fabsf(rc.y));
             if (SUP)  // |q| <= 127 maps below thr, |q| >= 128 above it
-                dmax = fmaxf(dmax, c3_fmax3(c3_fmax3(0.f, fabsf(qa.x), fabsf(qa.y)), fabsf(qc.x), fabsf(qc.y)) *
-                                       (thr / 127.5f));
+                m = fmaxf(m, c3_fmax3(c3_fmax3(0.f, fabsf(qa.x), fabsf(qa.y)), fabsf(qc.x), fabsf(qc.y)) * (thr / 127.5f));
+            // uncertified group: decide its 4 codes exactly right here
+            if (!(m < thr)) return c3_exact4<FMT>(a, c, s, inv);
             return c3_pack4(__float_as_uint(ta.x), __float_as_uint(ta.y), __float_as_uint(tc.x), __float_as_uint(tc.y));
         } else {
-            uint32_t s0, s1, s2, s3;
-            const uint32_t w = c3_pack4(quant_e4m3_try(a.x, inv, s0), quant_e4m3_try(a.y, inv, s1),
-                                        quant_e4m3_try(c.x, inv, s2), quant_e4m3_try(c.y, inv, s3));
-            dmax = fmaxf(dmax, (float)(s0 | s1 | s2 | s3));
+            uint32_t bad = 0;
+            const uint32_t w = e4m3x4_fast(a, c, ilo2, ihi2, s, bad);
+            dmax = bad ? 1.0f : dmax;
             return w;
         }
     }

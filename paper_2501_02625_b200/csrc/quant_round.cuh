@@ -231,6 +231,68 @@ HALO_HD uint8_t quant_int8_try_r(float x, float s, float inv_s, float h, uint32_
     return (uint8_t)(f2u(t) & 0xFFu);
 }
 
+#if defined(__CUDACC__)
+// Fast E4M3 for 4 values (device only).  The hardware F2FP
+// (cvt.rn.satfinite.e4m3x2.f32) rounds to nearest-even with saturation at
+// 448, exactly the reference's round_minifloat (quantize.hpp:138-150,
+// 162-163) applied to its argument.  It is applied to x*inv_lo and x*inv_hi,
+// where inv_lo/hi = RN(RN(1/s) * (1 -+ 2^-21)) bracket 1/s tightly enough
+// that x*inv_lo <= x/s <= x*inv_hi (relative slack 2^-21 against <= 2^-22
+// of rounding), so equal codes prove the code of the exact quotient by
+// monotonicity -- subnormal and saturating ranges included; where they
+// differ, one fma decides (e4m3x4_fast below).  The hardware
+// encodes a negative value that rounds to zero as 0x80; the reference adds
+// +0.0 (quantize.hpp:149), so such bytes become 0x00.
+__device__ __forceinline__ uint32_t e4m3_word(float2 a, float2 c) {
+    uint32_t w;
+    asm("{\n\t.reg .b16 lo, hi;\n\t"
+        "cvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n\t"
+        "cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n\t"
+        "mov.b32 %0, {lo, hi};\n\t}"
+        : "=r"(w)
+        : "f"(a.x), "f"(a.y), "f"(c.x), "f"(c.y));
+    return w;
+}
+// magnitude of an E4M3 code 0..0x7E
+__device__ __forceinline__ float e4m3_mag(uint32_t b) {
+    const uint32_t e = b >> 3, m = b & 7u;
+    return e ? __uint_as_float(((e + 120u) << 23) | (m << 20)) : (float)m * 0.001953125f;
+}
+// Exact E4M3 codes of x[i]/s for 4 values (bit-exact with round_code):
+// when the two bracketed conversions disagree on a byte, the codes are the
+// two grid neighbours of the quotient and the sign of x - mid*s (one fma,
+// exact sign) picks the side; an exact tie takes the even code.  `bad` is
+// kept for the callers' slow-path plumbing and stays 0.
+__device__ __forceinline__ uint32_t e4m3x4_fast(float2 a, float2 c, float2 inv_lo2, float2 inv_hi2, float s,
+                                                uint32_t& bad) {
+    const uint32_t wl = e4m3_word(__fmul2_rn(a, inv_lo2), __fmul2_rn(c, inv_lo2));
+    const uint32_t wh = e4m3_word(__fmul2_rn(a, inv_hi2), __fmul2_rn(c, inv_hi2));
+    uint32_t w = wl;
+    const uint32_t diff = wl ^ wh;
+    if (diff) {
+        const float xs[4] = {a.x, a.y, c.x, c.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if ((diff >> (8 * i)) & 0xFFu) {
+                const uint32_t bl = (wl >> (8 * i)) & 0x7Fu, bh = (wh >> (8 * i)) & 0x7Fu;  // adjacent magnitudes
+                const float mid = 0.5f * (e4m3_mag(bl) + e4m3_mag(bh));
+                const float r = fmaf(-mid, s, fabsf(xs[i]));
+                const uint32_t pick = r > 0.f ? bh : (r < 0.f ? bl : ((bl & 1u) ? bh : bl));
+                w = (w & ~(0x7Fu << (8 * i))) | (pick << (8 * i));
+            }
+        }
+    }
+    (void)bad;
+    const uint32_t nz = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;  // bytes with a nonzero magnitude
+    return w & (nz | 0x7F7F7F7Fu);
+}
+__device__ __forceinline__ void e4m3_brackets(float inv, float2& lo2, float2& hi2) {
+    const float lo = __fmul_rn(inv, 1.0f - 4.76837158203125e-07f), hi = __fmul_rn(inv, 1.0f + 4.76837158203125e-07f);
+    lo2 = make_float2(lo, lo);
+    hi2 = make_float2(hi, hi);
+}
+#endif
+
 // decode for the dequantize / epilogue paths
 HALO_HD float e4m3_to_float(uint8_t b) {
     const int e = (b >> 3) & 0xF, m = b & 7;

@@ -113,3 +113,17 @@ if "gemm_epi" in what:
         ms = timeit(lambda: halo.qmatmul(a, b, one, one, out=out), ops=2 * M * N * K, name=f"gemm_epi[{M}x{N}x{K} {out}]",
                     tiles=(M // 256) * (N // 256))
         del a, b
+if "fp8" in what:
+    for nm, (r, c) in {"dY": (8192, 4096), "dG": (8192, 14336)}.items():
+        e = (torch.randn(r, c, generator=g, device=dev) * 1e-3).to(bf)
+        n = r * c
+        for fmt in (0, 1):
+            timeit(lambda: halo.left_rotate_quantize(e, B, fmt=fmt), nbytes=4 * n, name=f"k2_fmt{fmt}[{nm} {r}x{c}]")
+        del e
+    for nm, (r, c) in {"X": (8192, 4096), "H": (8192, 14336)}.items():
+        a = torch.randn(r, c, generator=g, device=dev).to(bf)
+        n = r * c
+        for fmt in (0, 1):
+            timeit(lambda: halo.rotate_quantize(a, B, fmt=fmt), nbytes=3 * n, name=f"k1_fmt{fmt}[{nm} {r}x{c}]")
+            timeit(lambda: halo.rotate_quantize(a, 1, fmt=fmt), nbytes=3 * n, name=f"k1_fmt{fmt}_B1[{nm} {r}x{c}]")
+        del a
