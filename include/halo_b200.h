@@ -198,6 +198,14 @@ HALO_API halo_status halo_ctx_destroy(halo_ctx* ctx);
 HALO_API halo_status halo_linear_forward(halo_linear* layer, const void* x, int32_t x_dtype, int64_t b, void* y,
                                 int32_t y_dtype, halo_ctx* ctx, halo_stream_t stream);
 
+/* forward() fed the (XH)_Q already held by `src` (a context of another
+ * layer with the same in_features and X quantizer: format, placement,
+ * Hadamard block, granularity) -- the Llama gate/up pattern: X is quantized
+ * once for both.  Same results as halo_linear_forward on the same X; `src`
+ * must stay alive (and not be re-forwarded) until `ctx`'s backward. */
+HALO_API halo_status halo_linear_forward_shared(halo_linear* layer, const halo_ctx* src, halo_ctx* ctx, void* y,
+                                       int32_t y_dtype, halo_stream_t stream);
+
 /* backward, halo_linear.hpp:305-439: e_y (b x n) -> e_x (b x m), grad_w
  * (n x m; may be NULL to skip G). */
 HALO_API halo_status halo_linear_backward(halo_linear* layer, const halo_ctx* ctx, const void* e_y, int32_t e_dtype,

@@ -111,6 +111,13 @@ public:
     }
     void reset_counters() { check(halo_linear_reset_counters(h_)); }
 
+    // forward on the (XH)_Q already held by `src` (same X quantizer): the
+    // Llama gate/up pattern quantizes X once (halo_linear_forward_shared)
+    void forward_shared(const SavedContext& src, void* y, SavedContext& ctx, halo_stream_t st = nullptr,
+                        int32_t y_dtype = HALO_DTYPE_BF16) const {
+        check(halo_linear_forward_shared(h_, src.get(), ctx.get(), y, y_dtype, st));
+    }
+
 private:
     int64_t n_, m_;
     halo_scheme scheme_;

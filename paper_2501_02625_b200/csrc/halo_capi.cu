@@ -157,6 +157,9 @@ struct halo_ctx {
     const uint8_t* wq_codes = nullptr;  // ctx.wq (own buffer or the layer's qweight)
     const float* wq_scale = nullptr;
     const float* xq_scale = nullptr;
+    const uint8_t* xq_borrow = nullptr;  // (XH)_Q shared from another context (halo_linear_forward_shared)
+    int64_t had_block = 0;
+    const uint8_t* xq_codes() const { return xq_borrow ? xq_borrow : xq.as<uint8_t>(); }
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
         xq.release(); wq.release(); ehq.release(); eq.release(); wq2.release(); scratch.release();
@@ -617,6 +620,8 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     int64_t B = 1;
     if (rot && resolve_block(l->m, s.had_block, &B, "forward") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
     c->row_gran = s.granularity == HALO_GRAN_ROW;
+    c->xq_borrow = nullptr;
+    c->had_block = s.had_block;
     if (c->row_gran) {
         // Granularity::row (quantize.hpp:73-132): X per token, W per output
         // channel -- both on non-contracted dims of F, so the integer GEMM
@@ -672,6 +677,69 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
     c->valid = true;
     return cuda_check("forward");
+}
+
+// Forward that reuses another context's (XH)_Q: two layers fed the same X
+// under the same quantizer (Llama gate/up projections) quantize it once.
+// The reference quantizes per layer (halo_linear.hpp:292-294); the codes are
+// identical, so results are unchanged and the input counter is not bumped.
+extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx* src, halo_ctx* c, void* y,
+                                                  int32_t y_dtype, halo_stream_t stream) {
+    if (!l || !src || !c || !y) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
+    if (src == c) return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared: source and target context are the same");
+    if (!src->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared: source context has no forward");
+    if (!valid_dtype(y_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
+    const halo_scheme& s = l->s;
+    if (src->m != l->m || src->fmt != s.format_x || src->xq_rotated != (bool)s.F.middle ||
+        src->row_gran != (s.granularity == HALO_GRAN_ROW) || src->had_block != s.had_block)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared: the source context's X quantizer differs from this layer's");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t b = src->b;
+    c->valid = false;
+    c->b = b;
+    c->m = l->m;
+    c->n = l->n;
+    c->fmt = s.format_x;
+    c->xq_rotated = c->wq_rotated = s.F.middle;
+    c->row_gran = src->row_gran;
+    c->had_block = s.had_block;
+    c->xq_borrow = src->xq_codes();
+    c->xq_scale = src->xq_scale;
+    DevScalars* d = c->d();
+    if (c->row_gran) {
+        int64_t B = 1;
+        if (s.F.middle && resolve_block(l->m, s.had_block, &B, "forward") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+        if (c->wq.ensure((size_t)(l->n * l->m)) != HALO_OK || c->ws_rows.ensure((size_t)l->n * sizeof(float)) != HALO_OK ||
+            c->amax_rows.ensure((size_t)l->n * sizeof(unsigned)) != HALO_OK)
+            return HALO_ERR_CUDA;
+        {
+            ProfScope ps(PC_K1, (double)l->n * l->m * (dt_bytes(l->w_dtype) + 1), st);
+            if (!rows_v3_per_row(s.format_w, l->w_dtype, l->w, l->n, l->m, B, c->amax_rows.as<unsigned>(),
+                                 c->ws_rows.as<float>(), c->wq.as<uint8_t>(), &d->err, st))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "forward: row-granularity operands must be 32 B aligned");
+        }
+        ++l->cw;
+        c->wq_codes = c->wq.as<uint8_t>();
+        c->wq_scale = c->ws_rows.as<float>();
+        ProfScope ps(PC_GEMM, 2.0 * (double)b * l->n * l->m, st);
+        const int gr = run_gemm_v(s.format_x, c->xq_codes(), c->wq_codes, b, l->n, l->m, 1, 1, nullptr, c->xq_scale,
+                                  nullptr, c->wq_scale, y, y_dtype == HALO_DTYPE_F32 ? 0 : 1, 0, 1.0f, 0, l->n, st);
+        if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
+        c->valid = true;
+        return cuda_check("forward_shared");
+    }
+    if (l->qcodes) {
+        c->wq_codes = l->qcodes;
+        c->wq_scale = l->qscale;
+    } else {
+        const halo_status r = quantize_weight(l, c, s.F.middle, c->wq, SW, &c->wq_codes, &c->wq_scale, st);
+        if (r != HALO_OK) return r;
+    }
+    const int gr = prof_gemm(s.format_x, c->xq_codes(), c->wq_codes, b, l->n, l->m, 1, 1, c->xq_scale, c->wq_scale, y,
+                             y_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
+    if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
+    c->valid = true;
+    return cuda_check("forward_shared");
 }
 
 // out = P (fp32, rows x cols) optionally right-rotated, converted to dtype
@@ -775,21 +843,22 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
 
     // ---- gradient path (:418-439): G = (E_Y^T)_Q (XH)_Q [H^T]
     if (grad_w) {
-        const uint8_t* xq = c->xq.as<uint8_t>();
+        const uint8_t* xq = c->xq_codes();
+        const float* sxp = c->xq_scale;
         if (s.G.right && fuse_k4() && fusable_block(Bm)) {
             // grad_w = (E_Y^T)_Q (XH)_Q H^T (:433-437), the right transform in
             // the GEMM epilogue
-            int gr = prof_gemm_x(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], grad_w,
+            int gr = prof_gemm_x(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, grad_w,
                                  gw_dtype == HALO_DTYPE_F32 ? 0 : 1, Bm, 0, m, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
         } else if (s.G.right) {
             if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
             float* G = c->gscratch.as<float>();
-            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], G, 0, st);
+            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, G, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
             finish_right(G, grad_w, gw_dtype, n, m, Bm, true, st);
         } else {
-            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], &d->scale[SX], grad_w,
+            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, grad_w,
                               gw_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
         }
@@ -832,7 +901,7 @@ extern "C" halo_status halo_linear_reset_counters(halo_linear* l) {
 extern "C" halo_status halo_ctx_saved(const halo_ctx* c, const uint8_t** xq, const float** sx, const uint8_t** wq,
                                       const float** sw, int64_t* batch_rows) {
     if (!c || !c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: no forward context");
-    if (xq) *xq = c->xq.as<uint8_t>();
+    if (xq) *xq = c->xq_codes();
     if (sx) *sx = c->xq_scale ? c->xq_scale : &c->d()->scale[SX];
     if (wq) *wq = c->wq_codes;
     if (sw) *sw = c->wq_scale;

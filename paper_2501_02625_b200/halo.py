@@ -367,6 +367,18 @@ class HaloLinearLayer:
         ctx._layer_b = b
         return y
 
+    def forward_shared(self, src: SavedContext, ctx: SavedContext) -> torch.Tensor:
+        """forward() on the X already quantized in ``src`` (another layer's
+        context with the same in_features and X quantizer): the gate/up pattern
+        of a Llama MLP quantizes X once.  Identical results to forward(x)."""
+        b = src._layer_b
+        y = torch.empty((b, self.out_features), dtype=self.out_dtype, device=self.w.device)
+        check(lib().halo_linear_forward_shared(self._h, src._h, ctx._h, _ptr(y), _DT[self.out_dtype], _stream()))
+        self._last_b = b
+        ctx._layer_b = b
+        ctx._shared_src = src  # keep the borrowed codes alive
+        return y
+
     def backward(self, ctx: SavedContext, e_y: torch.Tensor, need_grad_w: bool = True,
                  e_x_dtype=None) -> BackwardResult:
         _need_cuda(e_y)

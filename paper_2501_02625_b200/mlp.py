@@ -29,10 +29,12 @@ class HaloMLP:
         self.down = halo.HaloLinearLayer(w_down, scheme, out_dtype=bf)
         self.ctx = [halo.SavedContext() for _ in range(3)]
         self._act = None
+        self.share_x = True
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         g = self.gate.forward(x, self.ctx[0])
-        u = self.up.forward(x, self.ctx[1])
+        # up_proj sees the same X under the same quantizer: reuse gate's (XH)_Q
+        u = self.up.forward_shared(self.ctx[0], self.ctx[1]) if self.share_x else self.up.forward(x, self.ctx[1])
         h = torch.empty_like(g)
         check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
         self._act = (g, u)

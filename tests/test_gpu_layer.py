@@ -176,3 +176,32 @@ def test_scheme_validation(H):
         H.scheme_from_string("halo3")
     with pytest.raises(ValueError):
         H.scheme_from_string("")
+
+
+@pytest.mark.parametrize("fmt,gran", [(0, 0), (1, 0), (0, 1)])
+def test_forward_shared_equals_forward(H, orc, fmt, gran):
+    """Llama gate/up pattern: up.forward_shared(gate_ctx) reuses gate's (XH)_Q.
+    Outputs (and, for tensor granularity, the backward) equal up.forward(x)
+    bit for bit; the input counter is not bumped."""
+    b, m, n, block = 256, 512, 384, 256
+    X, W, E = inputs(orc, b, m, n)
+    W2 = orc.bf16_round(orc.randn(n, m, 9, 1.0 / np.sqrt(m)))
+    bf = torch.bfloat16
+    sch = H.halo2(fmt, block, gran)
+    gate = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(bf), sch, out_dtype=torch.float32)
+    up = H.HaloLinearLayer(torch.from_numpy(W2).cuda().to(bf), sch, out_dtype=torch.float32)
+    up_ref = H.HaloLinearLayer(torch.from_numpy(W2).cuda().to(bf), sch, out_dtype=torch.float32)
+    x = torch.from_numpy(X).cuda().to(bf)
+    cg, cu, cr = H.SavedContext(), H.SavedContext(), H.SavedContext()
+    gate.forward(x, cg)
+    y = up.forward_shared(cg, cu)
+    y_ref = up_ref.forward(x, cr)
+    assert torch.equal(y, y_ref)
+    assert up.counters().x == 0 and up_ref.counters().x == 1
+    if gran == 0:
+        e = torch.from_numpy(E).cuda().to(bf)
+        bs, br = up.backward(cu, e), up_ref.backward(cr, e)
+        assert torch.equal(bs.e_x, br.e_x) and torch.equal(bs.grad_w, br.grad_w)
+    other = H.HaloLinearLayer(torch.from_numpy(W2[:, :256].copy()).cuda().to(bf), H.halo2(fmt, block, gran))
+    with pytest.raises(ValueError):
+        other.forward_shared(cg, H.SavedContext())  # in_features differ
