@@ -472,7 +472,7 @@ struct V4Cfg {
     static constexpr int ROW_ELEMS = 128 / sizeof(InT);       // 64 bf16 / 32 fp32
     static constexpr int CHUNK_ROWS = 1024 / ROW_ELEMS;       // 16 / 32
     static constexpr int STAGE_BYTES = 1024 * sizeof(InT);    // 2 / 4 KB
-    static constexpr int STAGES = sizeof(InT) == 2 ? 4 : 3;
+    static constexpr int STAGES = sizeof(InT) == 2 ? 2 : 3;
     static constexpr int WARPS = 4;
     static constexpr int XCH_BYTES = 4096;                    // exchange, per warp
     static constexpr size_t SMEM = 1024 + (size_t)WARPS * (STAGES * STAGE_BYTES + XCH_BYTES) + WARPS * STAGES * 8;

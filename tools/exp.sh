@@ -1,6 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for m in 0 7; do
-HALO_GEMM_DEBUG_SKIP_EPI=$m timeout 200 python tools/bench_kernels.py gemm_sweep > gpurun_out/kern$m.log 2>&1
-done
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
 echo done
