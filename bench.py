@@ -274,10 +274,12 @@ def main():
     e2e = None
     if not args.no_e2e:
         # Public-API step with host I/O: every step copies its X and dY from
-        # pinned host memory and reads dX back.  The copies run on a side
-        # stream, double-buffered, so step i+1's inputs upload (and step i's
-        # dX downloads) while step i computes - all inside the timed region.
-        cs = torch.cuda.Stream(device=dev)
+        # pinned host memory and reads dX back.  Uploads and downloads run on
+        # two side streams (both PCIe directions at once), double-buffered, so
+        # step i+1's inputs upload and step i-1's dX downloads while step i
+        # computes - all inside the timed region.
+        cs = torch.cuda.Stream(device=dev)   # uploads (H2D copy engine)
+        ds = torch.cuda.Stream(device=dev)   # downloads (D2H copy engine, full duplex with the uploads)
         main = torch.cuda.current_stream(dev)
         hx = [x.cpu().pin_memory() for _ in range(2)]
         hdy = [dy.cpu().pin_memory() for _ in range(2)]
@@ -304,12 +306,13 @@ def main():
                 main.wait_event(ready[k])
                 dx_dev = step(xs[k], dys[k])
                 used[k].record(main)
-                with torch.cuda.stream(cs):
-                    cs.wait_event(used[k])
+                with torch.cuda.stream(ds):
+                    ds.wait_event(used[k])
                     hdx[k].copy_(dx_dev, non_blocking=True)
-                    dx_dev.record_stream(cs)
-                    done[k].record(cs)
+                    dx_dev.record_stream(ds)
+                    done[k].record(ds)
             main.wait_stream(cs)
+            main.wait_stream(ds)
 
         for e in used:
             e.record(main)
@@ -332,7 +335,7 @@ def main():
                "h2d_bytes_per_step": hx[0].numel() * 2 + hdy[0].numel() * 2, "d2h_bytes_per_step": hdx[0].numel() * 2,
                "ms_per_step": e_ms / args.steps,
                "api": "paper_2501_02625_b200.mlp.HaloMLP over the C ABI (halo_linear_forward/backward); "
-                      "H2D/D2H on a side stream, double-buffered, overlapping the previous/next step"}
+                      "H2D and D2H on two side streams, double-buffered, overlapping the neighbouring steps"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -205,3 +205,28 @@ def test_forward_shared_equals_forward(H, orc, fmt, gran):
     other = H.HaloLinearLayer(torch.from_numpy(W2[:, :256].copy()).cuda().to(bf), H.halo2(fmt, block, gran))
     with pytest.raises(ValueError):
         other.forward_shared(cg, H.SavedContext())  # in_features differ
+
+
+@pytest.mark.parametrize("sch", ["halo2_int8", "halo1_fp8", "halo2_fp8"])
+def test_llama_block_runs_and_tracks_bf16(H, sch):
+    """cfg3 glue: a (small) Llama block over HALO linears (autograd Function)
+    runs forward+backward and stays close to the same block on bf16 linears."""
+    from paper_2501_02625_b200.block import LlamaBlock
+    scheme = {"halo2_int8": H.halo2(H.INT8, 256), "halo1_fp8": H.halo1(H.FP8_E4M3, 256),
+              "halo2_fp8": H.halo2(H.FP8_E4M3, 256)}[sch]
+    kw = dict(hidden=512, heads=4, kv_heads=2, inter=1024, seq=256, seed=3)
+    qb, rb = LlamaBlock(scheme, **kw), LlamaBlock(None, bf16=True, **kw)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(512, 512, generator=g, device="cuda").to(torch.bfloat16)
+    dy = (torch.randn(512, 512, generator=g, device="cuda") * 1e-2).to(torch.bfloat16)
+    outs = []
+    for blk in (qb, rb):
+        xi = x.detach().requires_grad_(True)
+        y = blk.forward(xi)
+        y.backward(dy)
+        outs.append((y.float(), xi.grad.float()))
+    rel = lambda a, b: ((a - b).norm() / b.norm()).item()
+    assert torch.isfinite(outs[0][0]).all() and torch.isfinite(outs[0][1]).all()
+    assert rel(outs[0][0] - x.float(), outs[1][0] - x.float()) < 0.1  # block update (y - x)
+    assert rel(outs[0][1], outs[1][1]) < 0.25
+    assert all(l.grad is not None and torch.isfinite(l.grad).all() for l in qb.linears())

@@ -1,5 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1
 echo done
