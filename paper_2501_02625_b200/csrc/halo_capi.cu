@@ -175,6 +175,12 @@ struct halo_linear {
     const uint8_t* qcodes = nullptr;
     const float* qscale = nullptr;
     std::atomic<int64_t> cx{0}, cw{0}, ce{0};
+    // PEFT: (WH)_Q frozen at construction (halo_linear.hpp:237-250)
+    Buffer frozen, frozen_dev;
+    ~halo_linear() {
+        frozen.release();
+        frozen_dev.release();
+    }
 };
 
 static int prof_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
@@ -503,7 +509,10 @@ extern "C" halo_status halo_qmatmul_scaled(int32_t format, const uint8_t* a, int
 // ================================================================= layer
 
 static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
-    if (s.peft) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: peft is not on the device path yet");
+    if (s.peft && !(s.F.middle && !s.F.left && !s.F.right && s.E.left && s.E.right && !s.E.middle))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: peft fixes placements F:M and E:LR");  // :242-244
+    if (s.peft && s.granularity != HALO_GRAN_TENSOR)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: peft on the device path uses tensor granularity");
     if (!s.quantize_f || !s.quantize_e || !s.quantize_g)
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
@@ -542,6 +551,32 @@ extern "C" halo_status halo_linear_create(const halo_scheme* scheme, const void*
     l->n = out_features;
     l->w = w;
     l->w_dtype = w_dtype;
+    if (scheme->peft) {
+        // frozen_wq_ = quantize(transform_right(w, spec_m)) once (:248-249)
+        if (!w) {
+            delete l;
+            return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: peft needs the weight at construction");
+        }
+        int64_t B;
+        if (resolve_block(in_features, scheme->had_block, &B, "peft") != HALO_OK ||
+            l->frozen.ensure((size_t)(out_features * in_features)) != HALO_OK ||
+            l->frozen_dev.ensure(sizeof(DevScalars)) != HALO_OK) {
+            delete l;
+            return HALO_ERR_CUDA;
+        }
+        cudaMemset(l->frozen_dev.p, 0, sizeof(DevScalars));
+        DevScalars* d = l->frozen_dev.as<DevScalars>();
+        const halo_status r = rotate_quantize_impl(w, w_dtype, out_features, in_features, B, true, scheme->format_w,
+                                                   nullptr, l->frozen.as<uint8_t>(), &d->amax[SW], &d->scale[SW],
+                                                   &d->err, (cudaStream_t)0);
+        if (r != HALO_OK || cudaStreamSynchronize((cudaStream_t)0) != cudaSuccess) {
+            delete l;
+            return r != HALO_OK ? r : fail(HALO_ERR_CUDA, "peft: freezing the weight failed");
+        }
+        l->qcodes = l->frozen.as<uint8_t>();
+        l->qscale = &d->scale[SW];
+        l->cw = 1;
+    }
     *out = l;
     return HALO_OK;
 }
@@ -560,6 +595,7 @@ extern "C" halo_status halo_linear_set_weight(halo_linear* l, const void* w, int
 
 extern "C" halo_status halo_linear_set_qweight(halo_linear* l, const uint8_t* codes, const float* scale) {
     if (!l) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight: null layer");
+    if (l->s.peft) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight: a peft layer's weight codes are frozen");
     if (codes && !scale) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight: codes without a scale");
     l->qcodes = codes;
     l->qscale = scale;
@@ -791,11 +827,14 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         c->b_pad = b_pad;
         if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK) return HALO_ERR_CUDA;
         if (c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
-        // (H_b E_Y)_Q and (E_Y)_Q in one pass (:399 and :371)
-        halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->ehq.as<uint8_t>(), c->eq.as<uint8_t>(),
-                                        &d->amax[SEH], &d->amax[SE], &d->scale[SEH], &d->scale[SE], &d->err, st);
+        // (H_b E_Y)_Q and (E_Y)_Q in one pass (:399 and :371); the plain
+        // codes only feed G, so PEFT / no-grad_w backwards skip them (:446-448)
+        const bool plain = grad_w && !s.peft;
+        halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->ehq.as<uint8_t>(),
+                                        plain ? c->eq.as<uint8_t>() : nullptr, &d->amax[SEH], &d->amax[SE],
+                                        &d->scale[SEH], &d->scale[SE], &d->err, st);
         if (r != HALO_OK) return r;
-        l->ce += 2;
+        l->ce += plain ? 2 : 1;
         float* P = c->scratch.as<float>();
         if (fuse_k4() && fusable_block(Bb)) {
             // prod^T = wq^T ehq^T (:401, transposed: M = in-features,
@@ -841,8 +880,10 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         }
     }
 
-    // ---- gradient path (:418-439): G = (E_Y^T)_Q (XH)_Q [H^T]
-    if (grad_w) {
+    // ---- gradient path (:418-439): G = (E_Y^T)_Q (XH)_Q [H^T]; a PEFT layer
+    // has no weight gradient (its U/V gradients are working-precision
+    // matmuls of the caller, :312-318)
+    if (grad_w && !s.peft) {
         const uint8_t* xq = c->xq_codes();
         const float* sxp = c->xq_scale;
         if (s.G.right && fuse_k4() && fusable_block(Bm)) {
@@ -873,6 +914,12 @@ extern "C" halo_status halo_linear_export_inference_weights(halo_linear* l, uint
     if (!l->w) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: no weight set");
     int64_t B;
     if (resolve_block(l->m, l->s.had_block, &B, "export") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    if (l->s.peft) {  // export_inference_weights returns frozen_wq_ (:333-334)
+        cudaStream_t st = (cudaStream_t)stream;
+        cudaMemcpyAsync(codes, l->qcodes, (size_t)(l->n * l->m), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(scale, l->qscale, sizeof(float), cudaMemcpyDeviceToDevice, st);
+        return cuda_check("export");
+    }
     if (l->s.granularity == HALO_GRAN_ROW)  // `scale` receives out_features floats
         return halo_rotate_quantize_rows(l->w, l->w_dtype, l->n, l->m, l->s.had_block, l->s.format_w, codes, scale,
                                          stream);

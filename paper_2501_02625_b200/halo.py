@@ -410,3 +410,51 @@ class HaloLinearLayer:
 
     def reset_counters(self):
         check(lib().halo_linear_reset_counters(self._h))
+
+
+class PeftHaloLinear:
+    """HaloLinearLayerT's PEFT form (halo_linear.hpp:236-250, 272-283, 311-319,
+    441-455): W is frozen and quantized once, (WH)_Q at construction; the
+    forward is ``(XH)_Q (WH)_Q^T + (X U^T) V^T`` and the backward
+    ``E_X = H_b (H_b^T E_Y)_Q (WH)_Q H_m^T + (E_Y V) U`` with the LoRA
+    gradients ``grad_V = E_Y^T (X U^T)``, ``grad_U = (E_Y V)^T X``.  The
+    quantized products run on the device path (scheme "halo-peft": F:M, E:LR);
+    the rank-r LoRA products are plain working-precision matmuls (torch /
+    cuBLAS), as the reference computes them in double."""
+
+    def __init__(self, w: torch.Tensor, u: torch.Tensor, v: torch.Tensor, fmt: int = INT8, had_block: int = 0,
+                 out_dtype=torch.bfloat16):
+        if u.shape[1] != w.shape[1] or v.shape[0] != w.shape[0] or u.shape[0] != v.shape[1]:
+            raise ValueError("halo layer: U/V shapes must be r x m and n x r")
+        self.layer = HaloLinearLayer(w, scheme_from_string("halo-peft", fmt, had_block), out_dtype=out_dtype)
+        self.u, self.v = u, v
+        self.out_dtype = out_dtype
+
+    @property
+    def lora_rank(self):
+        return self.u.shape[0]
+
+    def forward(self, x: torch.Tensor, ctx: SavedContext) -> torch.Tensor:
+        y = self.layer.forward(x, ctx)
+        ctx._peft_x = x  # SavedContextT keeps x for the LoRA gradients (:271)
+        if self.lora_rank > 0:
+            y = (y.float() + (x.float() @ self.u.float().t()) @ self.v.float().t()).to(self.out_dtype)
+        return y
+
+    def backward(self, ctx: SavedContext, e_y: torch.Tensor):
+        """Returns (e_x, grad_u, grad_v)."""
+        e_x = self.layer.backward(ctx, e_y, need_grad_w=False).e_x
+        x = ctx._peft_x.float()
+        ey = e_y.float()
+        ev = ey @ self.v.float()  # b x r
+        if self.lora_rank > 0:
+            e_x = (e_x.float() + ev @ self.u.float()).to(e_x.dtype)
+        grad_v = ey.t() @ (x @ self.u.float().t())
+        grad_u = ev.t() @ x
+        return e_x, grad_u, grad_v
+
+    def export_inference_weights(self):
+        return self.layer.export_inference_weights()
+
+    def counters(self) -> Counters:
+        return self.layer.counters()

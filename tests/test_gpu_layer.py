@@ -230,3 +230,37 @@ def test_llama_block_runs_and_tracks_bf16(H, sch):
     assert rel(outs[0][0] - x.float(), outs[1][0] - x.float()) < 0.1  # block update (y - x)
     assert rel(outs[0][1], outs[1][1]) < 0.25
     assert all(l.grad is not None and torch.isfinite(l.grad).all() for l in qb.linears())
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_peft_layer(H, orc, fmt):
+    """PEFT (halo_linear.hpp:236-250, 441-455): the quantized products equal
+    the HALO-2 oracle bit for bit (frozen (WH)_Q == per-step quantization of
+    an unchanged W), LoRA terms within working-precision tolerance; counters
+    w == 1 (frozen once), x == 1 per forward, e == 1 per backward; no dW."""
+    b, m, n, r, block = 256, 512, 256, 8, 256
+    X, W, E = inputs(orc, b, m, n)
+    rng = np.random.default_rng(4)
+    U = orc.bf16_round((rng.standard_normal((r, m)) * 0.05).astype(np.float32))
+    V = orc.bf16_round((rng.standard_normal((n, r)) * 0.05).astype(np.float32))
+    dev_ = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    peft = H.PeftHaloLinear(dev_(W).to(torch.bfloat16), dev_(U), dev_(V), fmt, block, out_dtype=torch.float32)
+    ctx = H.SavedContext()
+    y = peft.forward(dev_(X).to(torch.bfloat16), ctx)
+    e_x, gu, gv = peft.backward(ctx, dev_(E).to(torch.bfloat16))
+    want = orc.linear(2, fmt, block, X, W, E)
+    X64, U64, V64, E64 = (a.astype(np.float64) for a in (X, U, V, E))
+    y_w = want["Y"].astype(np.float64) + (X64 @ U64.T) @ V64.T
+    ex_w = want["EX"].astype(np.float64) + (E64 @ V64) @ U64
+    rel = lambda a, w: np.linalg.norm(a.astype(np.float64) - w) / np.linalg.norm(w)
+    tol = 1e-6 if fmt == 0 else 1e-4
+    assert rel(y.cpu().numpy(), y_w) < tol
+    assert rel(e_x.float().cpu().numpy(), ex_w) < tol
+    assert rel(gv.cpu().numpy(), E64.T @ (X64 @ U64.T)) < 1e-5
+    assert rel(gu.cpu().numpy(), (E64 @ V64).T @ X64) < 1e-5
+    c = peft.counters()
+    assert (c.x, c.w, c.e) == (1, 1, 1)
+    codes, s = peft.export_inference_weights()
+    wq, ws = orc.quantize(orc.fwht_rows(W, block), fmt)
+    assert s.item() == ws[0]
+    assert np.array_equal(codes.cpu().numpy().view(np.uint8), orc.codes_to_bytes(wq, fmt).view(np.uint8))
