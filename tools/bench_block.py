@@ -56,6 +56,54 @@ def run(name, scheme, bf16, args):
             "note": "step = block forward + backward (5 projections, RMSNorm, RoPE, causal GQA SDPA attention)"}
 
 
+def run_mlp(name, scheme, args):
+    """Module-level comparison on cfg2's MLP (8192 tokens): HaloMLP (the
+    bench.py path) vs the same MLP on bf16 cuBLAS linears with torch autograd."""
+    import torch.nn.functional as F
+    from paper_2501_02625_b200.mlp import HaloMLP
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    bf = torch.bfloat16
+    H, I, T = 4096, 14336, 8192
+    wg = (torch.randn(I, H, generator=g, device=dev) / H ** 0.5).to(bf)
+    wu = (torch.randn(I, H, generator=g, device=dev) / H ** 0.5).to(bf)
+    wd = (torch.randn(H, I, generator=g, device=dev) / I ** 0.5).to(bf)
+    x = torch.randn(T, H, generator=g, device=dev).to(bf)
+    dy = (torch.randn(T, H, generator=g, device=dev) * 1e-3).to(bf)
+    if scheme is None:
+        ws = [w.clone().requires_grad_(True) for w in (wg, wu, wd)]
+
+        def step():
+            xi = x.detach().requires_grad_(True)
+            y = F.linear(F.silu(F.linear(xi, ws[0])) * F.linear(xi, ws[1]), ws[2])
+            y.backward(dy)
+            for w in ws:
+                w.grad = None
+    else:
+        mlp = HaloMLP(wg, wu, wd, scheme)
+
+        def step():
+            mlp.forward(x)
+            mlp.backward(dy)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step()
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    ms = tot / args.steps
+    return {"config": "MLP " + name, "tokens": T, "ms_per_step": round(ms, 3), "tokens_per_s": round(T / ms * 1e3),
+            "gemm_TOPS_equiv": round(6.0 * T * 3 * H * I / ms / 1e9, 1),
+            "note": "cfg2 Llama-3-8B MLP fwd+bwd; bf16 = F.linear (cuBLAS) + torch autograd"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
@@ -69,6 +117,11 @@ def main():
     base = res[0]["ms_per_step"]
     for r in res:
         r["speedup_vs_bf16"] = round(base / r["ms_per_step"], 3)
+        print(json.dumps(r), flush=True)
+    mres = [run_mlp("bf16 (cuBLAS linears)", None, args), run_mlp("HALO-2 INT8 block 256", halo.halo2(halo.INT8, 256), args),
+            run_mlp("HALO-2 FP8-E4M3 block 256", halo.halo2(halo.FP8_E4M3, 256), args)]
+    for r in mres:
+        r["speedup_vs_bf16"] = round(mres[0]["ms_per_step"] / r["ms_per_step"], 3)
         print(json.dumps(r), flush=True)
 
 
