@@ -238,6 +238,16 @@ HALO_API halo_status halo_device_copy(void* dst, const void* src, int64_t bytes,
 HALO_API halo_status halo_swiglu_forward(const void* g, const void* u, void* h, int64_t n, halo_stream_t stream);
 HALO_API halo_status halo_swiglu_backward(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n,
                                           halo_stream_t stream);
+/* halo_swiglu_backward over [b x cols] fused with phase A (the absmax
+ * pass) of the error-path quantization of both input projections
+ * (halo_linear.hpp:393-399 and :371 for `gate` and `up`, HALO-2 family:
+ * E.left).  The following halo_linear_backward(gate, gctx, dg, ...) and
+ * halo_linear_backward(up, uctx, du, ...) — called with these exact dg / du
+ * buffers and batch — reuse the absmax words instead of re-reading dg / du.
+ * Other schemes: identical to halo_swiglu_backward. */
+HALO_API halo_status halo_swiglu_backward_absmax(const halo_linear* gate, halo_ctx* gctx, const halo_linear* up,
+                                                 halo_ctx* uctx, const void* dh, const void* g, const void* u,
+                                                 void* dg, void* du, int64_t b, int64_t cols, halo_stream_t stream);
 /* out = a + b elementwise (f32 or bf16), n % 8 == 0 */
 HALO_API halo_status halo_add(const void* a, const void* b, void* out, int32_t dtype, int64_t n,
                               halo_stream_t stream);

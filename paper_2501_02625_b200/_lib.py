@@ -132,10 +132,11 @@ def lib():
     L.halo_device_copy.argtypes = [_vp, _vp, _i64, _vp]
     L.halo_swiglu_forward.argtypes = [_vp, _vp, _vp, _i64, _vp]
     L.halo_swiglu_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _vp]
+    L.halo_swiglu_backward_absmax.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]
     L.halo_add.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp]
     L.halo_profile_enable.argtypes = [C.c_int]
     L.halo_profile_read.argtypes = [C.POINTER(Profile)]
-    for fn in ("halo_swiglu_forward", "halo_swiglu_backward", "halo_add", "halo_profile_enable",
+    for fn in ("halo_swiglu_forward", "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
                "halo_profile_read"):
         getattr(L, fn).restype = C.c_int
     for fn in ("halo_scheme_from_string", "halo_rotate_quantize", "halo_rotate_absmax",
@@ -177,5 +178,6 @@ EXPORTS = (
     "halo_linear_forward", "halo_linear_backward", "halo_linear_export_inference_weights",
     "halo_linear_counters", "halo_linear_reset_counters", "halo_ctx_saved",
     "halo_ctx_error_operands", "halo_ctx_check", "halo_device_copy", "halo_swiglu_forward",
-    "halo_swiglu_backward", "halo_add", "halo_profile_enable", "halo_profile_read",
+    "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
+    "halo_profile_read",
 )

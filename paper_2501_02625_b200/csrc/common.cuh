@@ -85,6 +85,21 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // absmax of non-negative floats via the integer order of their bit patterns
+// SwiGLU glue (the Llama MLP's activation; not part of the reference path).
+// Every rounding is spelled out so the fused kernels (K1 swiglu-absmax, K2
+// swiglu-absmax) and the stand-alone glue kernels produce identical bits.
+__device__ __forceinline__ float swiglu_sigmoid(float g) { return __frcp_rn(__fadd_rn(1.0f, __expf(-g))); }
+// h = silu(g) * u
+__device__ __forceinline__ float swiglu_fwd1(float g, float u) {
+    return __fmul_rn(__fmul_rn(g, swiglu_sigmoid(g)), u);
+}
+// du = dh * silu(g);  dg = dh * u * s * (1 + g * (1 - s)),  s = sigmoid(g)
+__device__ __forceinline__ void swiglu_bwd1(float dh, float g, float u, float& dg, float& du) {
+    const float s = swiglu_sigmoid(g);
+    du = __fmul_rn(__fmul_rn(dh, g), s);
+    dg = __fmul_rn(__fmul_rn(__fmul_rn(dh, u), s), __fmaf_rn(g, __fadd_rn(1.0f, -s), 1.0f));
+}
+
 __device__ __forceinline__ void atomic_absmax(unsigned* slot, float v) {
     atomicMax(slot, __float_as_uint(v));
 }

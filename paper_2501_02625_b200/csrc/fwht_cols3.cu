@@ -23,7 +23,10 @@
 // (max(|u+v|,|u-v|) = |u|+|v| exactly) and propagate NaN.
 #include "common.cuh"
 #include "halo_internal.h"
+#include "sm100.cuh"
 
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 namespace halo_b200 {
@@ -148,20 +151,29 @@ enum : int { C3_ABSMAX = 0, C3_QUANT = 1 };
 constexpr int C3_COLS = 32, C3_ROWS = 256;  // one CTA tile
 constexpr int C3_WARPS = 4;
 constexpr size_t C3_SMEM = (size_t)C3_ROWS * C3_COLS * sizeof(float);  // 32 KB fp32 exchange
+constexpr int C3_STAGE = C3_ROWS * C3_COLS * 2;                         // 16 KB bf16 TMA stage
+constexpr int C3_TS = 1;                                                // TMA ring depth (bf16)
 
 }  // namespace
 
-template <int LB, typename InT, int FMT, int MODE, bool SUP_R, bool SUP_P>
+// TS > 0 (bf16 input): the CTA's tiles stream through a TS-deep ring of
+// 16 KB shared-memory stages filled by TMA (box 32 columns x 256 rows, rows
+// past b and columns past `cols` zero-filled by the copy engine); thread 0
+// refills a stage right after the tile's first exchange barrier, when every
+// thread has read it, so the next tiles' HBM latency hides behind compute.
+template <int LB, typename InT, int FMT, int MODE, bool SUP_R, bool SUP_P, int TS>
 __global__ void __launch_bounds__(128, 4)
-    k_cols_v3(const InT* __restrict__ in, int64_t b, int64_t rows_pad, int64_t cols, float norm, unsigned* amax_r,
+    k_cols_v3(const __grid_constant__ CUtensorMap tm, const InT* __restrict__ in, int64_t b, int64_t rows_pad, int64_t cols, float norm, unsigned* amax_r,
               unsigned* amax_p, const float* sup_r, const float* sup_p, uint8_t* __restrict__ codes_r,
               uint8_t* __restrict__ codes_p, unsigned* err, float* sro, float* spo) {
     constexpr bool FOLD = (LB % 2) == 0;
     constexpr int P1 = LB < 4 ? LB : 4;  // row bits handled in phase 1
     constexpr int P2 = LB > 4 ? LB - 4 : 0;
-    extern __shared__ __align__(16) float4 X4[];  // [256 rows][8 float4]
+    extern __shared__ __align__(128) float4 X4[];  // [256 rows][8 float4], then the TMA stages
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int cg = l & 7, q = 4 * w + (l >> 3);  // 4-column group, row group
+    uint8_t* const stg = reinterpret_cast<uint8_t*>(X4) + C3_SMEM;
+    uint64_t* const bars = reinterpret_cast<uint64_t*>(stg + (TS > 0 ? TS : 0) * C3_STAGE);
     Quant<FMT, SUP_R> qr;
     Quant<FMT, SUP_P> qp;
     if constexpr (MODE == C3_QUANT) {
@@ -202,14 +214,32 @@ __global__ void __launch_bounds__(128, 4)
         }
     };
 
-    auto run = [&](auto edge_tag, int64_t r0, int64_t c0) {
+    // TMA ring: refill stage s with tile `next` once every thread has read it
+    auto refill = [&](int s, int64_t next) {
+        if constexpr (TS > 0) {
+            if (threadIdx.x == 0 && next >= 0) {
+                mbar_expect_tx(&bars[s], C3_STAGE);
+                tma_load_2d(stg + s * C3_STAGE, &tm, &bars[s], (int)((next % ct) * C3_COLS),
+                            (int)((next / ct) * C3_ROWS));
+            }
+        }
+    };
+    auto run = [&](auto edge_tag, int64_t r0, int64_t c0, int s, int64_t next) {
         constexpr bool EDGE = decltype(edge_tag)::value;
         const int64_t col = c0 + 4 * cg;
         const bool cok = !EDGE || col < cols;
         const int64_t row1 = r0 + 16 * q;
         // ---------------- phase 1: rows 16q + m
         float2 v[16][2];
-        {
+        if constexpr (TS > 0) {
+            const uint8_t* p = stg + s * C3_STAGE + (16 * q) * (C3_COLS * 2) + cg * 8;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const uint2 r = *reinterpret_cast<const uint2*>(p + m * (C3_COLS * 2));
+                v[m][0] = make_float2(__uint_as_float(r.x << 16), __uint_as_float(r.x & 0xFFFF0000u));
+                v[m][1] = make_float2(__uint_as_float(r.y << 16), __uint_as_float(r.y & 0xFFFF0000u));
+            }
+        } else {
             const InT* p = in + row1 * cols + col;
 #pragma unroll
             for (int m = 0; m < 16; ++m) {
@@ -273,6 +303,10 @@ __global__ void __launch_bounds__(128, 4)
             }
         }
         if constexpr (P2 == 0) {
+            if constexpr (TS > 0) {
+                __syncthreads();  // stage s fully read
+                refill(s, next);
+            }
             if constexpr (MODE == C3_QUANT) emit_rot(edge_tag, v, row1, 1, col, cok);
         } else {
             // ---------------- exchange (fp32, row-major [256][64])
@@ -280,6 +314,7 @@ __global__ void __launch_bounds__(128, 4)
             for (int m = 0; m < 16; ++m)
                 X4[(16 * q + m) * 8 + cg] = make_float4(v[m][0].x, v[m][0].y, v[m][1].x, v[m][1].y);
             __syncthreads();
+            refill(s, next);  // stage s fully read (phase 1 precedes the barrier)
             // ---------------- phase 2: thread (cg, mm = q) takes rows 16i + mm
             float2 u[16][2];
 #pragma unroll
@@ -312,11 +347,33 @@ __global__ void __launch_bounds__(128, 4)
         }
     };
 
-    for (int64_t tile = blockIdx.x; tile < ct * rt; tile += gridDim.x) {
+    const int64_t ntiles = ct * rt;
+    if constexpr (TS > 0) {
+        if (threadIdx.x == 0) {
+            tma_prefetch_desc(&tm);
+            for (int s = 0; s < TS; ++s) mbar_init(&bars[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int s = 0; s < TS; ++s) {
+                const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+                refill(s, t < ntiles ? t : -1);
+            }
+        }
+        __syncthreads();
+    }
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int64_t r0 = (tile / ct) * C3_ROWS, c0 = (tile % ct) * C3_COLS;
         const bool interior = r0 + C3_ROWS <= b && r0 + C3_ROWS <= rows_pad && c0 + C3_COLS <= cols;
-        if (interior) run(std::false_type{}, r0, c0);
-        else run(std::true_type{}, r0, c0);
+        int s = 0;
+        int64_t next = -1;
+        if constexpr (TS > 0) {
+            s = it % TS;
+            mbar_wait(&bars[s], (uint32_t)(it / TS) & 1u);
+            const int64_t nt = tile + (int64_t)TS * gridDim.x;
+            next = nt < ntiles ? nt : -1;
+        }
+        if (interior) run(std::false_type{}, r0, c0, s, next);
+        else run(std::true_type{}, r0, c0, s, next);
     }
     if constexpr (MODE == C3_ABSMAX) {
 #pragma unroll
@@ -333,23 +390,217 @@ __global__ void __launch_bounds__(128, 4)
     }
 }
 
+// ------------------------------------------------------------------ K2 + SwiGLU backward
+// Phase A of K2 for both MLP input projections, fused with the SwiGLU
+// backward glue: dG, dU are computed from (dH, G, U) on the fly
+// (swiglu_bwd1, the exact formula of the stand-alone glue kernel), stored in
+// bf16 for K2's quantize passes, and the rotated and plain absmax words of
+// both come out of the same pass — one read of dH, G, U replaces the glue
+// kernel plus two K2 absmax passes over dG and dU.
+
+// rotated + plain absmax of one 256 x 32 tile held as thread (cg, q)'s rows
+// 16q + m (phase 1 layout of k_cols_v3)
+template <int LB>
+__device__ __forceinline__ void c3_tile_absmax(float2 (&v)[16][2], float4* X4, int q, int cg, float& am_r, float& am_p) {
+    constexpr int P1 = LB < 4 ? LB : 4;
+    constexpr int P2 = LB > 4 ? LB - 4 : 0;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        am_p = c3_max3nan(am_p, fabsf(v[m][0].x), fabsf(v[m][0].y));
+        am_p = c3_max3nan(am_p, fabsf(v[m][1].x), fabsf(v[m][1].y));
+    }
+#pragma unroll
+    for (int t = 0; t < P1; ++t) {
+        const int h = 1 << t;
+        const bool last = P2 == 0 && t == P1 - 1;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            if ((m & h) == 0) {
+                if (last) {
+                    am_r = c3_max3nan(am_r, fabsf(v[m][0].x) + fabsf(v[m + h][0].x), fabsf(v[m][0].y) + fabsf(v[m + h][0].y));
+                    am_r = c3_max3nan(am_r, fabsf(v[m][1].x) + fabsf(v[m + h][1].x), fabsf(v[m][1].y) + fabsf(v[m + h][1].y));
+                } else {
+                    c3_bfly(v[m][0], v[m + h][0]);
+                    c3_bfly(v[m][1], v[m + h][1]);
+                }
+            }
+        }
+    }
+    if constexpr (LB == 0) {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            am_r = c3_max3nan(am_r, fabsf(v[m][0].x), fabsf(v[m][0].y));
+            am_r = c3_max3nan(am_r, fabsf(v[m][1].x), fabsf(v[m][1].y));
+        }
+    }
+    if constexpr (P2 > 0) {
+#pragma unroll
+        for (int m = 0; m < 16; ++m)
+            X4[(16 * q + m) * 8 + cg] = make_float4(v[m][0].x, v[m][0].y, v[m][1].x, v[m][1].y);
+        __syncthreads();
+        float2 w[16][2];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float4 f = X4[(16 * i + q) * 8 + cg];
+            w[i][0] = make_float2(f.x, f.y);
+            w[i][1] = make_float2(f.z, f.w);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < P2; ++t) {
+            const int h = 1 << t;
+            const bool last = t == P2 - 1;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if ((i & h) == 0) {
+                    if (last) {
+                        am_r = c3_max3nan(am_r, fabsf(w[i][0].x) + fabsf(w[i + h][0].x), fabsf(w[i][0].y) + fabsf(w[i + h][0].y));
+                        am_r = c3_max3nan(am_r, fabsf(w[i][1].x) + fabsf(w[i + h][1].x), fabsf(w[i][1].y) + fabsf(w[i + h][1].y));
+                    } else {
+                        c3_bfly(w[i][0], w[i + h][0]);
+                        c3_bfly(w[i][1], w[i + h][1]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void c3_unpack(const uint2 (&pk)[16], float2 (&v)[16][2]) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        v[m][0] = make_float2(__uint_as_float(pk[m].x << 16), __uint_as_float(pk[m].x & 0xFFFF0000u));
+        v[m][1] = make_float2(__uint_as_float(pk[m].y << 16), __uint_as_float(pk[m].y & 0xFFFF0000u));
+    }
+}
+
+template <int LB>
+__global__ void __launch_bounds__(128, 3)
+    k_cols_swiglu_absmax(const __nv_bfloat16* __restrict__ dH, const __nv_bfloat16* __restrict__ G,
+                         const __nv_bfloat16* __restrict__ U, __nv_bfloat16* __restrict__ dG,
+                         __nv_bfloat16* __restrict__ dU, int64_t b, int64_t rows_pad, int64_t cols, float norm,
+                         unsigned* am_gr, unsigned* am_gp, unsigned* am_ur, unsigned* am_up, unsigned* err) {
+    extern __shared__ __align__(16) float4 X4[];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int cg = l & 7, q = 4 * w + (l >> 3);
+    float gr = 0.f, gp = 0.f, ur = 0.f, up = 0.f;
+    const int64_t ct = (cols + C3_COLS - 1) / C3_COLS, rt = (rows_pad + C3_ROWS - 1) / C3_ROWS;
+    for (int64_t tile = blockIdx.x; tile < ct * rt; tile += gridDim.x) {
+        const int64_t r0 = (tile / ct) * C3_ROWS, c0 = (tile % ct) * C3_COLS;
+        const int64_t col = c0 + 4 * cg;
+        const bool cok = col < cols;
+        const int64_t row1 = r0 + 16 * q;
+        uint2 pg[16], pu[16];
+        {
+            const int64_t off = row1 * cols + col;
+            const uint2* ph = reinterpret_cast<const uint2*>(dH + off);
+            const uint2* pgi = reinterpret_cast<const uint2*>(G + off);
+            const uint2* pui = reinterpret_cast<const uint2*>(U + off);
+            uint2* og = reinterpret_cast<uint2*>(dG + off);
+            uint2* ou = reinterpret_cast<uint2*>(dU + off);
+            const int64_t st = cols / 4;  // uint2 per row
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const bool ok = cok && row1 + m < b;
+                uint2 rh = make_uint2(0, 0), rg = rh, ru = rh;
+                if (ok) {
+                    rh = __ldg(ph + m * st);
+                    rg = __ldg(pgi + m * st);
+                    ru = __ldg(pui + m * st);
+                }
+                const uint32_t hw[2] = {rh.x, rh.y}, gw[2] = {rg.x, rg.y}, uw[2] = {ru.x, ru.y};
+                uint32_t dgw[2], duw[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    float g0, g1, u0, u1;
+                    swiglu_bwd1(__uint_as_float(hw[j] << 16), __uint_as_float(gw[j] << 16), __uint_as_float(uw[j] << 16), g0, u0);
+                    swiglu_bwd1(__uint_as_float(hw[j] & 0xFFFF0000u), __uint_as_float(gw[j] & 0xFFFF0000u),
+                                __uint_as_float(uw[j] & 0xFFFF0000u), g1, u1);
+                    dgw[j] = pack_bf16x2(g0, g1);
+                    duw[j] = pack_bf16x2(u0, u1);
+                }
+                pg[m] = make_uint2(dgw[0], dgw[1]);
+                pu[m] = make_uint2(duw[0], duw[1]);
+                if (ok) {
+                    og[m * st] = pg[m];
+                    ou[m * st] = pu[m];
+                }
+            }
+        }
+        {
+            float2 v[16][2];
+            c3_unpack(pg, v);
+            c3_tile_absmax<LB>(v, X4, q, cg, gr, gp);
+        }
+        {
+            float2 v[16][2];
+            c3_unpack(pu, v);
+            c3_tile_absmax<LB>(v, X4, q, cg, ur, up);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gr = c3_max3nan(gr, __shfl_xor_sync(0xffffffffu, gr, o), 0.f);
+        gp = c3_max3nan(gp, __shfl_xor_sync(0xffffffffu, gp, o), 0.f);
+        ur = c3_max3nan(ur, __shfl_xor_sync(0xffffffffu, ur, o), 0.f);
+        up = c3_max3nan(up, __shfl_xor_sync(0xffffffffu, up, o), 0.f);
+    }
+    gr *= norm;  // monotone: max(fl(|x| * norm)) == fl(max|x| * norm)
+    ur *= norm;
+    if (l == 0) {
+        atomic_absmax(am_gr, fabsf(gr));
+        atomic_absmax(am_gp, fabsf(gp));
+        atomic_absmax(am_ur, fabsf(ur));
+        atomic_absmax(am_up, fabsf(up));
+        constexpr float F = 3.402823466e38f;
+        if (!(gr <= F) || !(gp <= F) || !(ur <= F) || !(up <= F))
+            atomicOr(err, ERRF_NONFINITE);
+    }
+}
+
 namespace {
 
-template <int LB, typename InT, int FMT, int MODE, bool SR, bool SP>
-void c3_launch(const InT* in, int64_t b, int64_t rows_pad, int64_t cols, unsigned* ar, unsigned* ap, const float* sr,
-               const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err, float* sro, float* spo, cudaStream_t st) {
-    auto kern = k_cols_v3<LB, InT, FMT, MODE, SR, SP>;
+template <int LB, typename InT, int FMT, int MODE, bool SR, bool SP, int TS>
+void c3_go(const CUtensorMap& tm, const InT* in, int64_t b, int64_t rows_pad, int64_t cols, unsigned* ar, unsigned* ap,
+           const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err, float* sro, float* spo,
+           cudaStream_t st) {
+    auto kern = k_cols_v3<LB, InT, FMT, MODE, SR, SP, TS>;
+    const size_t smem = C3_SMEM + (size_t)TS * C3_STAGE + (TS > 0 ? 8 * TS : 0);
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C3_SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C3_WARPS, C3_SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C3_WARPS, smem);
         if (per_sm < 1) per_sm = 1;
     }
     const int64_t tiles = ((cols + C3_COLS - 1) / C3_COLS) * ((rows_pad + C3_ROWS - 1) / C3_ROWS);
     const int64_t cap = (int64_t)num_sms() * per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    kern<<<grid, 32 * C3_WARPS, C3_SMEM, st>>>(in, b, rows_pad, cols, hadamard_norm(int64_t(1) << LB), ar, ap, sr, sp, cr, cp,
-                                     err, sro, spo);
+    kern<<<grid, 32 * C3_WARPS, smem, st>>>(tm, in, b, rows_pad, cols, hadamard_norm(int64_t(1) << LB), ar, ap, sr, sp,
+                                            cr, cp, err, sro, spo);
+}
+
+inline bool c3_use_tma() {
+    static const int v = [] {
+        const char* e = getenv("HALO_K2_TMA");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+template <int LB, typename InT, int FMT, int MODE, bool SR, bool SP>
+void c3_launch(const InT* in, int64_t b, int64_t rows_pad, int64_t cols, unsigned* ar, unsigned* ap, const float* sr,
+               const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err, float* sro, float* spo, cudaStream_t st) {
+    CUtensorMap tm;
+    if constexpr (sizeof(InT) == 2) {
+        // TMA ring: row pitch a multiple of 16 B, 16 B aligned base
+        if (c3_use_tma() && cols % 8 == 0 && (uintptr_t)in % 16 == 0 &&
+            encode_2d_plain(&tm, 1, in, (uint64_t)cols, (uint64_t)b, (uint64_t)cols * 2, C3_COLS, C3_ROWS)) {
+            c3_go<LB, InT, FMT, MODE, SR, SP, C3_TS>(tm, in, b, rows_pad, cols, ar, ap, sr, sp, cr, cp, err, sro, spo, st);
+            return;
+        }
+    }
+    memset(&tm, 0, sizeof(tm));
+    c3_go<LB, InT, FMT, MODE, SR, SP, 0>(tm, in, b, rows_pad, cols, ar, ap, sr, sp, cr, cp, err, sro, spo, st);
 }
 
 template <int LB>
@@ -390,6 +641,45 @@ bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t
     case 6: c3_dispatch<6>(mode, fmt, in_dtype, in, b, rows_pad, cols, ar, ap, sr, sp, cr, cp, err, sro, spo, st); break;
     case 7: c3_dispatch<7>(mode, fmt, in_dtype, in, b, rows_pad, cols, ar, ap, sr, sp, cr, cp, err, sro, spo, st); break;
     default: c3_dispatch<8>(mode, fmt, in_dtype, in, b, rows_pad, cols, ar, ap, sr, sp, cr, cp, err, sro, spo, st); break;
+    }
+    return true;
+}
+
+// K2 phase A for the MLP's gate and up projections fused with the SwiGLU
+// backward: dG, dU (bf16, [b x cols]) written, absmax words (rotated over
+// blocks of B rows of the b_pad-padded token axis, and plain) of both.
+bool cols_swiglu_absmax(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t b, int64_t rows_pad,
+                        int64_t cols, int64_t B, unsigned* gr, unsigned* gp, unsigned* ur, unsigned* up, unsigned* err,
+                        cudaStream_t st) {
+    if (B < 1 || B > 256 || (B & (B - 1)) || cols % 4) return false;
+    for (const void* p : {dh, g, u, (const void*)dg, (const void*)du})
+        if ((uintptr_t)p % 8) return false;
+    int lb = 0;
+    while ((int64_t(1) << lb) < B) ++lb;
+    const int64_t tiles = ((cols + C3_COLS - 1) / C3_COLS) * ((rows_pad + C3_ROWS - 1) / C3_ROWS);
+    auto go = [&](auto kern) {
+        static int per_sm = 0;
+        if (!per_sm) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C3_SMEM);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C3_WARPS, C3_SMEM);
+            if (per_sm < 1) per_sm = 1;
+        }
+        const int64_t cap = (int64_t)num_sms() * per_sm;
+        kern<<<(unsigned)(tiles < cap ? tiles : cap), 32 * C3_WARPS, C3_SMEM, st>>>(
+            static_cast<const __nv_bfloat16*>(dh), static_cast<const __nv_bfloat16*>(g),
+            static_cast<const __nv_bfloat16*>(u), static_cast<__nv_bfloat16*>(dg), static_cast<__nv_bfloat16*>(du), b,
+            rows_pad, cols, hadamard_norm(B), gr, gp, ur, up, err);
+    };
+    switch (lb) {
+    case 0: go(k_cols_swiglu_absmax<0>); break;
+    case 1: go(k_cols_swiglu_absmax<1>); break;
+    case 2: go(k_cols_swiglu_absmax<2>); break;
+    case 3: go(k_cols_swiglu_absmax<3>); break;
+    case 4: go(k_cols_swiglu_absmax<4>); break;
+    case 5: go(k_cols_swiglu_absmax<5>); break;
+    case 6: go(k_cols_swiglu_absmax<6>); break;
+    case 7: go(k_cols_swiglu_absmax<7>); break;
+    default: go(k_cols_swiglu_absmax<8>); break;
     }
     return true;
 }

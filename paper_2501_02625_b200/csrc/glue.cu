@@ -9,7 +9,6 @@
 
 namespace halo_b200 {
 
-__device__ __forceinline__ float sigmoidf_(float g) { return 1.0f / (1.0f + __expf(-g)); }
 
 // H = silu(G) * U, all bf16, n % 8 == 0
 __global__ void __launch_bounds__(256) k_swiglu_fwd(const __nv_bfloat16* __restrict__ G,
@@ -21,7 +20,7 @@ __global__ void __launch_bounds__(256) k_swiglu_fwd(const __nv_bfloat16* __restr
         load8(G + i, g);
         load8(U + i, u);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) h[j] = g[j] * sigmoidf_(g[j]) * u[j];
+        for (int j = 0; j < 8; ++j) h[j] = swiglu_fwd1(g[j], u[j]);
         store8(H + i, h);
     }
 }
@@ -39,11 +38,7 @@ __global__ void __launch_bounds__(256) k_swiglu_bwd(const __nv_bfloat16* __restr
         load8(G + i, g);
         load8(U + i, u);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float s = sigmoidf_(g[j]);
-            du[j] = dh[j] * g[j] * s;
-            dg[j] = dh[j] * u[j] * s * (1.0f + g[j] * (1.0f - s));
-        }
+        for (int j = 0; j < 8; ++j) swiglu_bwd1(dh[j], g[j], u[j], dg[j], du[j]);
         store8(dG + i, dg);
         store8(dU + i, du);
     }

@@ -159,6 +159,10 @@ struct halo_ctx {
     const float* xq_scale = nullptr;
     const uint8_t* xq_borrow = nullptr;  // (XH)_Q shared from another context (halo_linear_forward_shared)
     int64_t had_block = 0;
+    // halo_swiglu_backward_absmax: the absmax words of E_Y (SEH, SE) were
+    // computed by the fused pass for this exact E_Y buffer and batch
+    const void* e_amax_src = nullptr;
+    int64_t e_amax_b = 0;
     const uint8_t* xq_codes() const { return xq_borrow ? xq_borrow : xq.as<uint8_t>(); }
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
@@ -382,10 +386,11 @@ extern "C" halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_
 
 static halo_status left_quant_impl(const void* e, int32_t dt, int64_t b, int64_t n, int64_t B, int64_t b_pad,
                                    int32_t fmt, uint8_t* codes_rot, uint8_t* codes_plain, unsigned* amax_r,
-                                   unsigned* amax_p, float* s_r, float* s_p, unsigned* err, cudaStream_t st) {
-    cudaMemsetAsync(amax_r, 0, sizeof(unsigned), st);
-    cudaMemsetAsync(amax_p, 0, sizeof(unsigned), st);
-    {
+                                   unsigned* amax_p, float* s_r, float* s_p, unsigned* err, cudaStream_t st,
+                                   bool have_amax = false) {
+    if (!have_amax) {
+        cudaMemsetAsync(amax_r, 0, sizeof(unsigned), st);
+        cudaMemsetAsync(amax_p, 0, sizeof(unsigned), st);
         ProfScope ps(PC_K2, 0.0, st);
         run_cols(e, dt, b, b_pad, n, B, 0, fmt, amax_r, amax_p, nullptr, nullptr, nullptr, nullptr, nullptr, 0, err,
                  nullptr, nullptr, st);
@@ -646,6 +651,7 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     const bool rot = s.F.middle;
     // ctx = SavedContextT{}  (:270-273)
     c->valid = false;
+    c->e_amax_src = nullptr;
     c->b = b;
     c->m = l->m;
     c->n = l->n;
@@ -732,6 +738,7 @@ extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t b = src->b;
     c->valid = false;
+    c->e_amax_src = nullptr;
     c->b = b;
     c->m = l->m;
     c->n = l->n;
@@ -830,9 +837,13 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         // (H_b E_Y)_Q and (E_Y)_Q in one pass (:399 and :371); the plain
         // codes only feed G, so PEFT / no-grad_w backwards skip them (:446-448)
         const bool plain = grad_w && !s.peft;
+        // absmax words already produced by halo_swiglu_backward_absmax for
+        // this E_Y: skip K2's phase A
+        const bool have_amax = c->e_amax_src == e_y && c->e_amax_b == b && e_dtype == HALO_DTYPE_BF16;
+        c->e_amax_src = nullptr;
         halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->ehq.as<uint8_t>(),
                                         plain ? c->eq.as<uint8_t>() : nullptr, &d->amax[SEH], &d->amax[SE],
-                                        &d->scale[SEH], &d->scale[SE], &d->err, st);
+                                        &d->scale[SEH], &d->scale[SE], &d->err, st, have_amax);
         if (r != HALO_OK) return r;
         l->ce += plain ? 2 : 1;
         float* P = c->scratch.as<float>();
@@ -1007,6 +1018,52 @@ extern "C" halo_status halo_swiglu_backward(const void* dh, const void* g, const
     cudaStream_t st = (cudaStream_t)stream;
     ProfScope ps(PC_GLUE, (double)n * 10, st);
     run_swiglu_bwd(dh, g, u, dg, du, n, st);
+    return cuda_check("swiglu_backward");
+}
+
+// SwiGLU backward fused with K2's phase A of both input projections (HALO-2
+// family: E.left).  dG, dU are written as by halo_swiglu_backward and the
+// absmax words of (H_b dG), dG, (H_b dU), dU land in the two contexts, so
+// the following halo_linear_backward(gate, gctx, dG, ...) and
+// halo_linear_backward(up, uctx, dU, ...) skip their absmax passes.  For
+// schemes without the left rotation this is halo_swiglu_backward.
+extern "C" halo_status halo_swiglu_backward_absmax(const halo_linear* gate, halo_ctx* gctx, const halo_linear* up,
+                                                   halo_ctx* uctx, const void* dh, const void* g, const void* u,
+                                                   void* dg, void* du, int64_t b, int64_t cols, halo_stream_t stream) {
+    if (!gate || !gctx || !up || !uctx || !dh || !g || !u || !dg || !du || b <= 0 || cols <= 0)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "swiglu_backward_absmax: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    gctx->e_amax_src = nullptr;
+    uctx->e_amax_src = nullptr;
+    const bool fuse = gate->s.E.left && up->s.E.left && gate->s.had_block == up->s.had_block && gate->n == cols &&
+                      up->n == cols && gctx->valid && uctx->valid && gctx->b == b && uctx->b == b && cols % 4 == 0;
+    if (fuse) {
+        const int64_t b_pad = halo_padded_batch(b, gate->s.had_block);
+        int64_t Bb;
+        if (resolve_block(b_pad, gate->s.had_block, &Bb, "swiglu backward (token dim)") != HALO_OK)
+            return HALO_ERR_INVALID_ARGUMENT;
+        DevScalars* dgs = gctx->d();
+        DevScalars* dus = uctx->d();
+        cudaMemsetAsync(&dgs->amax[SEH], 0, 2 * sizeof(unsigned), st);  // SEH, SE adjacent
+        cudaMemsetAsync(&dus->amax[SEH], 0, 2 * sizeof(unsigned), st);
+        bool ok;
+        {
+            ProfScope ps(PC_GLUE, (double)b * cols * 10.0, st);
+            ok = cols_swiglu_absmax(dh, g, u, dg, du, b, b_pad, cols, Bb, &dgs->amax[SEH], &dgs->amax[SE],
+                                    &dus->amax[SEH], &dus->amax[SE], &dgs->err, st);
+        }
+        if (ok) {
+            gctx->e_amax_src = dg;
+            gctx->e_amax_b = b;
+            uctx->e_amax_src = du;
+            uctx->e_amax_b = b;
+            return cuda_check("swiglu_backward_absmax");
+        }
+    }
+    {
+        ProfScope ps(PC_GLUE, (double)b * cols * 10.0, st);
+        run_swiglu_bwd(dh, g, u, dg, du, b * cols, st);
+    }
     return cuda_check("swiglu_backward");
 }
 

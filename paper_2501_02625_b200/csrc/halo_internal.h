@@ -59,6 +59,10 @@ bool cols_v2(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t
 bool encode_2d_sw128(CUtensorMap* map, int dtype, const void* base, uint64_t inner, uint64_t outer,
                      uint32_t box_outer);
 
+// 2-D tensor map without swizzle, zero OOB fill (gemm_sm100.cu)
+bool encode_2d_plain(CUtensorMap* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer);
+
 // K1 kernel generation (HALO_K1_VERSION, default 4)
 int k1_version();
 
@@ -75,6 +79,12 @@ bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t
 // amax_rows / row_scales: `rows` words / floats of device scratch / output
 bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, int64_t B,
                      unsigned* amax_rows, float* row_scales, uint8_t* codes, unsigned* err, cudaStream_t st);
+
+// K2 phase A of the MLP gate/up projections fused with the SwiGLU backward
+// (fwht_cols3.cu)
+bool cols_swiglu_absmax(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t b, int64_t rows_pad,
+                        int64_t cols, int64_t B, unsigned* gr, unsigned* gp, unsigned* ur, unsigned* up, unsigned* err,
+                        cudaStream_t st);
 
 // elementwise glue (glue.cu)
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);

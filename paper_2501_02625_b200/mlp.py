@@ -11,6 +11,7 @@ silu -> fc2, backward in reverse :179-209) with the Llama gate added.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -30,6 +31,9 @@ class HaloMLP:
         self.ctx = [halo.SavedContext() for _ in range(3)]
         self._act = None
         self.share_x = True
+        # SwiGLU backward fused with the absmax pass of the gate/up error
+        # quantization (halo_swiglu_backward_absmax); False = separate kernels
+        self.fuse_glue = os.environ.get("HALO_MLP_FUSE_GLUE", "0") == "1"
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         g = self.gate.forward(x, self.ctx[0])
@@ -46,8 +50,13 @@ class HaloMLP:
         bd = self.down.backward(self.ctx[2], dy, need_grad_w)
         dg = torch.empty_like(g)
         du = torch.empty_like(u)
-        check(lib().halo_swiglu_backward(halo._ptr(bd.e_x), halo._ptr(g), halo._ptr(u), halo._ptr(dg),
-                                         halo._ptr(du), g.numel(), halo._stream()))
+        if self.fuse_glue:
+            check(lib().halo_swiglu_backward_absmax(self.gate._h, self.ctx[0]._h, self.up._h, self.ctx[1]._h,
+                                                    halo._ptr(bd.e_x), halo._ptr(g), halo._ptr(u), halo._ptr(dg),
+                                                    halo._ptr(du), g.shape[0], g.shape[1], halo._stream()))
+        else:
+            check(lib().halo_swiglu_backward(halo._ptr(bd.e_x), halo._ptr(g), halo._ptr(u), halo._ptr(dg),
+                                             halo._ptr(du), g.numel(), halo._stream()))
         bg = self.gate.backward(self.ctx[0], dg, need_grad_w)
         bu = self.up.backward(self.ctx[1], du, need_grad_w)
         dx = torch.empty_like(bg.e_x)

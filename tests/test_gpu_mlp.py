@@ -1,0 +1,125 @@
+"""GPU tests of the Llama MLP block over HALO linears (paper_2501_02625_b200.mlp).
+
+The SwiGLU glue is not part of the reference path; its kernels are checked
+against a torch fp32 statement of the same formula (bf16 outputs within a few
+ulps: the device sigmoid uses the hardware exp2).  The fused glue
+(halo_swiglu_backward_absmax: SwiGLU backward + the absmax pass of both
+projections' error quantization) must reproduce the unfused composition
+(glue kernel, then two full halo_linear_backward calls) BIT-EXACTLY: same
+dG / dU bits, same scales, same codes, hence the same E_X and grad_W.
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_02625_b200 import halo, mlp
+    return halo, mlp
+
+
+def _weights(I, H, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    bf = torch.bfloat16
+    wg = (torch.randn(I, H, generator=g, device="cuda") / H ** 0.5).to(bf)
+    wu = (torch.randn(I, H, generator=g, device="cuda") / H ** 0.5).to(bf)
+    wd = (torch.randn(H, I, generator=g, device="cuda") / I ** 0.5).to(bf)
+    return wg, wu, wd, g
+
+
+def test_swiglu_glue_vs_torch(M):
+    halo, _ = M
+    from paper_2501_02625_b200._lib import check, lib
+    g_ = torch.Generator(device="cuda").manual_seed(3)
+    n = 1 << 16
+    bf = torch.bfloat16
+    g = (torch.randn(n, generator=g_, device="cuda") * 3).to(bf)
+    u = torch.randn(n, generator=g_, device="cuda").to(bf)
+    dh = torch.randn(n, generator=g_, device="cuda").to(bf)
+    h = torch.empty_like(g)
+    dg = torch.empty_like(g)
+    du = torch.empty_like(g)
+    check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), n, halo._stream()))
+    check(lib().halo_swiglu_backward(halo._ptr(dh), halo._ptr(g), halo._ptr(u), halo._ptr(dg), halo._ptr(du), n,
+                                     halo._stream()))
+    gf, uf, dhf = g.float(), u.float(), dh.float()
+    s = torch.sigmoid(gf)
+    ref_h = gf * s * uf
+    ref_du = dhf * gf * s
+    ref_dg = dhf * uf * s * (1 + gf * (1 - s))
+    for got, ref in ((h, ref_h), (du, ref_du), (dg, ref_dg)):
+        err = (got.float() - ref).abs()
+        assert bool((err <= 2 ** -6 * ref.abs() + 1e-30).all()), float((err / ref.abs().clamp_min(1e-30)).max())
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("T,H,I", [(512, 256, 768), (300, 256, 512), (2048, 512, 1024)])
+def test_mlp_fused_glue_bitexact(M, fmt, T, H, I):
+    """Fused SwiGLU-backward + K2 absmax == glue kernel + two full backwards."""
+    halo, mlp = M
+    wg, wu, wd, g = _weights(I, H)
+    x = torch.randn(T, H, generator=g, device="cuda").to(torch.bfloat16)
+    x[:, [1, 7]] *= 30
+    dy = (torch.randn(T, H, generator=g, device="cuda") * 1e-3).to(torch.bfloat16)
+    outs = []
+    for fuse in (False, True):
+        m = mlp.HaloMLP(wg, wu, wd, halo.halo2(fmt, 256))
+        m.fuse_glue = fuse
+        y = m.forward(x)
+        dx, grads = m.backward(dy)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), dx.clone(), [gw.clone() for gw in grads]))
+    (y0, dx0, g0), (y1, dx1, g1) = outs
+    assert torch.equal(y0, y1)
+    assert torch.equal(dx0, dx1)
+    for a, b in zip(g0, g1):
+        assert torch.equal(a, b)
+
+
+def test_mlp_fused_glue_other_schemes_fall_back(M):
+    """HALO-1 has no left rotation: the fused entry is the plain glue kernel."""
+    halo, mlp = M
+    wg, wu, wd, g = _weights(512, 256, seed=5)
+    x = torch.randn(256, 256, generator=g, device="cuda").to(torch.bfloat16)
+    dy = (torch.randn(256, 256, generator=g, device="cuda") * 1e-3).to(torch.bfloat16)
+    res = []
+    for fuse in (False, True):
+        m = mlp.HaloMLP(wg, wu, wd, halo.halo1(0, 256))
+        m.fuse_glue = fuse
+        m.forward(x)
+        dx, grads = m.backward(dy)
+        torch.cuda.synchronize()
+        res.append((dx.clone(), [t.clone() for t in grads]))
+    assert torch.equal(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        assert torch.equal(a, b)
+
+
+def test_mlp_stale_absmax_not_reused(M):
+    """The precomputed absmax words are consumed only for the same E_Y buffer:
+    a backward with a different buffer recomputes them."""
+    halo, mlp = M
+    wg, wu, wd, g = _weights(512, 256, seed=7)
+    x = torch.randn(256, 256, generator=g, device="cuda").to(torch.bfloat16)
+    dy = (torch.randn(256, 256, generator=g, device="cuda") * 1e-3).to(torch.bfloat16)
+    m = mlp.HaloMLP(wg, wu, wd, halo.halo2(0, 256))
+    m.forward(x)
+    dx1, gr1 = m.backward(dy)
+    # same forward context, unfused reference on a fresh module
+    r = mlp.HaloMLP(wg, wu, wd, halo.halo2(0, 256))
+    r.fuse_glue = False
+    r.forward(x)
+    dx2, gr2 = r.backward(dy)
+    # direct gate backward with another E (copy of dG scaled): must not reuse
+    e = (torch.randn(256, 512, generator=g, device="cuda") * 1e-2).to(torch.bfloat16)
+    a = m.gate.backward(m.ctx[0], e)
+    b = r.gate.backward(r.ctx[0], e)
+    torch.cuda.synchronize()
+    assert torch.equal(dx1, dx2)
+    assert torch.equal(a.e_x, b.e_x)
+    assert torch.equal(a.grad_w, b.grad_w)
