@@ -13,9 +13,11 @@ quantized GEMMs per step / step time (TOPS).
 
 N > 1 (torchrun, one rank per GPU): HQ-FSDP (hqfsdp.hpp) — every rank owns a
 row shard of each weight and runs the block on its own 8192 tokens (weak
-scaling); per step the INT8 (WH)_Q codes are all-gathered for the forward,
-regathered under the saved scale for the backward, and dW is reduce-scattered,
-all over NCCL inside the timed step.
+scaling).  Default (peer): each rank quantizes its rows of (WH)_Q under the
+shared scale into a CUDA-IPC buffer and the GEMMs read the peers' rows in
+place over NVLink (no all-gather; absmax exchange + barriers by a device
+mailbox kernel); dW is reduce-scattered over NCCL.  --fsdp-gather: the
+NCCL all-gather / regather variant.  All inside the timed step.
 `--impl reference` times the reference's own CPU implementation (the
 unmodified headers compiled into oracle/_ref) on a bounded sample.
 """
@@ -162,6 +164,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fsdp", action="store_true", help="HQ-FSDP path even at N=1 (always on for N>1)")
+    ap.add_argument("--fsdp-gather", action="store_true", help="HQ-FSDP with NCCL all-gathers instead of peer reads")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -199,8 +202,12 @@ def main():
     x = x.to(bf)
     dy = (torch.randn(b, HIDDEN, generator=g, device=dev) * 1e-3).to(bf)
     scheme = halo.halo2(fmt, args.block)
-    use_fsdp = world > 1 or args.fsdp
-    if use_fsdp:
+    use_fsdp = world > 1 or args.fsdp or args.fsdp_gather
+    if use_fsdp and not args.fsdp_gather:
+        # HQ-FSDP over peer memory: shards read in place by the GEMMs
+        from paper_2501_02625_b200.fsdp import PeerFsdpHaloMLP
+        mlp = PeerFsdpHaloMLP(wg, wu, wd, scheme)
+    elif use_fsdp:
         # HQ-FSDP: weights row-sharded over the ranks, INT8 (WH)_Q gathered for
         # the forward, regathered for the backward, dW reduce-scattered
         from paper_2501_02625_b200.fsdp import FsdpHaloMLP
@@ -353,8 +360,11 @@ def main():
             "vs_baseline": None, "dtype": "int8" if fmt == halo.INT8 else "fp8_e4m3", "data": "synthetic",
             "config": {"workload": CONFIG_NAME, "global_batch": b * world, "seq_len": None,
                        "tokens_per_gpu": b, "hadamard_block": args.block,
-                       "parallelism": (f"hq-fsdp{world} (INT8 weight all-gather + regather, bf16 dW "
-                                       f"reduce-scatter over NCCL)" if use_fsdp else "single GPU"),
+                       "parallelism": ((f"hq-fsdp{world} (INT8 weight all-gather + regather, bf16 dW "
+                                        f"reduce-scatter over NCCL)" if args.fsdp_gather else
+                                        f"hq-fsdp{world} (INT8 weight shards read in place over NVLink by the "
+                                        f"GEMMs, device-mailbox absmax exchange, bf16 dW reduce-scatter over NCCL)")
+                                       if use_fsdp else "single GPU"),
                        "l2": "512 MiB buffer written between timed steps (outside the step events); "
                              "per-step working set ~2 GB > 126 MB L2"},
             "tokens_per_s": world * b * args.steps / (ms / 1e3),
@@ -374,6 +384,10 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()  # no rank frees its IPC-exported shards while a peer may still read them
+    if hasattr(mlp, "close"):
+        mlp.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -190,6 +190,15 @@ HALO_API halo_status halo_linear_set_weight(halo_linear* layer, const void* w, i
  * (WH)_Q (hqfsdp.hpp:204-237) or a frozen PEFT weight (halo_linear.hpp:248):
  * forward skips the weight quantization.  codes == NULL reverts. */
 HALO_API halo_status halo_linear_set_qweight(halo_linear* layer, const uint8_t* codes, const float* scale);
+/* HQ-FSDP without the all-gather (replaces quantized_all_gather +
+ * backward_regather, hqfsdp.hpp:204-266, for this layer): (WH)_Q is the row
+ * concatenation of n_parts equal shards, parts[i] (host array of device
+ * pointers: local memory or a peer GPU's, e.g. halo_ipc_open) holding rows
+ * [i*n/n_parts, (i+1)*n/n_parts).  The forward and E GEMMs read the shards in
+ * place over NVLink; `scale` is the shared per-tensor scale.  Requires
+ * n/n_parts % 256 == 0.  parts == NULL reverts. */
+HALO_API halo_status halo_linear_set_qweight_sharded(halo_linear* layer, const uint8_t* const* parts, int32_t n_parts,
+                                                     const float* scale);
 
 HALO_API halo_status halo_ctx_create(halo_ctx** out);
 HALO_API halo_status halo_ctx_destroy(halo_ctx* ctx);
@@ -251,6 +260,25 @@ HALO_API halo_status halo_swiglu_backward_absmax(const halo_linear* gate, halo_c
 /* out = a + b elementwise (f32 or bf16), n % 8 == 0 */
 HALO_API halo_status halo_add(const void* a, const void* b, void* out, int32_t dtype, int64_t n,
                               halo_stream_t stream);
+
+/* ------------------------------------------- HQ-FSDP over peer memory */
+/* Device buffers shareable across processes (CUDA IPC), zero-filled: the
+ * local weight shard's codes and the rank's mailbox (2*world u32). */
+#define HALO_PEER_MAX 8
+#define HALO_IPC_HANDLE_BYTES 64
+HALO_API halo_status halo_peer_alloc(int64_t bytes, void** ptr);
+HALO_API halo_status halo_peer_free(void* ptr);
+HALO_API halo_status halo_ipc_handle(const void* ptr, void* handle /* HALO_IPC_HANDLE_BYTES */);
+HALO_API halo_status halo_ipc_open(const void* handle, void** ptr);
+HALO_API halo_status halo_ipc_close(void* ptr);
+/* Stream-ordered barrier of `world` ranks over their mailboxes (host array
+ * of world device pointers, mailboxes[rank] local): posts *amax_in (if not
+ * NULL) to every rank, waits until every rank reached `epoch` (> 0, the same
+ * increasing sequence on all ranks), then writes the max of the posted
+ * values to *amax_out (if not NULL).  Replaces the absmax all-reduce of
+ * hqfsdp.hpp:172-196 and orders shard writes before peer reads. */
+HALO_API halo_status halo_peer_sync(void* const* mailboxes, int32_t world, int32_t rank, uint32_t epoch,
+                                    const float* amax_in, float* amax_out, halo_stream_t stream);
 
 /* ------------------------------------------------------------- profiling */
 /* Kernel classes: 0 K1 row-FWHT+quantize, 1 K2 column-FWHT+dual quantize,

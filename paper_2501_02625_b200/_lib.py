@@ -134,6 +134,16 @@ def lib():
     L.halo_swiglu_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _vp]
     L.halo_swiglu_backward_absmax.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]
     L.halo_add.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp]
+    L.halo_linear_set_qweight_sharded.argtypes = [_vp, C.POINTER(_vp), _i32, _vp]
+    L.halo_peer_alloc.argtypes = [_i64, C.POINTER(_vp)]
+    L.halo_peer_free.argtypes = [_vp]
+    L.halo_ipc_handle.argtypes = [_vp, C.c_char_p]
+    L.halo_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
+    L.halo_ipc_close.argtypes = [_vp]
+    L.halo_peer_sync.argtypes = [C.POINTER(_vp), _i32, _i32, C.c_uint32, _vp, _vp, _vp]
+    for fn in ("halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free", "halo_ipc_handle",
+               "halo_ipc_open", "halo_ipc_close", "halo_peer_sync"):
+        getattr(L, fn).restype = C.c_int
     L.halo_profile_enable.argtypes = [C.c_int]
     L.halo_profile_read.argtypes = [C.POINTER(Profile)]
     for fn in ("halo_swiglu_forward", "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
@@ -179,5 +189,6 @@ EXPORTS = (
     "halo_linear_counters", "halo_linear_reset_counters", "halo_ctx_saved",
     "halo_ctx_error_operands", "halo_ctx_check", "halo_device_copy", "halo_swiglu_forward",
     "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
-    "halo_profile_read",
+    "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
+    "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync",
 )

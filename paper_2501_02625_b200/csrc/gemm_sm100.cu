@@ -88,6 +88,14 @@ struct GemmArgs {
     // sa_vec[M] per row of C, sb_vec[N] per column of C
     const float* sa_vec;
     const float* sb_vec;
+    // sharded operands (HQ-FSDP without an all-gather): A / B split into
+    // *_shards equal parts of *_len rows along K (*_along_k) or along M / N,
+    // each part behind its own tensor map in global memory (parts may live
+    // in peer GPUs' HBM, reached over NVLink).  0 shards = tmA / tmB.
+    const CUtensorMap* a_maps;
+    int a_shards, a_len, a_along_k;
+    const CUtensorMap* b_maps;
+    int b_shards, b_len, b_along_k;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -394,6 +402,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        // shard maps were written to global memory by the host (copy
+        // engine): acquire them for the tensormap proxy before first use
+        for (int i = 0; i < p.a_shards; ++i)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.a_maps + i) : "memory");
+        for (int i = 0; i < p.b_shards; ++i)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.b_maps + i) : "memory");
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -435,6 +449,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 int mb, nb;
                 tile_coords(t, mt, nt, mb, nb);
                 const int m0 = mb * C::TILE_M + (int)rank * BM, n0 = nb * BN + (int)rank * C::B_ROWS;
+                // operand shards split along M / N: fixed for the tile
+                const CUtensorMap* mapA = &tmA;
+                const CUtensorMap* mapB = &tmB;
+                int am = m0, bn = n0;
+                if (p.a_shards && !p.a_along_k) {
+                    const int i = m0 / p.a_len;
+                    mapA = p.a_maps + i;
+                    am = m0 - i * p.a_len;
+                }
+                if (p.b_shards && !p.b_along_k) {
+                    const int i = n0 / p.b_len;
+                    mapB = p.b_maps + i;
+                    bn = n0 - i * p.b_len;
+                }
                 for (int kb = 0; kb < nkb; ++kb) {
                     const int k0 = kb * BK;
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -443,10 +471,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     if constexpr (CG == 2) {
                         if (leader) mbar_expect_tx(&full[stage], 2 * (A_STAGE_BYTES + B_STAGE_BYTES));
                         const uint32_t fb = full_leader0 + stage * 8;
-                        if (p.a_kmajor) tma_load_2d_2sm(a_dst, &tmA, fb, k0, m0);
-                        else tma_load_2d_2sm(a_dst, &tmA, fb, m0, k0);
-                        if (p.b_kmajor) tma_load_2d_2sm(b_dst, &tmB, fb, k0, n0);
-                        else tma_load_2d_2sm(b_dst, &tmB, fb, n0, k0);
+                        // operand shards split along K: the k-block's part
+                        const CUtensorMap* ma = mapA;
+                        const CUtensorMap* mb = mapB;
+                        int ak = k0, bk = k0;
+                        if (p.a_shards && p.a_along_k) {
+                            const int i = k0 / p.a_len;
+                            ma = p.a_maps + i;
+                            ak = k0 - i * p.a_len;
+                        }
+                        if (p.b_shards && p.b_along_k) {
+                            const int i = k0 / p.b_len;
+                            mb = p.b_maps + i;
+                            bk = k0 - i * p.b_len;
+                        }
+                        if (p.a_kmajor) tma_load_2d_2sm(a_dst, ma, fb, ak, am);
+                        else tma_load_2d_2sm(a_dst, ma, fb, am, ak);
+                        if (p.b_kmajor) tma_load_2d_2sm(b_dst, mb, fb, bk, bn);
+                        else tma_load_2d_2sm(b_dst, mb, fb, bn, bk);
                     } else {
                         mbar_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
                         if (p.a_kmajor) tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
@@ -911,10 +953,32 @@ int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
                       out_trans, n_valid, st);
 }
 
+namespace {
+thread_local const ShardSpec* t_shard_a = nullptr;
+thread_local const ShardSpec* t_shard_b = nullptr;
+}  // namespace
+
+ShardScope::ShardScope(const ShardSpec* a, const ShardSpec* b) {
+    t_shard_a = a;
+    t_shard_b = b;
+}
+ShardScope::~ShardScope() {
+    t_shard_a = nullptr;
+    t_shard_b = nullptr;
+}
+
+bool encode_shard_maps(const uint8_t* const* parts, int n, int64_t inner, int64_t rows, CUtensorMap* out) {
+    for (int i = 0; i < n; ++i)
+        if (!encode_map(&out[i], parts[i], (uint64_t)inner, (uint64_t)rows, 128)) return false;
+    return true;
+}
+
 int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                int b_kmajor, const float* sa, const float* sa_vec, const float* sb, const float* sb_vec, void* out,
                int out_kind, int xf_lb, float xf_norm, int out_trans, int64_t n_valid, cudaStream_t st) {
     if ((sa_vec || sb_vec) && (xf_lb > 0 || out_trans || out_kind == 2)) return -1;
+    const ShardSpec* sha = t_shard_a;
+    const ShardSpec* shb = t_shard_b;
     static const float kOne = 1.0f;
     static float* d_one = nullptr;
     if (!sa || !sb) {  // vector-only call: the tensor scale slot still needs a valid device word
@@ -947,9 +1011,22 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     const int cg = (cg_env == 1 || num_sms() < 2) ? 1 : 2;
     CUtensorMap ma, mb;
     const int b_box = BN / cg;
-    const bool ok_a = a_kmajor ? encode_map(&ma, A, K, M, BM) : encode_map(&ma, A, M, K, BK);
-    const bool ok_b = b_kmajor ? encode_map(&mb, B, K, N, b_box) : encode_map(&mb, B, N, K, BK);
+    // sharded operands: the parts' maps (box 128 x 128) replace tmA / tmB;
+    // every tile / k-block must fall inside one part
+    auto shard_ok = [&](const ShardSpec* sh, int64_t mn, int tile) {
+        if (!sh) return true;
+        if (cg != 2 || sh->n < 1 || sh->n > 64 || sh->len <= 0) return false;
+        const int64_t total = sh->along_k ? K : mn;
+        return (int64_t)sh->n * sh->len == total && sh->len % (sh->along_k ? BK : tile) == 0;
+    };
+    if (!shard_ok(sha, M, BM * 2) || !shard_ok(shb, N, BN)) return -1;
+    const bool ok_a = sha ? true : a_kmajor ? encode_map(&ma, A, K, M, BM) : encode_map(&ma, A, M, K, BK);
+    const bool ok_b = shb ? true : b_kmajor ? encode_map(&mb, B, K, N, b_box) : encode_map(&mb, B, N, K, BK);
     if (!ok_a || !ok_b) return -2;
+    if (sha) ma = sha->maps_host0;
+    if (sha) args.a_maps = sha->maps, args.a_shards = sha->n, args.a_len = (int)sha->len, args.a_along_k = sha->along_k;
+    if (shb) mb = shb->maps_host0;
+    if (shb) args.b_maps = shb->maps, args.b_shards = shb->n, args.b_len = (int)shb->len, args.b_along_k = shb->along_k;
     // C via TMA stores when the row pitch is a multiple of 16 B (HALO_GEMM_TMA_STORE=0 disables)
     static const int tma_store_env = [] {
         const char* e = getenv("HALO_GEMM_TMA_STORE");

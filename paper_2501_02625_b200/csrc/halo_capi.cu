@@ -28,6 +28,13 @@ halo_status fail(halo_status s, const std::string& msg) {
     return s;
 }
 
+}  // namespace
+
+// error text for the C ABI entries outside this file (peer.cu)
+void halo_b200::set_last_error(const char* msg) { g_err = msg; }
+
+namespace {
+
 halo_status cuda_check(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(HALO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -163,6 +170,7 @@ struct halo_ctx {
     // computed by the fused pass for this exact E_Y buffer and batch
     const void* e_amax_src = nullptr;
     int64_t e_amax_b = 0;
+    bool wq_sharded = false;  // forward used the layer's sharded (WH)_Q
     const uint8_t* xq_codes() const { return xq_borrow ? xq_borrow : xq.as<uint8_t>(); }
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
@@ -181,9 +189,15 @@ struct halo_linear {
     std::atomic<int64_t> cx{0}, cw{0}, ce{0};
     // PEFT: (WH)_Q frozen at construction (halo_linear.hpp:237-250)
     Buffer frozen, frozen_dev;
+    // HQ-FSDP without the all-gather: (WH)_Q as row shards in place (local
+    // or peer HBM), read by the GEMMs' TMA through per-shard maps
+    bool sharded = false;
+    Buffer shard_maps;
+    ShardSpec shard_n{}, shard_k{};  // split along N (F GEMM) / along K (E GEMM)
     ~halo_linear() {
         frozen.release();
         frozen_dev.release();
+        shard_maps.release();
     }
 };
 
@@ -604,6 +618,46 @@ extern "C" halo_status halo_linear_set_qweight(halo_linear* l, const uint8_t* co
     if (codes && !scale) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight: codes without a scale");
     l->qcodes = codes;
     l->qscale = scale;
+    l->sharded = false;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_linear_set_qweight_sharded(halo_linear* l, const uint8_t* const* parts, int32_t n_parts,
+                                                       const float* scale) {
+    if (!l) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: null layer");
+    if (l->s.peft) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: a peft layer's weight codes are frozen");
+    if (!parts || n_parts <= 0) {
+        l->sharded = false;
+        l->qcodes = nullptr;
+        l->qscale = nullptr;
+        return HALO_OK;
+    }
+    if (!scale) return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: codes without a scale");
+    if (l->s.granularity == HALO_GRAN_ROW)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: row granularity keeps per-channel scales local");
+    if (n_parts > 64 || l->n % n_parts)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: out_features must split evenly into the parts");
+    const int64_t len = l->n / n_parts;
+    // the F GEMM's 256-row N tiles and the E GEMM's 128-deep k-blocks must
+    // each fall inside one part; TMA rows are m bytes (a multiple of 16)
+    if (len % 256 || l->m % 16)
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "set_qweight_sharded: rows per part must be a multiple of 256 and in_features of 16");
+    for (int i = 0; i < n_parts; ++i)
+        if (!parts[i] || (uintptr_t)parts[i] % 16)
+            return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: parts must be 16 B aligned device pointers");
+    std::vector<CUtensorMap> maps((size_t)n_parts);
+    if (!encode_shard_maps(parts, n_parts, l->m, len, maps.data()))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "set_qweight_sharded: tensor map encoding failed");
+    if (l->shard_maps.ensure(maps.size() * sizeof(CUtensorMap)) != HALO_OK) return HALO_ERR_CUDA;
+    if (cudaMemcpy(l->shard_maps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+        return fail(HALO_ERR_CUDA, "set_qweight_sharded: map upload failed");
+    l->shard_n = ShardSpec{l->shard_maps.as<CUtensorMap>(), maps[0], (int)n_parts, len, 0};
+    l->shard_k = ShardSpec{l->shard_maps.as<CUtensorMap>(), maps[0], (int)n_parts, len, 1};
+    l->sharded = true;
+    l->qcodes = nullptr;
+    l->qscale = scale;
     return HALO_OK;
 }
 
@@ -668,7 +722,9 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         // Granularity::row (quantize.hpp:73-132): X per token, W per output
         // channel -- both on non-contracted dims of F, so the integer GEMM
         // stays exact and the epilogue applies sx[i] * sw[j]
-        if (l->qcodes) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row granularity with installed qweight codes");
+        if (l->qcodes || l->sharded)
+            return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row granularity with installed qweight codes");
+        c->wq_sharded = false;
         const int64_t mx = b > l->n ? b : l->n;
         if (c->xs_rows.ensure((size_t)b * sizeof(float)) != HALO_OK || c->wq.ensure((size_t)(l->n * l->m)) != HALO_OK ||
             c->ws_rows.ensure((size_t)l->n * sizeof(float)) != HALO_OK ||
@@ -705,8 +761,12 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
                                          &d->amax[SX], &d->scale[SX], &d->err, st);
     if (r != HALO_OK) return r;
     ++l->cx;
-    // ctx.wq = quantize(WH)  (:295-297), or the gathered / frozen codes
-    if (l->qcodes) {
+    // ctx.wq = quantize(WH)  (:295-297), or the gathered / frozen / sharded codes
+    c->wq_sharded = l->sharded;
+    if (l->sharded) {
+        c->wq_codes = nullptr;  // read in place by the GEMM (ShardScope)
+        c->wq_scale = l->qscale;
+    } else if (l->qcodes) {
         c->wq_codes = l->qcodes;
         c->wq_scale = l->qscale;
     } else {
@@ -714,6 +774,7 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         if (r != HALO_OK) return r;
     }
     // Y = qmatmul(xq, wq, transpose_b=true)  (:299)
+    ShardScope shards(nullptr, l->sharded ? &l->shard_n : nullptr);
     const int gr = prof_gemm(s.format_x, c->xq.as<uint8_t>(), c->wq_codes, b, l->n, l->m, 1, 1, &d->scale[SX],
                             c->wq_scale, y, y_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
     if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
@@ -750,6 +811,9 @@ extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx
     c->xq_scale = src->xq_scale;
     DevScalars* d = c->d();
     if (c->row_gran) {
+        if (l->qcodes || l->sharded)
+            return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row granularity with installed qweight codes");
+        c->wq_sharded = false;
         int64_t B = 1;
         if (s.F.middle && resolve_block(l->m, s.had_block, &B, "forward") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
         if (c->wq.ensure((size_t)(l->n * l->m)) != HALO_OK || c->ws_rows.ensure((size_t)l->n * sizeof(float)) != HALO_OK ||
@@ -771,13 +835,18 @@ extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx
         c->valid = true;
         return cuda_check("forward_shared");
     }
-    if (l->qcodes) {
+    c->wq_sharded = l->sharded;
+    if (l->sharded) {
+        c->wq_codes = nullptr;
+        c->wq_scale = l->qscale;
+    } else if (l->qcodes) {
         c->wq_codes = l->qcodes;
         c->wq_scale = l->qscale;
     } else {
         const halo_status r = quantize_weight(l, c, s.F.middle, c->wq, SW, &c->wq_codes, &c->wq_scale, st);
         if (r != HALO_OK) return r;
     }
+    ShardScope shards(nullptr, l->sharded ? &l->shard_n : nullptr);
     const int gr = prof_gemm(s.format_x, c->xq_codes(), c->wq_codes, b, l->n, l->m, 1, 1, c->xq_scale, c->wq_scale, y,
                              y_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
     if (gr != 0) return fail(gr == -1 ? HALO_ERR_INVALID_ARGUMENT : HALO_ERR_CUDA, "forward: GEMM launch failed");
@@ -821,7 +890,16 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     // weight operand for E with E's right rotation (:390)
     const uint8_t* wq = c->wq_codes;
     const float* sw = c->wq_scale;
+    // sharded (WH)_Q: the E GEMM reads the parts in place, split along its
+    // contracted dim (out_features) -- the backward "regather" of
+    // hqfsdp.hpp:200-226 without moving a byte
+    const ShardSpec* wsh = nullptr;
+    if (c->wq_sharded) {
+        if (!l->sharded) return fail(HALO_ERR_LOGIC, "halo layer: sharded weight codes were uninstalled before backward");
+        wsh = &l->shard_k;
+    }
     if ((bool)s.E.right != c->wq_rotated) {
+        if (wsh) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: sharded codes cannot be re-quantized for E");
         const halo_status r = quantize_weight(l, c, s.E.right, c->wq2, SW2, &wq, &sw, st);
         if (r != HALO_OK) return r;
     }
@@ -852,11 +930,13 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
             // N = padded tokens); the epilogue applies transform_left over
             // the token axis (:405-408) and stores take_rows(b) of prod
             // (:409) row-major.  ss = sw * s_ehq: same exact double product.
+            ShardScope shards(wsh, nullptr);  // A = (WH)_Q, MN-major, K = out_features
             int gr = prof_gemm_x(fmt, wq, c->ehq.as<uint8_t>(), m, b_pad, n, 0, 1, sw, &d->scale[SEH], P, 0, Bb, 1, b,
                                  st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
         } else {
             // prod = qmatmul(eq, wq)  (:401): B operand (n x m) is MN-major
+            ShardScope shards(nullptr, wsh);
             int gr = prof_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
             // prod = transform_left(prod); take_rows(b)  (:405-409), in place
@@ -872,6 +952,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
                                                    &d->amax[SE], &d->scale[SE], &d->err, st);
         if (r != HALO_OK) return r;
         l->ce += 1;
+        ShardScope shards(nullptr, wsh);  // B = (W[H])_Q, MN-major, K = out_features
         if (s.E.right && fuse_k4() && fusable_block(Bm)) {
             // E_X = (E_Y)_Q (WH)_Q H^T (:410-411) with the right transform in
             // the GEMM epilogue

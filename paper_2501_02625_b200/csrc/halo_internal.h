@@ -42,6 +42,26 @@ int run_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, 
 int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int xf_lb, float xf_norm,
                int out_trans, int64_t n_valid, cudaStream_t st);
+// Sharded GEMM operand (HQ-FSDP without an all-gather): the operand is the
+// row-concatenation of n equal parts of `len` rows (rows along K when
+// along_k, else along M / N), part i behind maps[i] (device array, u8,
+// box 128 x 128, 128 B swizzle: encode_shard_maps).  Parts may be peer
+// GPUs' memory (CUDA IPC over NVLink).  Installed for the run_gemm* calls of
+// the current thread by a ShardScope; the corresponding A / B pointer is
+// then ignored.
+struct ShardSpec {
+    const CUtensorMap* maps;  // device
+    CUtensorMap maps_host0;   // host copy of part 0 (kernel parameter placeholder)
+    int n;
+    int64_t len;
+    int along_k;
+};
+struct ShardScope {
+    ShardScope(const ShardSpec* a, const ShardSpec* b);
+    ~ShardScope();
+};
+bool encode_shard_maps(const uint8_t* const* parts, int n, int64_t inner, int64_t rows, CUtensorMap* out);
+
 // as run_gemm_x with optional per-row (sa_vec[M]) / per-column (sb_vec[N])
 // scales (Granularity::row on the non-contracted dims); no transform then.
 int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
@@ -85,6 +105,9 @@ bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_
 bool cols_swiglu_absmax(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t b, int64_t rows_pad,
                         int64_t cols, int64_t B, unsigned* gr, unsigned* gp, unsigned* ur, unsigned* up, unsigned* err,
                         cudaStream_t st);
+
+// halo_last_error() text (halo_capi.cu)
+void set_last_error(const char* msg);
 
 // elementwise glue (glue.cu)
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);

@@ -286,3 +286,163 @@ class FsdpHaloMLP:
 
     def gemm_ops(self, tokens):
         return self.mlp.gemm_ops(tokens)
+
+
+# ------------------------------------------------- peer-memory HQ-FSDP --
+
+class PeerBuffer:
+    """A device buffer from halo_peer_alloc (zero-filled, exportable by CUDA
+    IPC), optionally viewed as a torch tensor through the CUDA array
+    interface."""
+
+    _TYPESTR = {torch.int8: "|i1", torch.uint8: "|u1", torch.float32: "<f4"}
+
+    def __init__(self, nbytes: int):
+        import ctypes as C
+        from ._lib import check, lib
+        p = C.c_void_p()
+        check(lib().halo_peer_alloc(nbytes, C.byref(p)))
+        self.ptr, self.nbytes = p.value, nbytes
+
+    def tensor(self, shape, dtype) -> torch.Tensor:
+        ptr = self.ptr
+
+        class _View:
+            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": PeerBuffer._TYPESTR[dtype],
+                                        "data": (ptr, False), "version": 2, "strides": None}
+
+        return torch.as_tensor(_View(), device=torch.device("cuda", torch.cuda.current_device()))
+
+    def handle(self) -> bytes:
+        import ctypes as C
+        from ._lib import check, lib
+        buf = C.create_string_buffer(64)
+        check(lib().halo_ipc_handle(C.c_void_p(self.ptr), buf))
+        return buf.raw
+
+    def free(self):
+        from ._lib import lib
+        if self.ptr:
+            lib().halo_peer_free(self.ptr)
+            self.ptr = 0
+
+
+def _ipc_open(handle: bytes) -> int:
+    import ctypes as C
+    from ._lib import check, lib
+    p = C.c_void_p()
+    check(lib().halo_ipc_open(handle, C.byref(p)))
+    return p.value
+
+
+def _exchange(obj, group):
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return [obj]
+    out = [None] * world
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+class PeerFsdpHaloMLP(FsdpHaloMLP):
+    """HQ-FSDP MLP whose weight "gathers" move no bytes.
+
+    Every rank quantizes its rows of (WH)_Q under the shared scale into a
+    CUDA-IPC buffer; the GEMMs (F: B operand split along N; E: operand split
+    along its contracted dim) read the peers' rows in place over NVLink
+    (halo_linear_set_qweight_sharded).  The absmax all-reduce of
+    hqfsdp.hpp:172-196 and the ordering of shard writes before peer reads are
+    one stream-ordered mailbox kernel each (halo_peer_sync); the backward
+    regather (:243-266) is free because the forward's codes stay resident
+    under the saved scale.  The next step's first mailbox barrier also
+    guarantees no peer still reads a shard when it is re-quantized.  Weight
+    gradients are reduce-scattered as in FsdpHaloMLP.  Needs
+    out_features % (world * 256) == 0 for every projection.
+    """
+
+    def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16):
+        super().__init__(w_gate, w_up, w_down, scheme, group, check_stale, grad_dtype)
+        from ._lib import HALO_OK  # noqa: F401  (library loaded)
+        for p in self.params:
+            if p.pad_rows or p.shard_rows % 256:
+                raise ValueError("PeerFsdpHaloMLP: out_features must be a multiple of world * 256")
+        self.buffers = []  # no gathered copies
+        code_dt = torch.int8 if self.fmt == INT8 else torch.uint8
+        self.local = [PeerBuffer(p.shard_rows * p.cols) for p in self.params]
+        self.local_views = [b.tensor((p.shard_rows, p.cols), code_dt) for b, p in zip(self.local, self.params)]
+        self.mailbox = PeerBuffer(2 * self.world * 4)
+        dev = self.params[0].master.device
+        self.amax = [torch.zeros(1, dtype=torch.float32, device=dev) for _ in self.params]
+        self.scales = [torch.ones(1, dtype=torch.float32, device=dev) for _ in self.params]
+        handles = _exchange(([b.handle() for b in self.local], self.mailbox.handle()), group)
+        self._opened = []
+        self.parts = []
+        for i in range(len(self.params)):
+            row = []
+            for j in range(self.world):
+                if j == self.rank:
+                    row.append(self.local[i].ptr)
+                else:
+                    ptr = _ipc_open(handles[j][0][i])
+                    self._opened.append(ptr)
+                    row.append(ptr)
+            self.parts.append(row)
+        self.boxes = []
+        for j in range(self.world):
+            if j == self.rank:
+                self.boxes.append(self.mailbox.ptr)
+            else:
+                ptr = _ipc_open(handles[j][1])
+                self._opened.append(ptr)
+                self.boxes.append(ptr)
+        self.epoch = 0
+        for layer, parts, scale in zip(self.layers, self.parts, self.scales):
+            layer.set_qweight_sharded(parts, scale, keepalive=self)
+
+    def _sync(self, amax_in=None, amax_out=None):
+        import ctypes as C
+        from . import halo
+        from ._lib import check, lib
+        self.epoch += 1
+        arr = (C.c_void_p * self.world)(*self.boxes)
+        check(lib().halo_peer_sync(arr, self.world, self.rank, self.epoch, halo._ptr(amax_in), halo._ptr(amax_out),
+                                   halo._stream()))
+
+    def forward(self, x):
+        ops = CudaOps()
+        for i, p in enumerate(self.params):
+            am = ops.absmax(p.master, self.block, self.rotate).reshape(1).float()
+            # absmax "all-reduce": posted to every mailbox, max taken on device
+            self._sync(am, self.amax[i])
+            self.scales[i].copy_(scale_from_absmax(self.amax[i], p.format))
+            p.global_scale = self.scales[i]
+            p.local_absmax = am
+            p.scales_valid = True
+            self.ledger.record(self.ledger.scale_reduce, K_SCALE_BYTES, p.world)
+            self.local_views[i].copy_(ops.quantize(p.master, self.block, p.format, self.scales[i], self.rotate))
+            elems = p.shard_rows * p.world * p.cols
+            self.ledger.record(self.ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
+            self.ledger.bf16_gather_payload += 2 * elems
+        self._sync()  # every rank's shards written before any peer GEMM reads them
+        return self.mlp.forward(x)
+
+    def backward(self, dy):
+        for p in self.params:
+            if not p.scales_valid:
+                raise HaloLogicError("backward_regather: no saved forward scales")
+            self.ledger.backward_gathers += 1  # served in place: the codes never left
+            self.ledger.backward_consumers += 1
+        dx, grads = self.mlp.backward(dy)
+        shards = [reduce_scatter_grads(g, p, self.ledger, self.group) for g, p in zip(grads, self.params)]
+        return dx, shards
+
+    def close(self):
+        from ._lib import lib
+        torch.cuda.synchronize()
+        for layer in self.layers:
+            layer.set_qweight_sharded(None, None)
+        for ptr in self._opened:
+            lib().halo_ipc_close(ptr)
+        self._opened = []
+        for b in self.local + [self.mailbox]:
+            b.free()

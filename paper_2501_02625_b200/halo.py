@@ -355,6 +355,20 @@ class HaloLinearLayer:
         self._qweight = (codes, scale)
         check(lib().halo_linear_set_qweight(self._h, _ptr(codes), _ptr(scale)))
 
+    def set_qweight_sharded(self, parts, scale: torch.Tensor | None, keepalive=None):
+        """(WH)_Q as row shards read in place by the GEMMs (HQ-FSDP without
+        the all-gather): `parts` are device addresses (ints, e.g. local or
+        IPC-opened peer buffers) or tensors of out_features/len(parts) rows
+        each.  None reverts."""
+        if parts is None:
+            self._qweight = (None, None)
+            check(lib().halo_linear_set_qweight_sharded(self._h, None, 0, None))
+            return
+        ptrs = [p.data_ptr() if isinstance(p, torch.Tensor) else int(p) for p in parts]
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        self._qweight = (tuple(parts), scale, keepalive)
+        check(lib().halo_linear_set_qweight_sharded(self._h, arr, len(ptrs), _ptr(scale)))
+
     def forward(self, x: torch.Tensor, ctx: SavedContext) -> torch.Tensor:
         _need_cuda(x)
         if x.dim() != 2 or x.shape[1] != self.in_features:
