@@ -106,6 +106,13 @@ HALO_API halo_status halo_rotate_quantize(const void* a, int32_t a_dtype, int64_
 
 /* max |A H| over the tensor (hqfsdp.hpp:216-225, the per-rank local absmax),
  * written as a float to absmax_out (device). */
+/* phase B of halo_rotate_quantize under a given absmax (device float, the
+ * value halo_rotate_absmax produces -- e.g. the max over HQ-FSDP ranks,
+ * hqfsdp.hpp:172-196): scale = compute_scales(absmax) in-kernel, then the
+ * codes.  scale_out may be NULL. */
+HALO_API halo_status halo_rotate_quantize_amax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                               int64_t had_block, int32_t format, const float* amax, uint8_t* codes,
+                                               float* scale_out, halo_stream_t stream);
 HALO_API halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols, int64_t had_block,
                                float* absmax_out, halo_stream_t stream);
 
@@ -262,8 +269,20 @@ HALO_API halo_status halo_add(const void* a, const void* b, void* out, int32_t d
                               halo_stream_t stream);
 
 /* ------------------------------------------- HQ-FSDP over peer memory */
+/* Gradient reduce-scatter fused into the backward's G GEMM (replaces
+ * reduce_scatter_grads' transfer, hqfsdp.hpp:271-300): recv[i] (host array
+ * of `parts` device pointers, recv[rank] local, the others e.g. from
+ * halo_ipc_open) is rank i's receive buffer [parts][out_features/parts][in]
+ * fp32; every backward then TMA-stores this rank's fp32 partial G rows
+ * owned by rank i into slot `rank` of recv[i] (grad_w is not written).
+ * out_features/parts % 256 == 0.  recv == NULL reverts. */
+HALO_API halo_status halo_linear_set_grad_scatter(halo_linear* layer, void* const* recv, int32_t parts, int32_t rank);
+/* Owner side: out = T(sum_w double(recv[w]) / world) over [world][rows][cols]
+ * fp32 partials, rank order (hqfsdp.hpp:288-292); T = out_dtype. */
+HALO_API halo_status halo_reduce_scatter_shard(const float* recv, int32_t world, int64_t rows, int64_t cols, void* out,
+                                               int32_t out_dtype, halo_stream_t stream);
 /* Device buffers shareable across processes (CUDA IPC), zero-filled: the
- * local weight shard's codes and the rank's mailbox (2*world u32). */
+ * local weight shard's codes and the rank's mailbox (3*world u32). */
 #define HALO_PEER_MAX 8
 #define HALO_IPC_HANDLE_BYTES 64
 HALO_API halo_status halo_peer_alloc(int64_t bytes, void** ptr);

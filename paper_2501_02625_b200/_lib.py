@@ -141,8 +141,13 @@ def lib():
     L.halo_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
     L.halo_ipc_close.argtypes = [_vp]
     L.halo_peer_sync.argtypes = [C.POINTER(_vp), _i32, _i32, C.c_uint32, _vp, _vp, _vp]
+    L.halo_linear_set_grad_scatter.argtypes = [_vp, C.POINTER(_vp), _i32, _i32]
+    L.halo_rotate_quantize_amax.argtypes = [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp]
+    L.halo_rotate_quantize_amax.restype = C.c_int
+    L.halo_reduce_scatter_shard.argtypes = [_vp, _i32, _i64, _i64, _vp, _i32, _vp]
     for fn in ("halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free", "halo_ipc_handle",
-               "halo_ipc_open", "halo_ipc_close", "halo_peer_sync"):
+               "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
+               "halo_reduce_scatter_shard"):
         getattr(L, fn).restype = C.c_int
     L.halo_profile_enable.argtypes = [C.c_int]
     L.halo_profile_read.argtypes = [C.POINTER(Profile)]
@@ -190,5 +195,6 @@ EXPORTS = (
     "halo_ctx_error_operands", "halo_ctx_check", "halo_device_copy", "halo_swiglu_forward",
     "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
     "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
-    "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync",
+    "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
+    "halo_reduce_scatter_shard", "halo_rotate_quantize_amax",
 )

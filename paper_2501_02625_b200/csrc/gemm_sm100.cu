@@ -96,6 +96,12 @@ struct GemmArgs {
     int a_shards, a_len, a_along_k;
     const CUtensorMap* b_maps;
     int b_shards, b_len, b_along_k;
+    // scattered C (HQ-FSDP gradient reduce-scatter fused into the G GEMM):
+    // rows [i*c_len, (i+1)*c_len) of C go through c_maps[i] -- this rank's
+    // slot in the receive buffer of the rank owning those rows, possibly a
+    // peer GPU's HBM (TMA stores over NVLink).  0 parts = tmC.
+    const CUtensorMap* c_maps;
+    int c_parts, c_len;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -408,6 +414,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.a_maps + i) : "memory");
         for (int i = 0; i < p.b_shards; ++i)
             asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.b_maps + i) : "memory");
+        for (int i = 0; i < p.c_parts; ++i)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(p.c_maps + i) : "memory");
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -689,7 +697,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&tmC, S, col0, row0_);
+                        if (p.c_parts) {  // the owner's receive slot (fp32 partial of this rank)
+                            const int i = row0_ / p.c_len;
+                            tma_store_2d(p.c_maps + i, S, col0, row0_ - i * p.c_len);
+                        } else {
+                            tma_store_2d(&tmC, S, col0, row0_);
+                        }
                         bulk_commit();
                     }
                 }
@@ -956,15 +969,35 @@ int run_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
 namespace {
 thread_local const ShardSpec* t_shard_a = nullptr;
 thread_local const ShardSpec* t_shard_b = nullptr;
+thread_local const ScatterSpec* t_scatter_c = nullptr;
 }  // namespace
 
-ShardScope::ShardScope(const ShardSpec* a, const ShardSpec* b) {
+ShardScope::ShardScope(const ShardSpec* a, const ShardSpec* b, const ScatterSpec* c) {
     t_shard_a = a;
     t_shard_b = b;
+    t_scatter_c = c;
 }
 ShardScope::~ShardScope() {
     t_shard_a = nullptr;
     t_shard_b = nullptr;
+    t_scatter_c = nullptr;
+}
+
+bool encode_scatter_maps(void* const* recv, int parts, int slot, int64_t len, int64_t cols, CUtensorMap* out) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    for (int i = 0; i < parts; ++i) {
+        float* base = static_cast<float*>(recv[i]) + (int64_t)slot * len * cols;
+        const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)len};
+        const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        if (enc(&out[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
 }
 
 bool encode_shard_maps(const uint8_t* const* parts, int n, int64_t inner, int64_t rows, CUtensorMap* out) {
@@ -979,6 +1012,11 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     if ((sa_vec || sb_vec) && (xf_lb > 0 || out_trans || out_kind == 2)) return -1;
     const ShardSpec* sha = t_shard_a;
     const ShardSpec* shb = t_shard_b;
+    const ScatterSpec* scc = t_scatter_c;
+    // scattered C: fp32, row-major, every 32-row TMA box inside one part
+    if (scc && (out_kind != 0 || out_trans || sa_vec || sb_vec || scc->parts < 1 || scc->len % 256 ||
+                (int64_t)scc->parts * scc->len != M || (N * 4) % 16))
+        return -1;
     static const float kOne = 1.0f;
     static float* d_one = nullptr;
     if (!sa || !sb) {  // vector-only call: the tensor scale slot still needs a valid device word
@@ -1036,7 +1074,13 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     std::memset(&mc, 0, sizeof(mc));
     const int esz = out_kind == 1 ? 2 : 4;
     args.tma_store = 0;
-    if (tma_store_env && !out_trans && ((int64_t)N * esz) % 16 == 0 && (uintptr_t)out % 16 == 0) {
+    if (scc) {
+        mc = scc->maps_host0;
+        args.tma_store = 1;
+        args.c_maps = scc->maps;
+        args.c_parts = scc->parts;
+        args.c_len = (int)scc->len;
+    } else if (tma_store_env && !out_trans && ((int64_t)N * esz) % 16 == 0 && (uintptr_t)out % 16 == 0) {
         auto enc = get_encode();
         const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
         const cuuint64_t strides[1] = {(cuuint64_t)N * esz};

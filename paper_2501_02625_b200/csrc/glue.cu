@@ -59,6 +59,32 @@ __global__ void __launch_bounds__(256) k_add(const T* __restrict__ a, const T* _
     }
 }
 
+// HQ-FSDP reduce-scatter, owner side (hqfsdp.hpp:271-300): out[i] =
+// T(sum_w double(recv[w][i]) / world), accumulated in double in rank order
+template <typename T>
+__global__ void __launch_bounds__(256) k_rank_mean(const float* __restrict__ recv, int world, int64_t n,
+                                                   T* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < world; ++w) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(recv + (int64_t)w * n + i));
+            acc[0] += (double)v.x;
+            acc[1] += (double)v.y;
+            acc[2] += (double)v.z;
+            acc[3] += (double)v.w;
+        }
+        float r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = (float)(acc[j] / (double)world);
+        if constexpr (sizeof(T) == 4) {
+            *reinterpret_cast<float4*>(out + i) = make_float4(r[0], r[1], r[2], r[3]);
+        } else {
+            *reinterpret_cast<uint2*>(out + i) = make_uint2(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]));
+        }
+    }
+}
+
 static unsigned ew_grid(int64_t n) {
     int64_t want = (n / 8 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * 8;
@@ -86,6 +112,14 @@ void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cuda
     else
         k_add<float><<<ew_grid(n), 256, 0, st>>>(static_cast<const float*>(a), static_cast<const float*>(b),
                                                   static_cast<float*>(out), n);
+}
+
+void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st) {
+    const unsigned grid = ew_grid(n * 2);
+    if (dtype == DT_BF16)
+        k_rank_mean<__nv_bfloat16><<<grid, 256, 0, st>>>(recv, world, n, static_cast<__nv_bfloat16*>(out));
+    else
+        k_rank_mean<float><<<grid, 256, 0, st>>>(recv, world, n, static_cast<float*>(out));
 }
 
 }  // namespace halo_b200

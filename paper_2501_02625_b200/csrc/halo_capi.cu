@@ -194,10 +194,16 @@ struct halo_linear {
     bool sharded = false;
     Buffer shard_maps;
     ShardSpec shard_n{}, shard_k{};  // split along N (F GEMM) / along K (E GEMM)
+    // HQ-FSDP gradient reduce-scatter fused into the G GEMM: fp32 partial
+    // rows stored straight into the owners' receive buffers
+    bool scatter = false;
+    Buffer scatter_maps;
+    ScatterSpec scatter_c{};
     ~halo_linear() {
         frozen.release();
         frozen_dev.release();
         shard_maps.release();
+        scatter_maps.release();
     }
 };
 
@@ -376,6 +382,34 @@ extern "C" halo_status halo_rotate_quantize(const void* a, int32_t a_dtype, int6
 namespace {
 __global__ void k_word_to_float(const unsigned* w, float* out) { *out = __uint_as_float(*w); }
 }  // namespace
+
+// Phase B only, under a given absmax (e.g. the HQ-FSDP absmax exchanged
+// over the ranks): the scale is derived in-kernel exactly as from the
+// layer's own phase A (compute_scales, quantize.hpp:134-160).
+extern "C" halo_status halo_rotate_quantize_amax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                                 int64_t had_block, int32_t format, const float* amax,
+                                                 uint8_t* codes, float* scale_out, halo_stream_t stream) {
+    if (!a || !codes || !amax) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: null pointer");
+    if (!valid_dtype(a_dtype) || !valid_format(format))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: bad dtype/format");
+    if (rows < 0 || cols <= 0 || cols % 16)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: cols must be a positive multiple of 16");
+    if (rows == 0) return HALO_OK;
+    DevScalars* d = free_scalars();
+    if (!d) return HALO_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    // the absmax word is the float's bit pattern (non-negative)
+    unsigned* word = reinterpret_cast<unsigned*>(const_cast<float*>(amax));
+    ProfScope ps(PC_K1, (double)rows * cols * (dt_bytes(a_dtype) + 1), st);
+    if (had_block >= 0) {
+        int64_t B;
+        if (resolve_block(cols, had_block, &B, "rotate_quantize_amax") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+        run_rows(a, a_dtype, rows, cols, B, 1, format, word, nullptr, codes, nullptr, 0, &d->err, scale_out, st);
+    } else {
+        run_plain(a, a_dtype, rows * cols, 1, format, word, nullptr, codes, &d->err, scale_out, st);
+    }
+    return cuda_check("rotate_quantize_amax");
+}
 
 extern "C" halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
                                           int64_t had_block, float* absmax_out, halo_stream_t stream) {
@@ -661,6 +695,40 @@ extern "C" halo_status halo_linear_set_qweight_sharded(halo_linear* l, const uin
     return HALO_OK;
 }
 
+extern "C" halo_status halo_linear_set_grad_scatter(halo_linear* l, void* const* recv, int32_t parts, int32_t rank) {
+    if (!l) return fail(HALO_ERR_INVALID_ARGUMENT, "set_grad_scatter: null layer");
+    if (!recv || parts <= 0) {
+        l->scatter = false;
+        return HALO_OK;
+    }
+    if (parts > 64 || rank < 0 || rank >= parts || l->n % parts || (l->n / parts) % 256 || l->m % 4)
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "set_grad_scatter: out_features must split into parts of a multiple of 256 rows");
+    for (int i = 0; i < parts; ++i)
+        if (!recv[i] || (uintptr_t)recv[i] % 16)
+            return fail(HALO_ERR_INVALID_ARGUMENT, "set_grad_scatter: receive buffers must be 16 B aligned");
+    std::vector<CUtensorMap> maps((size_t)parts);
+    const int64_t len = l->n / parts;
+    if (!encode_scatter_maps(recv, parts, rank, len, l->m, maps.data()))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "set_grad_scatter: tensor map encoding failed");
+    if (l->scatter_maps.ensure(maps.size() * sizeof(CUtensorMap)) != HALO_OK) return HALO_ERR_CUDA;
+    if (cudaMemcpy(l->scatter_maps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+        return fail(HALO_ERR_CUDA, "set_grad_scatter: map upload failed");
+    l->scatter_c = ScatterSpec{l->scatter_maps.as<CUtensorMap>(), maps[0], (int)parts, len};
+    l->scatter = true;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_reduce_scatter_shard(const float* recv, int32_t world, int64_t rows, int64_t cols,
+                                                 void* out, int32_t out_dtype, halo_stream_t stream) {
+    if (!recv || !out || world < 1 || rows <= 0 || cols <= 0 || !valid_dtype(out_dtype) || (rows * cols) % 4)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "reduce_scatter_shard: bad argument");
+    ProfScope ps(PC_GLUE, (double)rows * cols * (4.0 * world + dt_bytes(out_dtype)), (cudaStream_t)stream);
+    run_rank_mean(recv, world, rows * cols, out, out_dtype, (cudaStream_t)stream);
+    return cuda_check("reduce_scatter_shard");
+}
+
 extern "C" halo_status halo_ctx_create(halo_ctx** out) {
     if (!out) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: null");
     auto* c = new halo_ctx();
@@ -914,7 +982,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         if (c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
         // (H_b E_Y)_Q and (E_Y)_Q in one pass (:399 and :371); the plain
         // codes only feed G, so PEFT / no-grad_w backwards skip them (:446-448)
-        const bool plain = grad_w && !s.peft;
+        const bool plain = (grad_w || l->scatter) && !s.peft;
         // absmax words already produced by halo_swiglu_backward_absmax for
         // this E_Y: skip K2's phase A
         const bool have_amax = c->e_amax_src == e_y && c->e_amax_b == b && e_dtype == HALO_DTYPE_BF16;
@@ -975,9 +1043,23 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     // ---- gradient path (:418-439): G = (E_Y^T)_Q (XH)_Q [H^T]; a PEFT layer
     // has no weight gradient (its U/V gradients are working-precision
     // matmuls of the caller, :312-318)
-    if (grad_w && !s.peft) {
+    if ((grad_w || l->scatter) && !s.peft) {
         const uint8_t* xq = c->xq_codes();
         const float* sxp = c->xq_scale;
+        if (l->scatter) {
+            // fp32 partial G of this rank's tokens, rows scattered to their
+            // owners (the reduce-scatter of hqfsdp.hpp:271-300 fused into the
+            // GEMM); halo_reduce_scatter_shard finishes the mean
+            if (s.G.right && !(fuse_k4() && fusable_block(Bm)))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "backward: scattered G needs the fused right transform");
+            ShardScope scat(nullptr, nullptr, &l->scatter_c);
+            const int gr = s.G.right ? prof_gemm_x(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp,
+                                                   nullptr, 0, Bm, 0, m, st)
+                                     : prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp,
+                                                 nullptr, 0, st);
+            if (gr != 0) return fail(HALO_ERR_CUDA, "backward: scattered G GEMM launch failed");
+            return cuda_check("backward");
+        }
         if (s.G.right && fuse_k4() && fusable_block(Bm)) {
             // grad_w = (E_Y^T)_Q (XH)_Q H^T (:433-437), the right transform in
             // the GEMM epilogue

@@ -56,10 +56,21 @@ struct ShardSpec {
     int64_t len;
     int along_k;
 };
+// Scattered fp32 C (the HQ-FSDP gradient reduce-scatter fused into the G
+// GEMM): rows [i*len, (i+1)*len) of C are TMA-stored through maps[i] into
+// this rank's slot of rank i's receive buffer (encode_scatter_maps).
+struct ScatterSpec {
+    const CUtensorMap* maps;  // device
+    CUtensorMap maps_host0;
+    int parts;
+    int64_t len;
+};
 struct ShardScope {
-    ShardScope(const ShardSpec* a, const ShardSpec* b);
+    ShardScope(const ShardSpec* a, const ShardSpec* b, const ScatterSpec* c = nullptr);
     ~ShardScope();
 };
+// receive buffers recv[i] = [parts][len][cols] fp32 of rank i; maps for slot `slot`
+bool encode_scatter_maps(void* const* recv, int parts, int slot, int64_t len, int64_t cols, CUtensorMap* out);
 bool encode_shard_maps(const uint8_t* const* parts, int n, int64_t inner, int64_t rows, CUtensorMap* out);
 
 // as run_gemm_x with optional per-row (sa_vec[M]) / per-column (sb_vec[N])
@@ -113,5 +124,7 @@ void set_last_error(const char* msg);
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);
 void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void* dU, int64_t n, cudaStream_t st);
 void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st);
+// out[i] = T(sum_w double(recv[w*n + i]) / world), n % 4 == 0
+void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st);
 
 }  // namespace halo_b200

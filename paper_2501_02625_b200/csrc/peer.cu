@@ -13,7 +13,11 @@
 // "shards written" / "shards no longer read" barriers, stream-ordered, with
 // no host round trip.
 //
-// Mailbox layout (u32): [0, world) flags, [world, 2 world) absmax words.
+// Mailbox layout (u32): [0, world) flags, [world, 3 world) absmax words in
+// two banks by epoch parity.  A rank can run at most one epoch ahead of a
+// peer's read of its box (posting epoch e + 2 needs that peer's e + 1 flag,
+// raised only after its epoch-e kernel has read the box), so two banks keep
+// a fast rank from overwriting a value a slow one has not read yet.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,7 +47,8 @@ __global__ void k_peer_sync(PeerBoxes boxes, int world, int rank, unsigned epoch
     const int j = threadIdx.x;
     if (j < world) {
         unsigned* peer = boxes.box[j];
-        if (amax_in) peer[world + rank] = __float_as_uint(fabsf(*amax_in));
+        const int bank = world + (int)(epoch & 1u) * world;
+        if (amax_in) peer[bank + rank] = __float_as_uint(fabsf(*amax_in));
         st_release_sys(peer + rank, epoch);  // orders the absmax word before the flag
         const unsigned* mine = boxes.box[rank];
         // flags grow monotonically; (int) difference tolerates wrap-around
@@ -53,8 +58,9 @@ __global__ void k_peer_sync(PeerBoxes boxes, int world, int rank, unsigned epoch
     if (amax_out && j == 0) {
         const unsigned* mine = boxes.box[rank];
         unsigned m = 0;
+        const int bank = world + (int)(epoch & 1u) * world;
         for (int i = 0; i < world; ++i) {
-            const unsigned v = ld_acquire_sys(mine + world + i);
+            const unsigned v = ld_acquire_sys(mine + bank + i);
             m = v > m ? v : m;  // non-negative floats order like their bits
         }
         *amax_out = __uint_as_float(m);

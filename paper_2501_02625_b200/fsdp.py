@@ -355,9 +355,12 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
     one stream-ordered mailbox kernel each (halo_peer_sync); the backward
     regather (:243-266) is free because the forward's codes stay resident
     under the saved scale.  The next step's first mailbox barrier also
-    guarantees no peer still reads a shard when it is re-quantized.  Weight
-    gradients are reduce-scattered as in FsdpHaloMLP.  Needs
-    out_features % (world * 256) == 0 for every projection.
+    guarantees no peer still reads a shard when it is re-quantized.  The
+    weight-gradient reduce-scatter (:271-300) is fused into the G GEMMs: each
+    rank's epilogue TMA-stores its fp32 partial rows into the owning rank's
+    receive slot over NVLink, and after one mailbox barrier the owner takes
+    the rank-order double mean -- the reference's arithmetic, bit for bit.
+    Needs out_features % (world * 256) == 0 for every projection.
     """
 
     def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16):
@@ -370,11 +373,14 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
         code_dt = torch.int8 if self.fmt == INT8 else torch.uint8
         self.local = [PeerBuffer(p.shard_rows * p.cols) for p in self.params]
         self.local_views = [b.tensor((p.shard_rows, p.cols), code_dt) for b, p in zip(self.local, self.params)]
-        self.mailbox = PeerBuffer(2 * self.world * 4)
+        self.mailbox = PeerBuffer(3 * self.world * 4)  # flags + two absmax banks (halo_peer_sync)
         dev = self.params[0].master.device
         self.amax = [torch.zeros(1, dtype=torch.float32, device=dev) for _ in self.params]
         self.scales = [torch.ones(1, dtype=torch.float32, device=dev) for _ in self.params]
-        handles = _exchange(([b.handle() for b in self.local], self.mailbox.handle()), group)
+        # receive buffers of the fused gradient reduce-scatter: [world][shard_rows][cols] fp32
+        self.recv = [PeerBuffer(self.world * p.shard_rows * p.cols * 4) for p in self.params]
+        handles = _exchange(([b.handle() for b in self.local], self.mailbox.handle(),
+                             [b.handle() for b in self.recv]), group)
         self._opened = []
         self.parts = []
         for i in range(len(self.params)):
@@ -395,9 +401,21 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
                 ptr = _ipc_open(handles[j][1])
                 self._opened.append(ptr)
                 self.boxes.append(ptr)
+        self.recv_parts = []
+        for i in range(len(self.params)):
+            row = []
+            for j in range(self.world):
+                if j == self.rank:
+                    row.append(self.recv[i].ptr)
+                else:
+                    ptr = _ipc_open(handles[j][2][i])
+                    self._opened.append(ptr)
+                    row.append(ptr)
+            self.recv_parts.append(row)
         self.epoch = 0
-        for layer, parts, scale in zip(self.layers, self.parts, self.scales):
+        for layer, parts, scale, recv in zip(self.layers, self.parts, self.scales, self.recv_parts):
             layer.set_qweight_sharded(parts, scale, keepalive=self)
+            layer.set_grad_scatter(recv, self.rank)
 
     def _sync(self, amax_in=None, amax_out=None):
         import ctypes as C
@@ -409,17 +427,24 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
                                    halo._stream()))
 
     def forward(self, x):
+        import ctypes as C
+        from . import halo
+        from ._lib import check, lib
         ops = CudaOps()
         for i, p in enumerate(self.params):
             am = ops.absmax(p.master, self.block, self.rotate).reshape(1).float()
             # absmax "all-reduce": posted to every mailbox, max taken on device
             self._sync(am, self.amax[i])
-            self.scales[i].copy_(scale_from_absmax(self.amax[i], p.format))
+            # quantize straight into the IPC-exported shard; the kernel derives
+            # the shared scale from the exchanged absmax (compute_scales)
+            check(lib().halo_rotate_quantize_amax(halo._ptr(p.master), halo._dt(p.master), p.shard_rows, p.cols,
+                                                  self.block if self.rotate else -1, p.format,
+                                                  halo._ptr(self.amax[i]), C.c_void_p(self.local[i].ptr),
+                                                  halo._ptr(self.scales[i]), halo._stream()))
             p.global_scale = self.scales[i]
             p.local_absmax = am
             p.scales_valid = True
             self.ledger.record(self.ledger.scale_reduce, K_SCALE_BYTES, p.world)
-            self.local_views[i].copy_(ops.quantize(p.master, self.block, p.format, self.scales[i], self.rotate))
             elems = p.shard_rows * p.world * p.cols
             self.ledger.record(self.ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
             self.ledger.bf16_gather_payload += 2 * elems
@@ -432,8 +457,21 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
                 raise HaloLogicError("backward_regather: no saved forward scales")
             self.ledger.backward_gathers += 1  # served in place: the codes never left
             self.ledger.backward_consumers += 1
-        dx, grads = self.mlp.backward(dy)
-        shards = [reduce_scatter_grads(g, p, self.ledger, self.group) for g, p in zip(grads, self.params)]
+        # G GEMMs stored every rank's fp32 partial rows into their owners'
+        # receive slots; once all ranks are past them, each owner takes the
+        # rank-order double mean of its rows (hqfsdp.hpp:288-292)
+        dx, _ = self.mlp.backward(dy)
+        self._sync()
+        import ctypes as C
+        from . import halo
+        from ._lib import check, lib
+        shards = []
+        for i, p in enumerate(self.params):
+            g = torch.empty((p.shard_rows, p.cols), dtype=self.layers[i].grad_dtype, device=p.master.device)
+            check(lib().halo_reduce_scatter_shard(C.c_void_p(self.recv[i].ptr), self.world, p.shard_rows, p.cols,
+                                                  halo._ptr(g), halo._dt(g), halo._stream()))
+            self.ledger.record(self.ledger.reduce_scatter, 2 * p.shard_rows * p.world * p.cols, p.world)
+            shards.append(g)
         return dx, shards
 
     def close(self):
@@ -441,8 +479,9 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
         torch.cuda.synchronize()
         for layer in self.layers:
             layer.set_qweight_sharded(None, None)
+            layer.set_grad_scatter(None, 0)
         for ptr in self._opened:
             lib().halo_ipc_close(ptr)
         self._opened = []
-        for b in self.local + [self.mailbox]:
+        for b in self.local + self.recv + [self.mailbox]:
             b.free()

@@ -369,6 +369,19 @@ class HaloLinearLayer:
         self._qweight = (tuple(parts), scale, keepalive)
         check(lib().halo_linear_set_qweight_sharded(self._h, arr, len(ptrs), _ptr(scale)))
 
+    def set_grad_scatter(self, recv, rank: int):
+        """Fuse the HQ-FSDP gradient reduce-scatter into the G GEMM: `recv`
+        are the ranks' receive-buffer addresses ([world][rows/world][in]
+        fp32 each); backward then returns grad_w None and stores this rank's
+        fp32 partial rows into their owners' slots.  None reverts."""
+        if recv is None:
+            self._scatter = None
+            check(lib().halo_linear_set_grad_scatter(self._h, None, 0, 0))
+            return
+        arr = (C.c_void_p * len(recv))(*[int(r) for r in recv])
+        check(lib().halo_linear_set_grad_scatter(self._h, arr, len(recv), rank))
+        self._scatter = tuple(recv)
+
     def forward(self, x: torch.Tensor, ctx: SavedContext) -> torch.Tensor:
         _need_cuda(x)
         if x.dim() != 2 or x.shape[1] != self.in_features:
@@ -403,8 +416,9 @@ class HaloLinearLayer:
             raise ValueError("halo layer: upstream error shape mismatch")
         ex_dt = e_x_dtype or self.out_dtype
         e_x = torch.empty((b, self.in_features), dtype=ex_dt, device=e_y.device)
+        scatter = getattr(self, "_scatter", None) is not None
         g = torch.empty((self.out_features, self.in_features), dtype=self.grad_dtype, device=e_y.device) \
-            if need_grad_w else None
+            if need_grad_w and not scatter else None
         check(lib().halo_linear_backward(self._h, ctx._h, _ptr(e_y), _dt(e_y), _ptr(e_x), _DT[ex_dt], _ptr(g),
                                          _DT[self.grad_dtype], _stream()))
         return BackwardResult(e_x, g)
