@@ -160,7 +160,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens", type=int, default=TOKENS)
     ap.add_argument("--block", type=int, default=BLOCK)
-    ap.add_argument("--fmt", default="int8", choices=["int8", "fp8"])
+    ap.add_argument("--fmt", default="int8", choices=["int8", "fp8", "fp6"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fsdp", action="store_true", help="HQ-FSDP path even at N=1 (always on for N>1)")
@@ -187,7 +187,7 @@ def main():
     from paper_2501_02625_b200 import halo
     from paper_2501_02625_b200.mlp import HaloMLP, profile_enable, profile_read
 
-    fmt = halo.INT8 if args.fmt == "int8" else halo.FP8_E4M3
+    fmt = {"int8": halo.INT8, "fp8": halo.FP8_E4M3, "fp6": halo.FP6_E3M2}[args.fmt]
     b = args.tokens
     g = torch.Generator(device=dev).manual_seed(1234)  # weights: identical on every rank
     bf = torch.bfloat16
@@ -357,7 +357,7 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int8" if fmt == halo.INT8 else "fp8_e4m3", "data": "synthetic",
+            "vs_baseline": None, "dtype": {halo.INT8: "int8", halo.FP8_E4M3: "fp8_e4m3", halo.FP6_E3M2: "fp6_e3m2"}[fmt], "data": "synthetic",
             "config": {"workload": CONFIG_NAME, "global_batch": b * world, "seq_len": None,
                        "tokens_per_gpu": b, "hadamard_block": args.block,
                        "parallelism": ((f"hq-fsdp{world} (INT8 weight all-gather + regather, bf16 dW "
@@ -368,7 +368,8 @@ def main():
                        "l2": "512 MiB buffer written between timed steps (outside the step events); "
                              "per-step working set ~2 GB > 126 MB L2"},
             "tokens_per_s": world * b * args.steps / (ms / 1e3),
-            "roofline": {"bound": "tensor", "kernel": "k3_gemm (tcgen05 kind::i8)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "k3_gemm (tcgen05 kind::i8)" if fmt == halo.INT8 else "k3_gemm (tcgen05 kind::f8f6f4)",
                          "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TFLOP/s",
                          "frac": round(gemm_tops / int8_peak, 4), "traffic": traffic,
                          "peak_source": f"2 x bf16_tflops_sustained of {peak_src} MEASURED_PEAKS.json "

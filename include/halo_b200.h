@@ -53,7 +53,7 @@ typedef enum halo_status {
 
 /* NumericFormat ids, quantize.hpp:22-29 (FP6/MX/BF16/IDENTITY emulation is
  * not part of this path and is rejected). */
-typedef enum halo_format { HALO_FMT_INT8 = 0, HALO_FMT_FP8_E4M3 = 1 } halo_format;
+typedef enum halo_format { HALO_FMT_INT8 = 0, HALO_FMT_FP8_E4M3 = 1, HALO_FMT_FP6_E3M2 = 2 } halo_format;
 
 typedef enum halo_dtype { HALO_DTYPE_F32 = 0, HALO_DTYPE_BF16 = 1 } halo_dtype;
 

@@ -168,11 +168,30 @@ def quantize(a, fmt=INT8, gran=0, scales=None):
     return codes, s
 
 
+def e3m2_table():
+    """Value of every 6-bit OCP E3M2 code (bias 3, no inf/NaN): the grid of
+    round_minifloat(x, 2, -2, 28) (quantize.hpp:138-150, 164-166)."""
+    c = np.arange(64)
+    e = (c >> 2) & 7
+    m = c & 3
+    v = np.where(e == 0, m * 0.0625, (1 + m / 4.0) * 2.0 ** (e - 3))
+    return np.where(c & 0x20, -v, v).astype(np.float32)
+
+
 def codes_to_bytes(codes, fmt):
+    """Code values -> the device's code bytes (INT8 two's complement, OCP
+    E4M3, and for FP6 the E3M2 code shifted into bits 7:2)."""
     codes = f32(codes)
     if fmt == INT8:
         out = np.empty(codes.shape, np.int8)
         orc().orc_codes_to_int8(codes, codes.size, out)
+    elif fmt == FP6_E3M2:
+        table = e3m2_table()
+        lut = {}
+        for c in range(63, -1, -1):  # 0.0 -> code 0 (the reference's +0)
+            lut[float(table[c])] = c
+        flat = np.array([lut[float(v) if v != 0 else 0.0] for v in codes.ravel()], np.uint8)
+        out = (flat << 2).astype(np.uint8).reshape(codes.shape)
     else:
         out = np.empty(codes.shape, np.uint8)
         orc().orc_codes_to_e4m3(codes, codes.size, out)

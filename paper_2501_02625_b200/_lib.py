@@ -20,6 +20,7 @@ HALO_ERR_CUDA = 4
 
 FMT_INT8 = 0
 FMT_FP8_E4M3 = 1
+FMT_FP6_E3M2 = 2  # one E3M2 code per byte, in bits 7:2 (the tcgen05 kind::f8f6f4 operand form)
 DTYPE_F32 = 0
 DTYPE_BF16 = 1
 OUT_F32, OUT_BF16, OUT_S32 = 0, 1, 2

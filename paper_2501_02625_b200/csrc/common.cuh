@@ -14,7 +14,7 @@
 
 namespace halo_b200 {
 
-enum Fmt : int { FMT_INT8 = 0, FMT_E4M3 = 1 };
+enum Fmt : int { FMT_INT8 = 0, FMT_E4M3 = 1, FMT_E3M2 = 2 };
 enum DType : int { DT_F32 = 0, DT_BF16 = 1 };
 
 // error flag bits written by kernels into the per-call status word
@@ -64,6 +64,7 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float v[8]) {
 template <int FMT>
 __device__ __forceinline__ uint8_t quant1(float x, float s, float inv) {
     if constexpr (FMT == FMT_INT8) return (uint8_t)quant_int8(x, s, inv);
+    else if constexpr (FMT == FMT_E3M2) return (uint8_t)(quant_e3m2(x, s, inv) << 2);  // MMA operand byte
     else return quant_e4m3(x, s, inv);
 }
 

@@ -452,6 +452,7 @@ static void rows_v2_launch(const InT* in, int64_t n, int64_t B, unsigned* amax, 
 bool rows_v2(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
              uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
     if (B < 8 || B > 256) return false;
+    if (mode == V2_QUANT && fmt == FMT_E3M2) return false;  // FP6: fwht3.cu / generic kernels
     if (mode == V2_XFORM) {
         if (in_dtype != DT_F32) return false;
         auto p = static_cast<const float*>(in);
@@ -495,6 +496,7 @@ bool cols_v2(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t
              unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, float* out,
              int64_t rows_out, unsigned* err, float* sro, float* spo, cudaStream_t st) {
     if (B > 256 || cols % 2) return false;
+    if (mode == V2_QUANT && fmt == FMT_E3M2) return false;  // FP6: fwht_cols3.cu / generic kernels
     if (mode == V2_XFORM) {
         if (in_dtype != DT_F32) return false;
         cols_v2_launch<float, 0, V2_XFORM>(static_cast<const float*>(in), b, rows_pad, cols, B, ar, ap, sr, sp, cr, cp,

@@ -120,6 +120,9 @@ __device__ __noinline__ uint32_t exact4(float2 a, float2 b, float s, float inv) 
     if constexpr (FMT == FMT_INT8)
         return pack4((uint8_t)quant_int8(a.x, s, inv), (uint8_t)quant_int8(a.y, s, inv), (uint8_t)quant_int8(b.x, s, inv),
                      (uint8_t)quant_int8(b.y, s, inv));
+    else if constexpr (FMT == FMT_E3M2)
+        return pack4(quant_e3m2(a.x, s, inv) << 2, quant_e3m2(a.y, s, inv) << 2, quant_e3m2(b.x, s, inv) << 2,
+                     quant_e3m2(b.y, s, inv) << 2);
     else
         return pack4(quant_e4m3(a.x, s, inv), quant_e4m3(a.y, s, inv), quant_e4m3(b.x, s, inv), quant_e4m3(b.y, s, inv));
 }
@@ -275,6 +278,8 @@ struct RowsCore {
             // decide its 4 codes exactly right here (divergent but rare)
             if (!(m < thr)) return exact4<FMT>(a, c, s, inv);
             return pack4(__float_as_uint(ta.x), __float_as_uint(ta.y), __float_as_uint(tc.x), __float_as_uint(tc.y));
+        } else if constexpr (FMT == FMT_E3M2) {
+            return e3m2x4_fast(a, c, ilo2, ihi2, s);
         } else {
             uint32_t bad = 0;
             const uint32_t w = e4m3x4_fast(a, c, ilo2, ihi2, s, bad);
@@ -639,6 +644,9 @@ void dispatch_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, uns
         else if (fmt == FMT_INT8) {                                                                                      \
             if (sup) launch_v3<LB, T, FMT_INT8, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);  \
             else launch_v3<LB, T, FMT_INT8, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);     \
+        } else if (fmt == FMT_E3M2) {                                                                                    \
+            if (sup) launch_v3<LB, T, FMT_E3M2, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);  \
+            else launch_v3<LB, T, FMT_E3M2, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);     \
         } else {                                                                                                         \
             if (sup) launch_v3<LB, T, FMT_E4M3, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);  \
             else launch_v3<LB, T, FMT_E4M3, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);     \

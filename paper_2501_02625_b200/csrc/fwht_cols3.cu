@@ -74,6 +74,9 @@ __device__ __noinline__ uint32_t c3_exact4(float2 a, float2 b, float s, float in
     if constexpr (FMT == FMT_INT8)
         return c3_pack4((uint8_t)quant_int8(a.x, s, inv), (uint8_t)quant_int8(a.y, s, inv),
                         (uint8_t)quant_int8(b.x, s, inv), (uint8_t)quant_int8(b.y, s, inv));
+    else if constexpr (FMT == FMT_E3M2)
+        return c3_pack4(quant_e3m2(a.x, s, inv) << 2, quant_e3m2(a.y, s, inv) << 2, quant_e3m2(b.x, s, inv) << 2,
+                        quant_e3m2(b.y, s, inv) << 2);
     else
         return c3_pack4(quant_e4m3(a.x, s, inv), quant_e4m3(a.y, s, inv), quant_e4m3(b.x, s, inv),
                         quant_e4m3(b.y, s, inv));
@@ -138,6 +141,8 @@ struct Quant {
             // uncertified group: decide its 4 codes exactly right here
             if (!(m < thr)) return c3_exact4<FMT>(a, c, s, inv);
             return c3_pack4(__float_as_uint(ta.x), __float_as_uint(ta.y), __float_as_uint(tc.x), __float_as_uint(tc.y));
+        } else if constexpr (FMT == FMT_E3M2) {
+            return e3m2x4_fast(a, c, ilo2, ihi2, s);
         } else {
             uint32_t bad = 0;
             const uint32_t w = e4m3x4_fast(a, c, ilo2, ihi2, s, bad);
@@ -613,6 +618,7 @@ void c3_dispatch(int mode, int fmt, int in_dtype, const void* in, int64_t b, int
         auto p = static_cast<const T*>(in);                                                                        \
         if (mode == C3_ABSMAX) c3_launch<LB, T, 0, C3_ABSMAX, false, false>(p, b, rows_pad, cols, ar, ap, sr, sp, cr, cp, err, sro, spo, st); \
         else if (fmt == FMT_INT8) HALO_C3Q(T, FMT_INT8)                                                            \
+        else if (fmt == FMT_E3M2) HALO_C3Q(T, FMT_E3M2)                                                            \
         else HALO_C3Q(T, FMT_E4M3)                                                                                 \
     }
     if (in_dtype == DT_BF16) HALO_C3(__nv_bfloat16) else HALO_C3(float)

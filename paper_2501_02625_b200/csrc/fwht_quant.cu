@@ -314,6 +314,7 @@ static void rows_dispatch(int mode, int fmt, const InT* in, int64_t rows, int64_
         } else {
             if (mode == MODE_ABSMAX) launch_rows_small<InT, 0, MODE_ABSMAX, OutT>(lb, in, n, norm, amax, sup, codes, out, err, sout, st);
             else if (fmt == FMT_INT8) launch_rows_small<InT, FMT_INT8, MODE_QUANT, OutT>(lb, in, n, norm, amax, sup, codes, out, err, sout, st);
+            else if (fmt == FMT_E3M2) launch_rows_small<InT, FMT_E3M2, MODE_QUANT, OutT>(lb, in, n, norm, amax, sup, codes, out, err, sout, st);
             else launch_rows_small<InT, FMT_E4M3, MODE_QUANT, OutT>(lb, in, n, norm, amax, sup, codes, out, err, sout, st);
         }
         return;
@@ -326,6 +327,7 @@ static void rows_dispatch(int mode, int fmt, const InT* in, int64_t rows, int64_
     } else {
         if (mode == MODE_ABSMAX) HALO_G(0, MODE_ABSMAX);
         else if (fmt == FMT_INT8) HALO_G(FMT_INT8, MODE_QUANT);
+        else if (fmt == FMT_E3M2) HALO_G(FMT_E3M2, MODE_QUANT);
         else HALO_G(FMT_E4M3, MODE_QUANT);
     }
 #undef HALO_G
@@ -338,6 +340,7 @@ static void plain_dispatch(int mode, int fmt, const InT* in, int64_t n, unsigned
     const unsigned blocks = grid_cap((n / 8 + 255) / 256, 8);
     if (mode == MODE_ABSMAX) k_plain<InT, 0, MODE_ABSMAX><<<blocks, 256, 0, st>>>(in, n, amax, sup, codes, err, sout);
     else if (fmt == FMT_INT8) k_plain<InT, FMT_INT8, MODE_QUANT><<<blocks, 256, 0, st>>>(in, n, amax, sup, codes, err, sout);
+    else if (fmt == FMT_E3M2) k_plain<InT, FMT_E3M2, MODE_QUANT><<<blocks, 256, 0, st>>>(in, n, amax, sup, codes, err, sout);
     else k_plain<InT, FMT_E4M3, MODE_QUANT><<<blocks, 256, 0, st>>>(in, n, amax, sup, codes, err, sout);
 }
 
@@ -360,6 +363,7 @@ static void cols_dispatch(int mode, int fmt, const InT* in, int64_t b, int64_t r
         if constexpr (std::is_same<InT, float>::value) HALO_G(0, MODE_XFORM);
     } else {
         if (fmt == FMT_INT8) HALO_G(FMT_INT8, MODE_QUANT);
+        else if (fmt == FMT_E3M2) HALO_G(FMT_E3M2, MODE_QUANT);
         else HALO_G(FMT_E4M3, MODE_QUANT);
         if (cp) plain_dispatch<InT>(MODE_QUANT, fmt, in, b * cols, ap, sp, cp, err, spo, st);
     }

@@ -357,9 +357,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
 
 // instruction descriptor (kind::i8 / kind::f8f6f4, dense)
 __host__ __device__ constexpr uint32_t make_idesc(int fmt, int a_mn, int b_mn, int M, int N) {
-    return (uint32_t)((fmt == FMT_INT8 ? 2u : 1u) << 4)         // D format: s32 / f32
-           | (uint32_t)((fmt == FMT_INT8 ? 1u : 0u) << 7)       // A: signed int8 / e4m3
-           | (uint32_t)((fmt == FMT_INT8 ? 1u : 0u) << 10)      // B
+    // A/B type: kind::i8 1 = signed; kind::f8f6f4 0 = E4M3, and for FP6 E3M2
+    // held in bits 7:2 of each byte the type code 2 -- measured on this B200
+    // (tools/fp6_probe.py: code 2 with MSB-aligned E3M2 reproduces every
+    // 64 x 64 code product exactly; the other codes / alignments do not)
+    return (uint32_t)((fmt == FMT_INT8 ? 2u : 1u) << 4)                           // D format: s32 / f32
+           | (uint32_t)((fmt == FMT_INT8 ? 1u : fmt == FMT_E3M2 ? 2u : 0u) << 7)  // A
+           | (uint32_t)((fmt == FMT_INT8 ? 1u : fmt == FMT_E3M2 ? 2u : 0u) << 10) // B
            | (uint32_t)(a_mn ? 1u : 0u) << 15 | (uint32_t)(b_mn ? 1u : 0u) << 16 |
            (uint32_t)(N >> 3) << 17 | (uint32_t)(M >> 4) << 24;
 }
@@ -1041,6 +1045,7 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         return e ? atoi(e) : 0;
     }();
     args.dbg_skip_epi = dbg;
+
     // HALO_GEMM_CG=1 pins the single-CTA kernel (A/B runs)
     static const int cg_env = [] {
         const char* e = getenv("HALO_GEMM_CG");
@@ -1098,15 +1103,15 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     const int tiles = (int)(((M + tile_m - 1) / tile_m) * ((N + BN - 1) / BN));
     if (cg == 1) {
         const int grid = tiles < num_sms() ? tiles : num_sms();
-        auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 1> : k_gemm<FMT_E4M3, 1>;
+        auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 1> : fmt == FMT_E3M2 ? k_gemm<FMT_E3M2, 1> : k_gemm<FMT_E4M3, 1>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<1>());
         kern<<<grid, GEMM_THREADS, gemm_smem<1>(), st>>>(ma, mb, mc, args);
     } else {
-        auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 2> : k_gemm<FMT_E4M3, 2>;
+        auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 2> : fmt == FMT_E3M2 ? k_gemm<FMT_E3M2, 2> : k_gemm<FMT_E4M3, 2>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<2>());
         // persistent: as many co-resident pairs as the GPCs can host
-        static int max_pairs[2] = {0, 0};
-        int& mp = max_pairs[fmt == FMT_INT8 ? 0 : 1];
+        static int max_pairs[3] = {0, 0, 0};
+        int& mp = max_pairs[fmt == FMT_INT8 ? 0 : fmt == FMT_E3M2 ? 2 : 1];
         cudaLaunchConfig_t cfg = {};
         cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
         cfg.dynamicSmemBytes = gemm_smem<2>();

@@ -60,7 +60,10 @@ halo_status resolve_block(int64_t d, int64_t had_block, int64_t* B, const char* 
     return HALO_OK;
 }
 
-bool valid_format(int32_t f) { return f == HALO_FMT_INT8 || f == HALO_FMT_FP8_E4M3; }
+// INT8, FP8 E4M3 and FP6 E3M2 (one code per byte, the E3M2 bits in 7:2:
+// the tcgen05 kind::f8f6f4 operand form)
+bool valid_format(int32_t f) { return f == HALO_FMT_INT8 || f == HALO_FMT_FP8_E4M3 || f == HALO_FMT_FP6_E3M2; }
+bool valid_gemm_format(int32_t f) { return valid_format(f); }
 bool valid_dtype(int32_t d) { return d == HALO_DTYPE_F32 || d == HALO_DTYPE_BF16; }
 
 // device scalar block: absmax words, scales, error flag
@@ -285,7 +288,7 @@ static halo_status placement_from(const char* s, size_t len, halo_placement* p) 
 // halo_linear.hpp:81-152
 extern "C" halo_status halo_scheme_from_string(const char* id, int32_t format, int64_t had_block, halo_scheme* out) {
     if (!id || !out) return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: null argument");
-    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: format must be int8 or fp8_e4m3");
+    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "scheme: format must be int8, fp8_e4m3 or fp6_e3m2");
     halo_scheme s;
     std::memset(&s, 0, sizeof(s));
     s.format_x = s.format_w = s.format_e = format;
@@ -493,7 +496,7 @@ extern "C" halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_
                                     int32_t b_kmajor, int64_t M, int64_t N, int64_t K, const float* scale_a,
                                     const float* scale_b, void* out, int32_t out_kind, halo_stream_t stream) {
     if (!a || !b || !out || !scale_a || !scale_b) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: null pointer");
-    if (!valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad format");
+    if (!valid_gemm_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad format");
     if (out_kind < 0 || out_kind > 2) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad out kind");
     const int r = prof_gemm(format, a, b, M, N, K, a_kmajor, b_kmajor, scale_a, scale_b, out, out_kind,
                            (cudaStream_t)stream);
@@ -527,7 +530,8 @@ extern "C" halo_status halo_rotate_quantize_rows(const void* a, int32_t a_dtype,
                                                  int64_t had_block, int32_t format, uint8_t* codes, float* scales_out,
                                                  halo_stream_t stream) {
     if (!a || !codes || !scales_out) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: null pointer");
-    if (!valid_dtype(a_dtype) || !valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: bad dtype/format");
+    if (!valid_dtype(a_dtype) || !valid_format(format) || format == HALO_FMT_FP6_E3M2)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: bad dtype/format (int8 or fp8_e4m3)");
     if (rows < 0 || cols <= 0 || cols % 256)
         return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: cols must be a positive multiple of 256");
     if (rows == 0) return HALO_OK;
@@ -575,7 +579,9 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     "halo layer: row granularity needs in_features % 256 == 0 and a Hadamard block <= 256");
     if (!valid_format(s.format_x) || s.format_x != s.format_w || s.format_x != s.format_e)
-        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: X/W/E formats must agree and be int8 or fp8_e4m3");
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: X/W/E formats must agree and be int8, fp8_e4m3 or fp6_e3m2");
+    if (s.format_x == HALO_FMT_FP6_E3M2 && s.granularity != HALO_GRAN_TENSOR)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: fp6_e3m2 on the device path uses tensor granularity");
     if (s.F.left || s.F.right) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_F must be O or M (apply_placement engine is not on the device path)");
     if (s.E.middle) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_E with M is not on the device path");
     if (s.G.left || s.G.middle) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_G must be O or R");

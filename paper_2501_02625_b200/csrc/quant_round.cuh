@@ -144,6 +144,65 @@ HALO_HD uint8_t quant_e4m3(float x, float s, float inv_s) {
     return (mag != 0 && x < 0.0f) ? (uint8_t)(mag | 0x80) : mag;
 }
 
+// ---------------------------------------------------------- FP6 E3M2 ----
+// quantize.hpp:138-150, 164-166: round_minifloat(x, 2 mantissa bits, min_exp
+// -2, saturate 28); zero is +0.  Code: OCP E3M2 (bias 3, no inf/NaN),
+// S.EEE.MM in the low 6 bits.  Device tensors hold the code shifted left by
+// two (bits 7:2 of the byte), the layout tcgen05 kind::f8f6f4 reads FP6
+// operands in (measured: tools/fp6_probe.py).
+HALO_HD float e3m2_step(float v) {
+    int e = (v > 0.0f) ? ilog2_pos(v) : -2;
+    if (e < -2) e = -2;
+    return ldexpf(1.0f, e - 2);
+}
+HALO_HD uint8_t e3m2_bits_pos(float v) {  // grid value (<= 28) -> 5 magnitude bits
+    if (v == 0.0f) return 0;
+    const int e = ilog2_pos(v);
+    if (e < -2) return (uint8_t)(int)(v * 16.0f);  // subnormal: m * 2^-4
+    const int mant = (int)((ldexpf(v, -e) - 1.0f) * 4.0f);
+    return (uint8_t)(((e + 3) << 2) | mant);
+}
+// 6-bit code of round_code(x / s, Fp6E3M2) (low-aligned)
+HALO_HD uint8_t quant_e3m2(float x, float s, float inv_s) {
+    const float a = fabsf(x);
+    const float y = a * inv_s;
+    float q0;
+    if (y >= 31.0f) {
+        q0 = 32.0f;  // beyond saturation; fixed below
+    } else {
+        const float st = e3m2_step(y);
+        q0 = rintf(y / st) * st;
+    }
+    float q = q0;
+    const float up = e3m2_step(q0);
+    const float mid_up = q0 + 0.5f * up;
+    const float r_up = fmaf(-mid_up, s, a);
+    if (r_up > 0.0f) {
+        q = q0 + up;
+    } else if (r_up == 0.0f) {
+        q = (e3m2_bits_pos(q0 > 28.0f ? 28.0f : q0) & 1) ? q0 + up : q0;
+    } else if (q0 > 0.0f) {
+        float dn = up;
+        if (q0 <= 28.0f && ldexpf(1.0f, ilog2_pos(q0)) == q0 && ilog2_pos(q0) > -2) dn = 0.5f * up;
+        const float mid_dn = q0 - 0.5f * dn;
+        const float r_dn = fmaf(-mid_dn, s, a);
+        if (r_dn < 0.0f) {
+            q = q0 - dn;
+        } else if (r_dn == 0.0f) {
+            const float lowv = q0 - dn;
+            q = (e3m2_bits_pos(lowv) & 1) ? q0 : lowv;
+        }
+    }
+    if (q > 28.0f) q = 28.0f;
+    const uint8_t mag = e3m2_bits_pos(q);
+    return (mag != 0 && x < 0.0f) ? (uint8_t)(mag | 0x20) : mag;
+}
+HALO_HD float e3m2_to_float(uint8_t c) {  // low-aligned code
+    const int e = (c >> 2) & 7, m = c & 3;
+    const float v = e == 0 ? (float)m * 0.0625f : (1.0f + (float)m * 0.25f) * ldexpf(1.0f, e - 3);
+    return (c & 0x20) ? -v : v;
+}
+
 // ------------------------------------------------------------ fast paths --
 // Same functions, cheaper common case: when y = x * inv sits closer than
 // kFastMargin (below) to the rounded grid value, the true quotient is
@@ -286,6 +345,45 @@ __device__ __forceinline__ uint32_t e4m3x4_fast(float2 a, float2 c, float2 inv_l
     const uint32_t nz = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;  // bytes with a nonzero magnitude
     return w & (nz | 0x7F7F7F7Fu);
 }
+// E3M2 counterpart of e4m3_word / e4m3x4_fast: the hardware F2FP
+// (cvt.rn.satfinite.e3m2x2.f32, RNE, saturating at 28) on the bracketed
+// quotients, one fma per disagreeing byte, +0 for zero magnitudes; returns
+// the 4 codes shifted into bits 7:2 of their bytes (the MMA operand form).
+__device__ __forceinline__ uint32_t e3m2_word(float2 a, float2 c) {
+    uint32_t w;
+    asm("{\n\t.reg .b16 lo, hi;\n\t"
+        "cvt.rn.satfinite.e3m2x2.f32 lo, %2, %1;\n\t"
+        "cvt.rn.satfinite.e3m2x2.f32 hi, %4, %3;\n\t"
+        "mov.b32 %0, {lo, hi};\n\t}"
+        : "=r"(w)
+        : "f"(a.x), "f"(a.y), "f"(c.x), "f"(c.y));
+    return w;
+}
+__device__ __forceinline__ float e3m2_mag(uint32_t b) {  // magnitude code 0..0x1F
+    const uint32_t e = b >> 2, m = b & 3u;
+    return e ? __uint_as_float(((e + 124u) << 23) | (m << 21)) : (float)m * 0.0625f;
+}
+__device__ __forceinline__ uint32_t e3m2x4_fast(float2 a, float2 c, float2 inv_lo2, float2 inv_hi2, float s) {
+    const uint32_t wl = e3m2_word(__fmul2_rn(a, inv_lo2), __fmul2_rn(c, inv_lo2));
+    const uint32_t wh = e3m2_word(__fmul2_rn(a, inv_hi2), __fmul2_rn(c, inv_hi2));
+    uint32_t w = wl;
+    const uint32_t diff = wl ^ wh;
+    if (diff) {
+        const float xs[4] = {a.x, a.y, c.x, c.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if ((diff >> (8 * i)) & 0xFFu) {
+                const uint32_t bl = (wl >> (8 * i)) & 0x1Fu, bh = (wh >> (8 * i)) & 0x1Fu;
+                const float mid = 0.5f * (e3m2_mag(bl) + e3m2_mag(bh));
+                const float r = fmaf(-mid, s, fabsf(xs[i]));
+                const uint32_t pick = r > 0.f ? bh : (r < 0.f ? bl : ((bl & 1u) ? bh : bl));
+                w = (w & ~(0x1Fu << (8 * i))) | (pick << (8 * i));
+            }
+        }
+    }
+    const uint32_t nz = ((w & 0x1F1F1F1Fu) + 0x1F1F1F1Fu) & 0x20202020u;  // bytes with a nonzero magnitude
+    return (w & (nz | 0x1F1F1F1Fu)) << 2;
+}
 __device__ __forceinline__ void e4m3_brackets(float inv, float2& lo2, float2& hi2) {
     const float lo = __fmul_rn(inv, 1.0f - 4.76837158203125e-07f), hi = __fmul_rn(inv, 1.0f + 4.76837158203125e-07f);
     lo2 = make_float2(lo, lo);
@@ -304,7 +402,7 @@ HALO_HD float e4m3_to_float(uint8_t b) {
 // 1.0 for an all-zero tensor.
 HALO_HD float scale_from_absmax(float absmax, int fmt) {
     if (absmax == 0.0f) return 1.0f;
-    const double fmax = fmt == 0 ? 127.0 : 448.0;
+    const double fmax = fmt == 0 ? 127.0 : fmt == 1 ? 448.0 : 28.0;  // format_max, quantize.hpp:53-63
     return (float)((double)absmax / fmax);
 }
 

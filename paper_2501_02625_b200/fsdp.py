@@ -34,18 +34,21 @@ import torch.distributed as dist
 
 from ._lib import HaloLogicError
 
-INT8, FP8_E4M3 = 0, 1
-_FMAX = {INT8: 127.0, FP8_E4M3: 448.0}
+INT8, FP8_E4M3, FP6_E3M2 = 0, 1, 2
+_FMAX = {INT8: 127.0, FP8_E4M3: 448.0, FP6_E3M2: 28.0}
 K_SCALE_BYTES = 4  # hqfsdp.hpp:55
 
 
 # ------------------------------------------------------------ byte model --
 
 def code_payload_bytes(fmt: int, elems: int) -> int:
-    """hqfsdp.hpp:36-49 (INT8/FP8 one byte per code)."""
+    """hqfsdp.hpp:36-49: INT8/FP8 one byte per code, FP6 four codes in three
+    bytes (the wire format; the device keeps one code per byte)."""
     if fmt in (INT8, FP8_E4M3):
         return elems
-    raise ValueError("only int8 / fp8_e4m3 payloads are on the device path")
+    if fmt == FP6_E3M2:
+        return (elems + 3) // 4 * 3
+    raise ValueError("only int8 / fp8_e4m3 / fp6_e3m2 payloads are on the device path")
 
 
 @dataclass

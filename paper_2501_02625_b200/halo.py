@@ -32,11 +32,12 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (DTYPE_BF16, DTYPE_F32, FMT_FP8_E4M3, FMT_INT8, OUT_BF16, OUT_F32, OUT_S32,
+from ._lib import (DTYPE_BF16, DTYPE_F32, FMT_FP6_E3M2, FMT_FP8_E4M3, FMT_INT8, OUT_BF16, OUT_F32, OUT_S32,
                    Counters, Scheme, check, lib)
 
 INT8 = FMT_INT8
 FP8_E4M3 = FMT_FP8_E4M3
+FP6_E3M2 = FMT_FP6_E3M2
 
 _DT = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16}
 
@@ -68,6 +69,15 @@ def _need_cuda(*ts):
 
 def code_dtype(fmt):
     return torch.int8 if fmt == INT8 else torch.uint8
+
+
+def fp6_decode(codes: torch.Tensor) -> torch.Tensor:
+    """Values of device FP6 E3M2 code bytes (E3M2 in bits 7:2), fp32."""
+    c = (codes.to(torch.int32) >> 2) & 0x3F
+    e = (c >> 2) & 7
+    m = (c & 3).to(torch.float32)
+    v = torch.where(e == 0, m * 0.0625, (1 + m / 4) * torch.exp2((e - 3).to(torch.float32)))
+    return torch.where((c & 0x20) != 0, -v, v)
 
 
 # ------------------------------------------------------------------ schemes

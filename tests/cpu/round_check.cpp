@@ -30,6 +30,17 @@ static void check(float x, float s, int fmt) {
             if (bad < 5) printf("int8 x=%a s=%a got %d fast %d want %g\n", x, s, got, fast, want);
             ++bad;
         }
+    } else if (fmt == ORC_FP6_E3M2) {
+        const uint8_t got = quant_e3m2(x, s, inv);
+        const float wv = (float)want;
+        // the 6-bit code of the oracle's grid value: decode every code, match
+        uint8_t wb = 0xFF;
+        for (int c = 0; c < 64; ++c)
+            if (e3m2_to_float((uint8_t)c) == wv && !(wv == 0.0f && c != 0)) { wb = (uint8_t)c; break; }
+        if (got != wb) {
+            if (bad < 5) printf("e3m2 x=%a s=%a got %02x want %02x (%g)\n", x, s, got, wb, want);
+            ++bad;
+        }
     } else {
         const uint8_t got = quant_e4m3(x, s, inv);
         uint32_t sl;
@@ -48,8 +59,8 @@ int main(int argc, char** argv) {
     const long long n = argc > 1 ? atoll(argv[1]) : 10000000;
     std::mt19937_64 g(12345);
     std::uniform_real_distribution<double> u(0.0, 1.0);
-    for (int fmt = 0; fmt < 2; ++fmt) {
-        const double fmax = fmt == 0 ? 127.0 : 448.0;
+    for (int fmt = 0; fmt < 3; ++fmt) {
+        const double fmax = fmt == 0 ? 127.0 : fmt == 1 ? 448.0 : 28.0;
         // 1) random scales, values spread over the whole code range
         for (long long i = 0; i < n; ++i) {
             const float s = (float)std::ldexp(1.0 + u(g), (int)(u(g) * 40) - 30);
@@ -61,7 +72,12 @@ int main(int argc, char** argv) {
         //    float neighbours.
         std::vector<double> mids;
         if (fmt == 0) { for (int q = -128; q <= 127; ++q) mids.push_back(q + 0.5); }
-        else {
+        else if (fmt == 2) {
+            std::vector<double> grid;
+            for (int c = 0; c < 32; ++c) grid.push_back(e3m2_to_float((uint8_t)c));
+            grid.push_back(32.0);
+            for (size_t k = 0; k + 1 < grid.size(); ++k) { mids.push_back(0.5 * (grid[k] + grid[k + 1])); mids.push_back(-0.5 * (grid[k] + grid[k + 1])); }
+        } else {
             std::vector<double> grid;
             for (int b = 0; b < 127; ++b) { uint8_t c = (uint8_t)b; grid.push_back(orc_e4m3_to_float(c)); }
             grid.push_back(480.0);
@@ -83,7 +99,8 @@ int main(int argc, char** argv) {
         }
         // 4) saturation and zeros
         for (float s : {1.0f, 0.25f, 3.0f}) {
-            for (float x : {0.0f, -0.0f, 1e-30f, -1e-30f, 1e6f, -1e6f, 127.5f, -127.5f, 464.0f, -464.0f, 448.0f, 447.9f})
+            for (float x : {0.0f, -0.0f, 1e-30f, -1e-30f, 1e6f, -1e6f, 127.5f, -127.5f, 464.0f, -464.0f, 448.0f, 447.9f,
+                            28.0f, 29.9f, 30.0f, -30.0f, 31.0f, 32.0f, 0.03125f, -0.03125f, 0.09375f})
                 check(x * s, s, fmt);
         }
     }

@@ -90,19 +90,23 @@ def test_layer_bf16_outputs_within_tolerance(H, orc, scheme):
 
 
 @pytest.mark.parametrize("scheme", ["halo0", "halo1", "halo2"])
-def test_layer_fp8(H, orc, scheme):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_layer_fp8(H, orc, scheme, fmt):
+    """FP8 E4M3 and FP6 E3M2 layers (tcgen05 kind::f8f6f4): codes and scales
+    bit-exact, outputs within 1e-5 of the reference's dequantized double
+    matmuls."""
     b, m, n, block = 256, 256, 128, 256
     X, W, E = inputs(orc, b, m, n, seed=3)
-    want = orc.linear(LEVELS[scheme], 1, block, X, W, E)
-    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16), H.scheme_from_string(scheme, 1, block),
+    want = orc.linear(LEVELS[scheme], fmt, block, X, W, E)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16), H.scheme_from_string(scheme, fmt, block),
                               out_dtype=torch.float32)
     ctx = H.SavedContext()
     y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
     back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
     xq, sx, wq, sw = ctx.saved(layer)
     assert sx.item() == want["sx"] and sw.item() == want["sw"]
-    assert np.array_equal(xq.cpu().numpy(), orc.codes_to_bytes(want["xq"], 1))
-    assert np.array_equal(wq.cpu().numpy(), orc.codes_to_bytes(want["wq"], 1))
+    assert np.array_equal(xq.cpu().numpy(), orc.codes_to_bytes(want["xq"], fmt))
+    assert np.array_equal(wq.cpu().numpy(), orc.codes_to_bytes(want["wq"], fmt))
     assert rel(y.cpu().numpy(), want["Y"]) < 1e-5
     assert rel(back.e_x.cpu().numpy(), want["EX"]) < 1e-5
     assert rel(back.grad_w.cpu().numpy(), want["GW"]) < 1e-5
