@@ -117,13 +117,24 @@ if "fp8" in what:
     for nm, (r, c) in {"dY": (8192, 4096), "dG": (8192, 14336)}.items():
         e = (torch.randn(r, c, generator=g, device=dev) * 1e-3).to(bf)
         n = r * c
-        for fmt in (0, 1):
+        for fmt in (0, 1, 2):
             timeit(lambda: halo.left_rotate_quantize(e, B, fmt=fmt), nbytes=4 * n, name=f"k2_fmt{fmt}[{nm} {r}x{c}]")
         del e
     for nm, (r, c) in {"X": (8192, 4096), "H": (8192, 14336)}.items():
         a = torch.randn(r, c, generator=g, device=dev).to(bf)
         n = r * c
-        for fmt in (0, 1):
+        for fmt in (0, 1, 2):
             timeit(lambda: halo.rotate_quantize(a, B, fmt=fmt), nbytes=3 * n, name=f"k1_fmt{fmt}[{nm} {r}x{c}]")
             timeit(lambda: halo.rotate_quantize(a, 1, fmt=fmt), nbytes=3 * n, name=f"k1_fmt{fmt}_B1[{nm} {r}x{c}]")
         del a
+    # GEMM throughput per format (F shape of gate_proj, both operands K-major)
+    M, N, K = 8192, 14336, 4096
+    for fmt in (0, 1, 2):
+        A = torch.randint(0, 64, (M, K), device=dev, dtype=torch.int32).to(torch.uint8) << 2
+        Bm = torch.randint(0, 64, (N, K), device=dev, dtype=torch.int32).to(torch.uint8) << 2
+        if fmt == 0:
+            A, Bm = A.view(torch.int8), Bm.view(torch.int8)
+        one = torch.ones(1, device=dev)
+        timeit(lambda: halo.qmatmul(A, Bm, one, one, fmt=fmt, out="bf16"), ops=2.0 * M * N * K,
+               name=f"gemm_fmt{fmt}[{M}x{N}x{K} bf16]")
+        del A, Bm
