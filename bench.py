@@ -165,6 +165,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fsdp", action="store_true", help="HQ-FSDP path even at N=1 (always on for N>1)")
     ap.add_argument("--fsdp-gather", action="store_true", help="HQ-FSDP with NCCL all-gathers instead of peer reads")
+    ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -226,6 +227,20 @@ def main():
     for _ in range(args.warmup):
         step(x, dy)
     torch.cuda.synchronize()
+    run_step = lambda: step(x, dy)  # noqa: E731
+    if args.graph:
+        # the whole step (all kernels, memsets, allocations) as one CUDA graph
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            step(x, dy)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        with torch.cuda.graph(graph):
+            step(x, dy)
+        graph.replay()
+        torch.cuda.synchronize()
+        run_step = graph.replay
 
     # ------------------------------------------------------------ timed region
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -237,7 +252,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))  # evict L2 between steps (outside the events)
             starts[i].record()
-            step(x, dy)
+            run_step()
             ends[i].record()
         torch.cuda.synchronize()
     if world > 1:
