@@ -532,6 +532,11 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
         if (w == 0) tma_prefetch_desc(&tm);
         for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // everything above overlaps the previous kernel's tail (PDL)
+    pdl_wait();
+    pdl_trigger();
+    if (l == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             const int64_t c = c0 + s * G;
             if (c < nchunks) {
@@ -618,8 +623,8 @@ void launch_v3(const InT* in, int64_t n, unsigned* amax, const float* sup, uint8
             int64_t want = ((n + 1023) / 1024 + C::WARPS - 1) / C::WARPS;
             const int64_t cap = (int64_t)num_sms() * per_sm;
             if (want > cap) want = cap;
-            kern<<<(unsigned)(want < 1 ? 1 : want), 32 * C::WARPS, C::SMEM, st>>>(tm, n, cols, norm, amax, sup, codes,
-                                                                              out, err, sout);
+            launch_pdl(kern, dim3((unsigned)(want < 1 ? 1 : want)), dim3(32 * C::WARPS), C::SMEM, st, tm, n, cols, norm,
+                       amax, sup, codes, out, err, sout);
             return;
         }
     }

@@ -179,6 +179,8 @@ __global__ void __launch_bounds__(128, 4)
     const int cg = l & 7, q = 4 * w + (l >> 3);  // 4-column group, row group
     uint8_t* const stg = reinterpret_cast<uint8_t*>(X4) + C3_SMEM;
     uint64_t* const bars = reinterpret_cast<uint64_t*>(stg + (TS > 0 ? TS : 0) * C3_STAGE);
+    pdl_wait();  // launched with PDL: the predecessor's writes are visible past this point
+    pdl_trigger();
     Quant<FMT, SUP_R> qr;
     Quant<FMT, SUP_P> qp;
     if constexpr (MODE == C3_QUANT) {
@@ -580,8 +582,8 @@ void c3_go(const CUtensorMap& tm, const InT* in, int64_t b, int64_t rows_pad, in
     const int64_t tiles = ((cols + C3_COLS - 1) / C3_COLS) * ((rows_pad + C3_ROWS - 1) / C3_ROWS);
     const int64_t cap = (int64_t)num_sms() * per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    kern<<<grid, 32 * C3_WARPS, smem, st>>>(tm, in, b, rows_pad, cols, hadamard_norm(int64_t(1) << LB), ar, ap, sr, sp,
-                                            cr, cp, err, sro, spo);
+    launch_pdl(kern, dim3(grid), dim3(32 * C3_WARPS), smem, st, tm, in, b, rows_pad, cols, hadamard_norm(int64_t(1) << LB),
+               ar, ap, sr, sp, cr, cp, err, sro, spo);
 }
 
 inline bool c3_use_tma() {

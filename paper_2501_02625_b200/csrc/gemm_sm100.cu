@@ -448,6 +448,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // setup above overlaps the previous kernel's tail (PDL); no global
+    // access before this point
+    pdl_wait();
+    pdl_trigger();
 
     if (warp == 0) {
         // ============================ TMA producer (both CTAs of a pair)
@@ -1116,11 +1120,13 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
         cfg.dynamicSmemBytes = gemm_smem<2>();
         cfg.stream = st;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         if (!mp) {
@@ -1129,6 +1135,7 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         }
         const int grid = 2 * (tiles < mp ? tiles : mp);
         cfg.gridDim = dim3(grid, 1, 1);
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
         const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, args);
         if (le != cudaSuccess) return (int)le;
     }

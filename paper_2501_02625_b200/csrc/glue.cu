@@ -5,6 +5,7 @@
 // The reference's toy block uses silu between fc1 and fc2 (model.hpp:77-96,
 // 169-171, 193-195); the Llama MLP gates it with a second projection.
 #include "common.cuh"
+#include "sm100.cuh"
 #include "halo_internal.h"
 
 namespace halo_b200 {
@@ -14,14 +15,28 @@ namespace halo_b200 {
 __global__ void __launch_bounds__(256) k_swiglu_fwd(const __nv_bfloat16* __restrict__ G,
                                                     const __nv_bfloat16* __restrict__ U,
                                                     __nv_bfloat16* __restrict__ H, int64_t n) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
-    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
-        float g[8], u[8], h[8];
+    pdl_wait();
+    pdl_trigger();
+    // two 8-element groups per thread and trip (one grid stride apart): four
+    // 16 B loads in flight before any math
+    const int64_t half = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += 2 * half) {
+        const int64_t i2 = i + half;
+        float g[8], u[8], g2[8], u2[8], h[8];
         load8(G + i, g);
         load8(U + i, u);
+        if (i2 < n) {
+            load8(G + i2, g2);
+            load8(U + i2, u2);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) h[j] = swiglu_fwd1(g[j], u[j]);
         store8(H + i, h);
+        if (i2 < n) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h[j] = swiglu_fwd1(g2[j], u2[j]);
+            store8(H + i2, h);
+        }
     }
 }
 
@@ -31,6 +46,8 @@ __global__ void __launch_bounds__(256) k_swiglu_bwd(const __nv_bfloat16* __restr
                                                     const __nv_bfloat16* __restrict__ U,
                                                     __nv_bfloat16* __restrict__ dG, __nv_bfloat16* __restrict__ dU,
                                                     int64_t n) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
         float dh[8], g[8], u[8], dg[8], du[8];
@@ -48,6 +65,8 @@ __global__ void __launch_bounds__(256) k_swiglu_bwd(const __nv_bfloat16* __restr
 template <typename T>
 __global__ void __launch_bounds__(256) k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
                                              int64_t n) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
         float x[8], y[8];
@@ -94,24 +113,23 @@ static unsigned ew_grid(int64_t n) {
 }
 
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st) {
-    k_swiglu_fwd<<<ew_grid(n), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(G), static_cast<const __nv_bfloat16*>(U),
-                                              static_cast<__nv_bfloat16*>(H), n);
+    launch_pdl(k_swiglu_fwd, dim3(ew_grid(n)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(G),
+               static_cast<const __nv_bfloat16*>(U), static_cast<__nv_bfloat16*>(H), n);
 }
 
 void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void* dU, int64_t n, cudaStream_t st) {
-    k_swiglu_bwd<<<ew_grid(n), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(dH), static_cast<const __nv_bfloat16*>(G),
-        static_cast<const __nv_bfloat16*>(U), static_cast<__nv_bfloat16*>(dG), static_cast<__nv_bfloat16*>(dU), n);
+    launch_pdl(k_swiglu_bwd, dim3(ew_grid(n)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(dH),
+               static_cast<const __nv_bfloat16*>(G), static_cast<const __nv_bfloat16*>(U),
+               static_cast<__nv_bfloat16*>(dG), static_cast<__nv_bfloat16*>(dU), n);
 }
 
 void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st) {
     if (dtype == DT_BF16)
-        k_add<__nv_bfloat16><<<ew_grid(n), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a),
-                                                          static_cast<const __nv_bfloat16*>(b),
-                                                          static_cast<__nv_bfloat16*>(out), n);
+        launch_pdl(k_add<__nv_bfloat16>, dim3(ew_grid(n)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(a),
+                   static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(out), n);
     else
-        k_add<float><<<ew_grid(n), 256, 0, st>>>(static_cast<const float*>(a), static_cast<const float*>(b),
-                                                  static_cast<float*>(out), n);
+        launch_pdl(k_add<float>, dim3(ew_grid(n)), dim3(256), 0, st, static_cast<const float*>(a),
+                   static_cast<const float*>(b), static_cast<float*>(out), n);
 }
 
 void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st) {
