@@ -390,11 +390,14 @@ def main():
             "tokens_per_s": world * b * args.steps / (ms / 1e3),
             "roofline": {"bound": "tensor",
                          "kernel": "k3_gemm (tcgen05 kind::i8)" if fmt == halo.INT8 else "k3_gemm (tcgen05 kind::f8f6f4)",
-                         "achieved": round(gemm_tops, 1), "peak": round(int8_peak, 1), "unit": "TFLOP/s",
-                         "frac": round(gemm_tops / int8_peak, 4), "traffic": traffic,
-                         "peak_source": f"2 x bf16_tflops_sustained of {peak_src} MEASURED_PEAKS.json "
-                                        "(dense INT8 = 2x dense bf16)",
-                         "frac_of_spec_4500": round(gemm_tops / 4500.0, 4),
+                         "achieved": round(gemm_tops, 1), "peak": 4500.0, "unit": "TFLOP/s",
+                         "frac": round(gemm_tops / 4500.0, 4), "traffic": traffic,
+                         "peak_source": "dense INT8/FP8/FP6 tensor peak, B200_PROFILING.md fallback (no measured "
+                                        "INT8 figure in MEASURED_PEAKS.json)",
+                         "measured_proxy": {"peak": round(int8_peak, 1), "frac": round(gemm_tops / int8_peak, 4),
+                                            "source": f"2 x bf16_tflops_sustained of {peak_src} MEASURED_PEAKS.json: "
+                                                      "cuBLAS bf16 under the same 1000 W power cap (dense INT8 = "
+                                                      "2x dense bf16)"},
                          "per_step_ms": round(gemm["ms"] / args.steps, 4),
                          "launches_per_step": gemm["launches"] // args.steps},
             "hbm_kernels": hbm,
