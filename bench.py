@@ -204,16 +204,34 @@ def main():
     dy = (torch.randn(b, HIDDEN, generator=g, device=dev) * 1e-3).to(bf)
     scheme = halo.halo2(fmt, args.block)
     use_fsdp = world > 1 or args.fsdp or args.fsdp_gather
+    peer_error = None
+    mlp = None
     if use_fsdp and not args.fsdp_gather:
-        # HQ-FSDP over peer memory: shards read in place by the GEMMs
+        # HQ-FSDP over peer memory: shards read in place by the GEMMs.  If
+        # CUDA IPC / peer access is unavailable on this node, every rank
+        # agrees to fall back to the NCCL all-gather protocol (reported).
         from paper_2501_02625_b200.fsdp import PeerFsdpHaloMLP
-        mlp = PeerFsdpHaloMLP(wg, wu, wd, scheme)
-    elif use_fsdp:
+        ok = 1
+        try:
+            mlp = PeerFsdpHaloMLP(wg, wu, wd, scheme)
+        except Exception as exc:  # noqa: BLE001
+            peer_error, ok = f"{type(exc).__name__}: {exc}"[:200], 0
+        if world > 1:
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ok = int(flag.item())
+        if not ok:
+            if mlp is not None:
+                mlp.close()
+            mlp = None
+            args.fsdp_gather = True
+            peer_error = peer_error or "a peer rank could not set up peer memory"
+    if use_fsdp and args.fsdp_gather:
         # HQ-FSDP: weights row-sharded over the ranks, INT8 (WH)_Q gathered for
         # the forward, regathered for the backward, dW reduce-scattered
         from paper_2501_02625_b200.fsdp import FsdpHaloMLP
         mlp = FsdpHaloMLP(wg, wu, wd, scheme)
-    else:
+    elif not use_fsdp:
         mlp = HaloMLP(wg, wu, wd, scheme)
     ops_step = mlp.gemm_ops(b)
 
@@ -385,6 +403,7 @@ def main():
                                         f"hq-fsdp{world} (INT8 weight shards read in place over NVLink by the "
                                         f"GEMMs, device-mailbox absmax exchange, bf16 dW reduce-scatter over NCCL)")
                                        if use_fsdp else "single GPU"),
+                       "peer_fallback": peer_error,
                        "l2": "512 MiB buffer written between timed steps (outside the step events); "
                              "per-step working set ~2 GB > 126 MB L2"},
             "tokens_per_s": world * b * args.steps / (ms / 1e3),

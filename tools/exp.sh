@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-for i in 1 2 3; do
-HALO_PDL=0 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_pdl0_$i.log 2>&1
-timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_pdl1_$i.log 2>&1
+: > gpurun_out/peer_stress.log
+for i in 1 2 3 4; do
+timeout 300 python -m pytest tests/test_gpu_peer.py -q -x -k two_processes >> gpurun_out/peer_stress.log 2>&1; echo "rc=$?" >> gpurun_out/peer_stress.log
 done
+timeout 600 python bench.py --no-cpu-baseline --fsdp > gpurun_out/bench_peer.log 2>&1; echo "rc=$?" >> gpurun_out/bench_peer.log
