@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(128, 3)
                          const __nv_bfloat16* __restrict__ U, __nv_bfloat16* __restrict__ dG,
                          __nv_bfloat16* __restrict__ dU, int64_t b, int64_t rows_pad, int64_t cols, float norm,
                          unsigned* am_gr, unsigned* am_gp, unsigned* am_ur, unsigned* am_up, unsigned* err) {
-    extern __shared__ __align__(16) float4 X4[];
+    extern __shared__ __align__(128) float4 X4[];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int cg = l & 7, q = 4 * w + (l >> 3);
     float gr = 0.f, gp = 0.f, ur = 0.f, up = 0.f;

@@ -101,6 +101,10 @@ int k1_version();
 bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
              uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
 
+// K1 / K4 for large blocks (fwht_big.cu): 512 <= B <= 16384, B = 2^k
+bool rows_big(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
+              uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
+
 // third-generation K2 (fwht_cols3.cu): absmax / quantize, B = 2^k <= 256
 bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
              unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
