@@ -50,7 +50,8 @@ LEVELS = {"halo0": 0, "halo1": 1, "halo2": 2}
 
 @pytest.mark.parametrize("scheme", ["halo0", "halo1", "halo2"])
 @pytest.mark.parametrize("b,m,n,block", [(256, 256, 128, 256), (300, 512, 256, 256), (64, 128, 96, 32),
-                                         (128, 256, 256, 0), (96, 64, 48, 16)])
+                                         (128, 256, 256, 0), (96, 64, 48, 16),
+                                         (1000, 1024, 256, 0), (512, 2048, 128, 0)])
 def test_layer_int8_bitexact(H, orc, scheme, b, m, n, block):
     X, W, E = inputs(orc, b, m, n)
     want = orc.linear(LEVELS[scheme], 0, block, X, W, E)
