@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(128) k_cols_lo(const InT* __restrict__ in, int
 template <int LBH, int FMT, int MODE>
 __global__ void __launch_bounds__(128) k_cols_hi(const float* __restrict__ buf, int64_t rows_pad, int64_t cols,
                                                  float norm, unsigned* amax, const float* supplied,
-                                                 uint8_t* __restrict__ codes, unsigned* err, float* scale_out) {
+                                                 uint8_t* __restrict__ codes, unsigned* err, float* scale_out,
+                                                 float* __restrict__ xout, int64_t rows_out) {
     constexpr int R = 1 << LBH;
     constexpr bool FOLD = ((LBH + 8) % 2) == 0;
     pdl_wait();
@@ -181,6 +182,13 @@ __global__ void __launch_bounds__(128) k_cols_hi(const float* __restrict__ buf, 
                     }
                 }
         }
+        if constexpr (MODE == 2) {  // transform only (K4-left): normalised fp32, rows < rows_out kept
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int64_t row = row0 + 256 * (int64_t)i;
+                if (row < rows_out) xout[row * cols + c] = __fmul_rn(v[i], norm);
+            }
+        }
         if constexpr (MODE == 1) {
 #pragma unroll
             for (int i = 0; i < R; ++i) {
@@ -228,20 +236,22 @@ float* cb_scratch(size_t elems) {
 
 template <int LBH, int FMT, int MODE>
 void cb_hi(const float* buf, int64_t rows_pad, int64_t cols, float norm, unsigned* amax, const float* sup,
-           uint8_t* codes, unsigned* err, float* sout, cudaStream_t st) {
+           uint8_t* codes, unsigned* err, float* sout, cudaStream_t st, float* xout = nullptr, int64_t rows_out = 0) {
     auto kern = k_cols_hi<LBH, FMT, MODE>;
     const int64_t tasks = rows_pad / 256 * ((cols + 31) / 32);
     int64_t grid = (tasks + 3) / 4;
     const int64_t cap = (int64_t)num_sms() * 16;
     if (grid > cap) grid = cap;
     launch_pdl(kern, dim3((unsigned)(grid < 1 ? 1 : grid)), dim3(128), 0, st, buf, rows_pad, cols, norm, amax, sup,
-               codes, err, sout);
+               codes, err, sout, xout, rows_out);
 }
 
 template <int LBH>
 void cb_hi_dispatch(int mode, int fmt, const float* buf, int64_t rows_pad, int64_t cols, float norm, unsigned* amax,
-                    const float* sup, uint8_t* codes, unsigned* err, float* sout, cudaStream_t st) {
-    if (mode == 0) cb_hi<LBH, 0, 0>(buf, rows_pad, cols, norm, amax, sup, codes, err, sout, st);
+                    const float* sup, uint8_t* codes, unsigned* err, float* sout, cudaStream_t st, float* xout,
+                    int64_t rows_out) {
+    if (mode == 2) cb_hi<LBH, 0, 2>(buf, rows_pad, cols, norm, amax, sup, codes, err, sout, st, xout, rows_out);
+    else if (mode == 0) cb_hi<LBH, 0, 0>(buf, rows_pad, cols, norm, amax, sup, codes, err, sout, st);
     else if (fmt == FMT_INT8) cb_hi<LBH, FMT_INT8, 1>(buf, rows_pad, cols, norm, amax, sup, codes, err, sout, st);
     else if (fmt == FMT_E3M2) cb_hi<LBH, FMT_E3M2, 1>(buf, rows_pad, cols, norm, amax, sup, codes, err, sout, st);
     else cb_hi<LBH, FMT_E4M3, 1>(buf, rows_pad, cols, norm, amax, sup, codes, err, sout, st);
@@ -249,13 +259,15 @@ void cb_hi_dispatch(int mode, int fmt, const float* buf, int64_t rows_pad, int64
 
 }  // namespace
 
-// K2 modes 0 (absmax) / 1 (quantize) for 512 <= B <= 16384 (B = 2^k,
+// K2 modes 0 (absmax) / 1 (quantize) / 2 (transform, fp32 in -> fp32 out,
+// rows < rows_out: K4-left) for 512 <= B <= 16384 (B = 2^k,
 // rows_pad a multiple of B, cols % 4 == 0).  The plain operand: absmax in
 // mode 0 (from the raw input), codes in mode 1 through run_plain.
 bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
               unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
-              float* sro, float* spo, cudaStream_t st) {
-    if (mode > 1 || B < 512 || B > 16384 || (B & (B - 1)) || rows_pad % B || cols % 4) return false;
+              float* sro, float* spo, cudaStream_t st, float* xout, int64_t rows_out) {
+    if (mode > 2 || B < 512 || B > 16384 || (B & (B - 1)) || rows_pad % B || cols % 4) return false;
+    if (mode == 2 && (in_dtype != DT_F32 || !xout)) return false;
     if ((uintptr_t)in % (in_dtype == DT_BF16 ? 8 : 16)) return false;
     float* buf = cb_scratch((size_t)rows_pad * (size_t)cols);
     if (!buf) return false;
@@ -265,7 +277,7 @@ bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_
         const int64_t tiles = (rows_pad / 256) * ((cols + 31) / 32);
         const int64_t cap = (int64_t)num_sms() * 4;
         const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-        unsigned* plain_amax = (mode == 0 && !sp) ? ap : nullptr;
+        unsigned* plain_amax = (mode == 0 && !sp && ap) ? ap : nullptr;
         if (in_dtype == DT_BF16)
             launch_pdl(k_cols_lo<__nv_bfloat16>, dim3(grid), dim3(128), 0, st, static_cast<const __nv_bfloat16*>(in), b,
                        rows_pad, cols, buf, plain_amax, err);
@@ -275,12 +287,12 @@ bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_
     }
     const float norm = hadamard_norm(B);
     switch (lb) {
-    case 9: cb_hi_dispatch<1>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st); break;
-    case 10: cb_hi_dispatch<2>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st); break;
-    case 11: cb_hi_dispatch<3>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st); break;
-    case 12: cb_hi_dispatch<4>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st); break;
-    case 13: cb_hi_dispatch<5>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st); break;
-    default: cb_hi_dispatch<6>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st); break;
+    case 9: cb_hi_dispatch<1>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
+    case 10: cb_hi_dispatch<2>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
+    case 11: cb_hi_dispatch<3>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
+    case 12: cb_hi_dispatch<4>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
+    case 13: cb_hi_dispatch<5>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
+    default: cb_hi_dispatch<6>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
     }
     if (mode == 1 && cp) run_plain(in, in_dtype, b * cols, 1, fmt, ap, sp, cp, err, spo, st);
     return true;

@@ -108,7 +108,7 @@ bool rows_big(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_
 // K2 for large blocks along the token axis (fwht_cols_big.cu): 512 <= B <= 16384
 bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
               unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
-              float* sro, float* spo, cudaStream_t st);
+              float* sro, float* spo, cudaStream_t st, float* xout = nullptr, int64_t rows_out = 0);
 
 // third-generation K2 (fwht_cols3.cu): absmax / quantize, B = 2^k <= 256
 bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
