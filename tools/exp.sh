@@ -1,3 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+for blk in 512 2048; do
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --block $blk > gpurun_out/bench_blk$blk.log 2>&1
+done
