@@ -180,10 +180,18 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # HALO_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 with gloo, to
+    # exercise the N>1 code path on a one-GPU box; numbers are not valid then
+    one_gpu = os.environ.get("HALO_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2501_02625_b200 import halo
     from paper_2501_02625_b200.mlp import HaloMLP, profile_enable, profile_read
