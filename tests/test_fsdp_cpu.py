@@ -128,3 +128,15 @@ def test_hqfsdp_protocol_gloo(orc, world):
         assert np.array_equal(got, mean)
     else:
         assert np.allclose(got, mean, rtol=1e-6, atol=1e-7)
+
+
+def test_fp6_payload_ratio():
+    """hqfsdp.hpp:36-49 / test_hqfsdp.cpp:245-257: FP6 packs 4 codes into 3
+    bytes -- 0.375 of BF16 (INT8 / FP8: 0.5)."""
+    from paper_2501_02625_b200 import fsdp
+    n = 256 * 64
+    assert fsdp.code_payload_bytes(fsdp.FP6_E3M2, n) == 12288
+    assert fsdp.code_payload_bytes(fsdp.FP6_E3M2, n) / (2 * n) == 0.375
+    assert fsdp.code_payload_bytes(fsdp.INT8, n) / (2 * n) == 0.5
+    assert fsdp.code_payload_bytes(fsdp.FP6_E3M2, 5) == 6  # (5 + 3) // 4 * 3
+

@@ -69,9 +69,3 @@ def test_fp6_golden_values(H):
     codes, scale = H.rotate_quantize(a, fmt=2, rotate=False)
     assert scale.item() == np.float32(30.0 / 28.0)
 
-
-def test_fp6_hqfsdp_payload():
-    """hqfsdp.hpp:36-49: FP6 packs 4 codes into 3 bytes: 0.375 of BF16."""
-    from paper_2501_02625_b200 import fsdp
-    assert fsdp.code_payload_bytes(fsdp.FP6_E3M2, 256 * 64) == 12288
-    assert fsdp.code_payload_bytes(fsdp.FP6_E3M2, 256 * 64) / (2 * 256 * 64) == 0.375
