@@ -1,4 +1,9 @@
 #!/bin/bash
 mkdir -p gpurun_out
-HALO_BENCH_ONE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --tokens 2048 > gpurun_out/bench_n2.log 2>&1; echo "rc=$?" >> gpurun_out/bench_n2.log
-HALO_BENCH_ONE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --steps 1 --warmup 3 > gpurun_out/bench_n2_ref.log 2>&1; echo "rc=$?" >> gpurun_out/bench_n2_ref.log
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+HALO_GEMM_SPLITK=0 timeout 300 python tools/bench_kernels.py gemm > gpurun_out/kern_sk0.log 2>&1
+timeout 300 python tools/bench_kernels.py gemm > gpurun_out/kern_sk1.log 2>&1
+for i in 1 2; do
+HALO_GEMM_SPLITK=0 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_sk0_$i.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_sk1_$i.log 2>&1
+done
