@@ -564,7 +564,8 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
         if (l == 0) {
             const int64_t cn = c + C::STAGES * G;
             if (cn < nchunks) {
-                fence_proxy_async_smem();
+                // no proxy fence: the stage's generic-proxy reads completed
+                // (their values fed phase 1) before the async-proxy refill
                 mbar_expect_tx(&bars[s], C::STAGE_BYTES);
                 tma_load_2d(stages + s * C::STAGE_BYTES, &tm, &bars[s], 0, (int)(cn * C::CHUNK_ROWS));
             }

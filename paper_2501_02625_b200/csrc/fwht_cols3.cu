@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(128, 4)
         const int64_t col = c0 + 4 * cg;
         const bool cok = !EDGE || col < cols;
         const int64_t row1 = r0 + 16 * q;
+        (void)cok;  // unused by some instantiations
+        (void)row1;
         // ---------------- phase 1: rows 16q + m
         float2 v[16][2];
         if constexpr (TS > 0) {
