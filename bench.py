@@ -318,6 +318,36 @@ def main():
                       "launches_per_step": v["launches"] // args.steps}
     share = {k: round(v["ms"] / max(1e-9, sum(u["ms"] for u in prof.values())), 3) for k, v in prof.items()}
 
+    # K1 per pass on the step's largest K1 operand (h: tokens x 14336, bf16):
+    # phase A alone (absmax: 2 B/elem) and phase B = (A + B) - A (quantize:
+    # 2 B in + 1 B out per elem), each against the measured HBM copy peak
+    if rank == 0:
+        hh = torch.randn(b, INTER, device=dev).to(bf)
+        nel = hh.numel()
+
+        def _t(fn, reps=5):
+            fn()
+            ts = []
+            for _ in range(reps):
+                flush.fill_(0.0)
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record()
+                fn()
+                b_.record()
+                torch.cuda.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            return statistics.median(ts)
+
+        t_a = _t(lambda: halo.rotate_absmax(hh, args.block))
+        t_ab = _t(lambda: halo.rotate_quantize(hh, args.block, fmt=fmt))
+        if "k1_rows_fwht_quant" in hbm:
+            ga, gb = 2 * nel / t_a / 1e6, 3 * nel / max(t_ab - t_a, 1e-6) / 1e6
+            hbm["k1_rows_fwht_quant"]["per_pass"] = {
+                "tensor": f"h {b}x{INTER} bf16", "phase_a_gbs": round(ga, 1), "phase_a_frac": round(ga / peaks["hbm_gbs"], 3),
+                "phase_b_gbs": round(gb, 1), "phase_b_frac": round(gb / peaks["hbm_gbs"], 3),
+                "note": "two passes per per-tensor scale (absmax before any code): the op's own frac counts the input once"}
+        del hh
+
     # -------------------------------------------------------------- end to end
     e2e = None
     if not args.no_e2e:

@@ -1,4 +1,3 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python tools/bench_kernels.py k1 > gpurun_out/kern_nofence.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_pp.log 2>&1; echo "rc=$?" >> gpurun_out/bench_pp.log
