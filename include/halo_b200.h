@@ -254,6 +254,13 @@ HALO_API halo_status halo_device_copy(void* dst, const void* src, int64_t bytes,
 HALO_API halo_status halo_swiglu_forward(const void* g, const void* u, void* h, int64_t n, halo_stream_t stream);
 HALO_API halo_status halo_swiglu_backward(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n,
                                           halo_stream_t stream);
+/* halo_swiglu_forward over [rows x cols] fused with phase A (the absmax pass)
+ * of the down projection's X quantization (halo_linear.hpp:292-294; rotated
+ * X with a 256 Hadamard block): the following halo_linear_forward(down, h,
+ * ..., dctx) with this exact h buffer and batch reuses the absmax word.
+ * Other configurations: identical to halo_swiglu_forward. */
+HALO_API halo_status halo_swiglu_forward_absmax(const halo_linear* down, halo_ctx* dctx, const void* g, const void* u,
+                                                void* h, int64_t rows, int64_t cols, halo_stream_t stream);
 /* halo_swiglu_backward over [b x cols] fused with phase A (the absmax
  * pass) of the error-path quantization of both input projections
  * (halo_linear.hpp:393-399 and :371 for `gate` and `up`, HALO-2 family:

@@ -134,6 +134,8 @@ def lib():
     L.halo_swiglu_forward.argtypes = [_vp, _vp, _vp, _i64, _vp]
     L.halo_swiglu_backward.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _vp]
     L.halo_swiglu_backward_absmax.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]
+    L.halo_swiglu_forward_absmax.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]
+    L.halo_swiglu_forward_absmax.restype = C.c_int
     L.halo_add.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp]
     L.halo_linear_set_qweight_sharded.argtypes = [_vp, C.POINTER(_vp), _i32, _vp]
     L.halo_peer_alloc.argtypes = [_i64, C.POINTER(_vp)]
@@ -197,5 +199,5 @@ EXPORTS = (
     "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
     "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
     "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
-    "halo_reduce_scatter_shard", "halo_rotate_quantize_amax",
+    "halo_reduce_scatter_shard", "halo_rotate_quantize_amax", "halo_swiglu_forward_absmax",
 )

@@ -576,6 +576,98 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
     core.reduce(absmax, err);
 }
 
+// ------------------------------------------ SwiGLU forward + K1 phase A
+// h = silu(g) * u (swiglu_fwd1, the glue kernel's exact formula), rounded to
+// bf16 and written out for K1's quantize pass, and in the same pass the
+// absmax of (h H) for the down projection's per-tensor scale (phase A with
+// B = 256): one read of g and u replaces the glue kernel's and phase A's.
+__global__ void __launch_bounds__(128) k_swiglu_absmax(const __grid_constant__ CUtensorMap tmg,
+                                                       const __grid_constant__ CUtensorMap tmu, int64_t n, float norm,
+                                                       __nv_bfloat16* __restrict__ h, unsigned* absmax, unsigned* err) {
+    using C = V4Cfg<__nv_bfloat16>;
+    constexpr int SB = 2 * C::STAGE_BYTES;  // g chunk + u chunk
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int k = l >> 3, p = l & 7;
+    uint8_t* stages = smem + w * C::STAGES * SB;
+    float4* xch = reinterpret_cast<float4*>(smem + C::WARPS * C::STAGES * SB + w * C::XCH_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::WARPS * (C::STAGES * SB + C::XCH_BYTES)) + w * C::STAGES;
+    const int64_t nchunks = n >> 10;
+    const int64_t G = (int64_t)gridDim.x * C::WARPS;
+    const int64_t c0 = (int64_t)blockIdx.x * C::WARPS + w;
+    if (l == 0) {
+        if (w == 0) {
+            tma_prefetch_desc(&tmg);
+            tma_prefetch_desc(&tmu);
+        }
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_wait();
+    pdl_trigger();
+    auto issue = [&](int s, int64_t c) {
+        mbar_expect_tx(&bars[s], SB);
+        tma_load_2d(stages + s * SB, &tmg, &bars[s], 0, (int)(c * C::CHUNK_ROWS));
+        tma_load_2d(stages + s * SB + C::STAGE_BYTES, &tmu, &bars[s], 0, (int)(c * C::CHUNK_ROWS));
+    };
+    if (l == 0)
+        for (int s = 0; s < C::STAGES; ++s)
+            if (c0 + s * G < nchunks) issue(s, c0 + s * G);
+    __syncwarp();
+    RowsCore<8, 0, V3_ABSMAX, false, float> core;
+    core.init(absmax, nullptr, norm, err, nullptr);
+    int i = 0;
+    for (int64_t c = c0; c < nchunks; c += G, ++i) {
+        const int s = i % C::STAGES;
+        mbar_wait(&bars[s], (uint32_t)(i / C::STAGES) & 1u);
+        float2 vg[16], vu[16];
+        v4_read<__nv_bfloat16>(stages + s * SB, k, p, vg);
+        v4_read<__nv_bfloat16>(stages + s * SB + C::STAGE_BYTES, k, p, vu);
+        // h in bf16 (what the unfused path quantizes), stored and transformed
+        uint32_t hw[16];
+        float2 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            hw[j] = pack_bf16x2(swiglu_fwd1(vg[j].x, vu[j].x), swiglu_fwd1(vg[j].y, vu[j].y));
+            v[j] = make_float2(__uint_as_float(hw[j] << 16), __uint_as_float(hw[j] & 0xFFFF0000u));
+        }
+        // every loaded value is consumed above: the stage's reads are done
+        __syncwarp();
+        if (l == 0 && c + C::STAGES * G < nchunks) issue(s, c + C::STAGES * G);
+        uint4* dst = reinterpret_cast<uint4*>(h + (c << 10) + k * 256 + p * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = make_uint4(hw[4 * j], hw[4 * j + 1], hw[4 * j + 2], hw[4 * j + 3]);
+        core.phase1(v);
+        core.finish(v, c << 10, n, k, p, xch, nullptr, (float*)nullptr);
+    }
+    core.reduce(absmax, err);
+}
+
+// h = swiglu(g, u) (bf16, n elements) and the rotated absmax of h (B = 256)
+bool swiglu_absmax(const void* g, const void* u, void* h, int64_t n, int64_t cols, unsigned* amax, unsigned* err,
+                   cudaStream_t st) {
+    using C = V4Cfg<__nv_bfloat16>;
+    if (n % 1024 || cols % 256 || (uintptr_t)g % 16 || (uintptr_t)u % 16 || (uintptr_t)h % 16) return false;
+    CUtensorMap tg, tu;
+    if (!encode_2d_sw128(&tg, 1, g, C::ROW_ELEMS, n / C::ROW_ELEMS, C::CHUNK_ROWS) ||
+        !encode_2d_sw128(&tu, 1, u, C::ROW_ELEMS, n / C::ROW_ELEMS, C::CHUNK_ROWS))
+        return false;
+    const size_t smem = 1024 + (size_t)C::WARPS * (C::STAGES * 2 * C::STAGE_BYTES + C::XCH_BYTES) + C::WARPS * C::STAGES * 8;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(k_swiglu_absmax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_swiglu_absmax, 32 * C::WARPS, smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int64_t want = (n / 1024 + C::WARPS - 1) / C::WARPS;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    if (want > cap) want = cap;
+    launch_pdl(k_swiglu_absmax, dim3((unsigned)(want < 1 ? 1 : want)), dim3(32 * C::WARPS), smem, st, tg, tu, n,
+               hadamard_norm(256), static_cast<__nv_bfloat16*>(h), amax, err);
+    return true;
+}
+
 // ============================================================ launcher
 
 namespace {

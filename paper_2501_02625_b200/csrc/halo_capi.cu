@@ -174,6 +174,10 @@ struct halo_ctx {
     const void* e_amax_src = nullptr;
     int64_t e_amax_b = 0;
     bool wq_sharded = false;  // forward used the layer's sharded (WH)_Q
+    // halo_swiglu_forward_absmax: the absmax word of (X H) (SX) was produced
+    // with this X buffer (h) by the fused pass
+    const void* x_amax_src = nullptr;
+    int64_t x_amax_b = 0;
     const uint8_t* xq_codes() const { return xq_borrow ? xq_borrow : xq.as<uint8_t>(); }
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
@@ -335,9 +339,10 @@ extern "C" halo_status halo_scheme_from_string(const char* id, int32_t format, i
 
 static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows, int64_t cols, int64_t B,
                                         bool rotate, int32_t fmt, const float* supplied, uint8_t* codes,
-                                        unsigned* amax_word, float* scale_out, unsigned* err, cudaStream_t st) {
+                                        unsigned* amax_word, float* scale_out, unsigned* err, cudaStream_t st,
+                                        bool have_amax = false) {
     const double n = (double)rows * (double)cols;
-    if (!supplied) {
+    if (!supplied && !have_amax) {
         cudaMemsetAsync(amax_word, 0, sizeof(unsigned), st);
         ProfScope ps(PC_K1, 0.0, st);  // phase A: its bytes are booked on phase B
         if (rotate) run_rows(a, dt, rows, cols, B, 0, fmt, amax_word, nullptr, nullptr, nullptr, 0, err, nullptr, st);
@@ -831,8 +836,11 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     }
     c->xq_scale = &d->scale[SX];
     // ctx.xq = quantize(XH)  (:292-294)
+    // phase A already done by halo_swiglu_forward_absmax for this exact X
+    const bool have_amax = c->x_amax_src == x && c->x_amax_b == b && x_dtype == HALO_DTYPE_BF16 && rot && B == 256;
+    c->x_amax_src = nullptr;
     halo_status r = rotate_quantize_impl(x, x_dtype, b, l->m, B, rot, s.format_x, nullptr, c->xq.as<uint8_t>(),
-                                         &d->amax[SX], &d->scale[SX], &d->err, st);
+                                         &d->amax[SX], &d->scale[SX], &d->err, st, have_amax);
     if (r != HALO_OK) return r;
     ++l->cx;
     // ctx.wq = quantize(WH)  (:295-297), or the gathered / frozen / sharded codes
@@ -1188,6 +1196,44 @@ extern "C" halo_status halo_swiglu_backward(const void* dh, const void* g, const
     ProfScope ps(PC_GLUE, (double)n * 10, st);
     run_swiglu_bwd(dh, g, u, dg, du, n, st);
     return cuda_check("swiglu_backward");
+}
+
+// SwiGLU forward fused with phase A of the down projection's X quantization
+// (rotated X, Hadamard block 256, bf16): h is written as by
+// halo_swiglu_forward and the absmax word of (h H) lands in `dctx`, so the
+// following halo_linear_forward(down, h, ..., dctx) skips its absmax pass.
+// Other configurations: identical to halo_swiglu_forward.
+extern "C" halo_status halo_swiglu_forward_absmax(const halo_linear* down, halo_ctx* dctx, const void* g,
+                                                  const void* u, void* h, int64_t rows, int64_t cols,
+                                                  halo_stream_t stream) {
+    if (!down || !dctx || !g || !u || !h || rows <= 0 || cols <= 0)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "swiglu_forward_absmax: bad argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    dctx->x_amax_src = nullptr;
+    int64_t B = 0;
+    const bool fuse = down->s.F.middle && down->s.granularity == HALO_GRAN_TENSOR && down->m == cols &&
+                      resolve_block(cols, down->s.had_block, &B, "swiglu forward") == HALO_OK && B == 256 &&
+                      (rows * cols) % 1024 == 0;
+    if (fuse) {
+        if (dctx->dev.ensure(sizeof(DevScalars)) != HALO_OK) return HALO_ERR_CUDA;
+        DevScalars* d = dctx->d();
+        cudaMemsetAsync(&d->amax[SX], 0, sizeof(unsigned), st);
+        bool ok;
+        {
+            ProfScope ps(PC_GLUE, (double)rows * cols * 6.0, st);
+            ok = swiglu_absmax(g, u, h, rows * cols, cols, &d->amax[SX], &d->err, st);
+        }
+        if (ok) {
+            dctx->x_amax_src = h;
+            dctx->x_amax_b = rows;
+            return cuda_check("swiglu_forward_absmax");
+        }
+    }
+    {
+        ProfScope ps(PC_GLUE, (double)rows * cols * 6.0, st);
+        run_swiglu_fwd(g, u, h, rows * cols, st);
+    }
+    return cuda_check("swiglu_forward");
 }
 
 // SwiGLU backward fused with K2's phase A of both input projections (HALO-2

@@ -129,6 +129,11 @@ bool cols_swiglu_absmax(const void* dh, const void* g, const void* u, void* dg, 
 // halo_last_error() text (halo_capi.cu)
 void set_last_error(const char* msg);
 
+// SwiGLU forward fused with K1 phase A of the down projection (fwht3.cu):
+// h = swiglu(g, u) in bf16 plus the absmax of h's 256-blockwise rotation
+bool swiglu_absmax(const void* g, const void* u, void* h, int64_t n, int64_t cols, unsigned* amax, unsigned* err,
+                   cudaStream_t st);
+
 // elementwise glue (glue.cu)
 void run_swiglu_fwd(const void* G, const void* U, void* H, int64_t n, cudaStream_t st);
 void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void* dU, int64_t n, cudaStream_t st);

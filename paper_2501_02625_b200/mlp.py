@@ -34,13 +34,21 @@ class HaloMLP:
         # SwiGLU backward fused with the absmax pass of the gate/up error
         # quantization (halo_swiglu_backward_absmax); False = separate kernels
         self.fuse_glue = os.environ.get("HALO_MLP_FUSE_GLUE", "0") == "1"
+        # SwiGLU forward fused with the down projection's absmax pass
+        # (halo_swiglu_forward_absmax, bit-exact; off: measured slower, see DESIGN)
+        self.fuse_fwd = os.environ.get("HALO_MLP_FUSE_FWD", "0") == "1"
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         g = self.gate.forward(x, self.ctx[0])
         # up_proj sees the same X under the same quantizer: reuse gate's (XH)_Q
         u = self.up.forward_shared(self.ctx[0], self.ctx[1]) if self.share_x else self.up.forward(x, self.ctx[1])
         h = torch.empty_like(g)
-        check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
+        if self.fuse_fwd:
+            # SwiGLU + the down projection's absmax pass in one read of g, u
+            check(lib().halo_swiglu_forward_absmax(self.down._h, self.ctx[2]._h, halo._ptr(g), halo._ptr(u),
+                                                   halo._ptr(h), g.shape[0], g.shape[1], halo._stream()))
+        else:
+            check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
         self._act = (g, u)
         return self.down.forward(h, self.ctx[2])
 

@@ -123,3 +123,29 @@ def test_mlp_stale_absmax_not_reused(M):
     assert torch.equal(dx1, dx2)
     assert torch.equal(a.e_x, b.e_x)
     assert torch.equal(a.grad_w, b.grad_w)
+
+
+@pytest.mark.parametrize("fmt", [0, 1, 2])
+def test_mlp_fused_forward_glue_bitexact(M, fmt):
+    """SwiGLU forward + the down projection's absmax pass in one kernel ==
+    glue kernel + the layer's own absmax pass (same h bits, same scale)."""
+    halo, mlp = M
+    wg, wu, wd, g = _weights(1024, 512, seed=11)
+    x = torch.randn(768, 512, generator=g, device="cuda").to(torch.bfloat16)
+    x[:, 3] *= 40
+    dy = (torch.randn(768, 512, generator=g, device="cuda") * 1e-3).to(torch.bfloat16)
+    outs = []
+    for fuse in (False, True):
+        m = mlp.HaloMLP(wg, wu, wd, halo.halo2(fmt, 256))
+        m.fuse_fwd = fuse
+        y = m.forward(x)
+        dx, grads = m.backward(dy)
+        torch.cuda.synchronize()
+        xq, sx, _, _ = m.ctx[2].saved(m.down)
+        outs.append((y.clone(), dx.clone(), [t.clone() for t in grads], xq.clone(), sx.clone()))
+    a, b = outs
+    assert torch.equal(a[3], b[3]) and torch.equal(a[4], b[4])
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    for u, v in zip(a[2], b[2]):
+        assert torch.equal(u, v)
+
