@@ -379,6 +379,10 @@ void run_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t 
     // direct loads), then fwht2.cu (8 <= B <= 256); this file keeps the
     // generic paths for the remaining block sizes.  HALO_K1_VERSION=2 / 3
     // pins an older kernel (A/B measurements).
+    if (base_dim_of(B)) {  // 12·2^k / 20·2^k blocks: the only path for them
+        rows_base(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st);
+        return;
+    }
     const int ver = k1_version();
     const bool aligned = ((uintptr_t)in % 32 == 0) && ((uintptr_t)codes % 32 == 0) && ((uintptr_t)out % 16 == 0);
     if (ver >= 3 && aligned &&
@@ -403,6 +407,11 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
               unsigned* amax_rot, unsigned* amax_plain, const float* sup_rot, const float* sup_plain,
               uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
               float* scale_rot_out, float* scale_plain_out, cudaStream_t st) {
+    if (base_dim_of(B)) {
+        cols_base(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
+                  codes_plain, err, scale_rot_out, scale_plain_out, st, out, rows_out);
+        return;
+    }
     if (mode != MODE_XFORM && k1_version() >= 3 &&
         cols_v3(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
                 codes_plain, err, scale_rot_out, scale_plain_out, st))

@@ -49,10 +49,11 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 halo_status resolve_block(int64_t d, int64_t had_block, int64_t* B, const char* what) {
     if (had_block < 0) return fail(HALO_ERR_INVALID_ARGUMENT, std::string(what) + ": negative Hadamard block");
     const int64_t blk = had_block ? had_block : d;
-    if (!is_pow2(blk))
+    // 2^k, or 2^k * 12 / 2^k * 20 (the Paley bases, fwht_base.cu) up to 20480
+    if (!is_pow2(blk) && !(base_dim_of(blk) && blk <= 20480))
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     std::string(what) + ": Hadamard block " + std::to_string(blk) +
-                        " is not a power of two (hadamard.hpp:69-98 bases 12/20 are not on the device path)");
+                        " is not 2^k, 12*2^k or 20*2^k (<= 20480) (hadamard.hpp:69-98)");
     if (d % blk != 0)
         return fail(HALO_ERR_INVALID_ARGUMENT, std::string(what) + ": Hadamard block " + std::to_string(blk) +
                                                    " does not divide dimension " + std::to_string(d));
@@ -443,7 +444,9 @@ extern "C" halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_
 static halo_status left_quant_impl(const void* e, int32_t dt, int64_t b, int64_t n, int64_t B, int64_t b_pad,
                                    int32_t fmt, uint8_t* codes_rot, uint8_t* codes_plain, unsigned* amax_r,
                                    unsigned* amax_p, float* s_r, float* s_p, unsigned* err, cudaStream_t st,
-                                   bool have_amax = false) {
+                                   bool have_amax = false, bool transpose_base = true) {
+    // transform_left_h (H E, halo_linear.hpp:399) or, for PEFT, transform_left (:449)
+    BaseScope orient(transpose_base);
     if (!have_amax) {
         cudaMemsetAsync(amax_r, 0, sizeof(unsigned), st);
         cudaMemsetAsync(amax_p, 0, sizeof(unsigned), st);
@@ -580,7 +583,8 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
                     "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
     if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: only tensor and row granularity are on the device path");
-    if (s.granularity == HALO_GRAN_ROW && (m % 256 || (s.had_block ? s.had_block : m) > 256))
+    if (s.granularity == HALO_GRAN_ROW && (m % 256 || (s.had_block ? s.had_block : m) > 256 ||
+                                           !is_pow2(s.had_block ? s.had_block : m)))
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     "halo layer: row granularity needs in_features % 256 == 0 and a Hadamard block <= 256");
     if (!valid_format(s.format_x) || s.format_x != s.format_w || s.format_x != s.format_e)
@@ -941,6 +945,7 @@ static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows,
                          cudaStream_t st) {
     // B == 1 is the identity transform with norm 1: an exact copy/convert
     ProfScope ps(PC_K4, (double)rows * cols * (4 + dt_bytes(dtype)), st);
+    BaseScope ht(true);  // transform_right_ht (H^T; = H for power-of-two blocks)
     run_rows(P, HALO_DTYPE_F32, rows, cols, rotate ? B : 1, 2, 0, nullptr, nullptr, nullptr, out, dtype, nullptr,
              nullptr, st);
 }
@@ -1003,7 +1008,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         c->e_amax_src = nullptr;
         halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->ehq.as<uint8_t>(),
                                         plain ? c->eq.as<uint8_t>() : nullptr, &d->amax[SEH], &d->amax[SE],
-                                        &d->scale[SEH], &d->scale[SE], &d->err, st, have_amax);
+                                        &d->scale[SEH], &d->scale[SE], &d->err, st, have_amax, !s.peft);
         if (r != HALO_OK) return r;
         l->ce += plain ? 2 : 1;
         float* P = c->scratch.as<float>();
@@ -1023,6 +1028,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
             // prod = transform_left(prod); take_rows(b)  (:405-409), in place
             ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
+            BaseScope orient(s.peft);  // transform_left (:406), PEFT transform_left_h (:451)
             run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                      P, b, nullptr, nullptr, nullptr, st);
         }

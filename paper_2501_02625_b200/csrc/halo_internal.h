@@ -110,6 +110,21 @@ bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_
               unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
               float* sro, float* spo, cudaStream_t st, float* xout = nullptr, int64_t rows_out = 0);
 
+// Hadamard blocks 12·2^k / 20·2^k (fwht_base.cu): the reference's Paley
+// bases.  Orientation (H or H^T, transpose_base of hadamard.hpp:136) from
+// the enclosing BaseScope; power-of-two blocks ignore it (H = H^T).
+struct BaseScope {
+    explicit BaseScope(bool transpose_base);
+    ~BaseScope();
+};
+int base_dim_of(int64_t B);  // 12, 20 or 0
+bool rows_base(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax,
+               const float* sup, uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout,
+               cudaStream_t st);
+bool cols_base(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
+               unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
+               float* sro, float* spo, cudaStream_t st, float* xout, int64_t rows_out);
+
 // third-generation K2 (fwht_cols3.cu): absmax / quantize, B = 2^k <= 256
 bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
              unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,

@@ -33,8 +33,8 @@ static int host_mode() {
     }
     expect(threw, "halo3 rejected with std::invalid_argument");
     threw = false;
-    try {  // 48 = 2^4 * 3 is not a power-of-two Hadamard dim (hadamard.hpp:96-98)
-        HaloLinearLayer l(nullptr, 16, 48, halo1());
+    try {  // 112 = 7 * 16 is not 2^k, 12*2^k or 20*2^k (hadamard.hpp:69-98)
+        HaloLinearLayer l(nullptr, 16, 112, halo1());
     } catch (const std::invalid_argument&) {
         threw = true;
     }

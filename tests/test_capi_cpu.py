@@ -70,8 +70,9 @@ def test_layer_validation_without_gpu(L):
     assert create(halo.halo2(halo.INT8, 256), 14336, 4096) == 0
     assert create(halo.halo2(halo.INT8, 256), 4096, 14336) == 0       # blocked: 256 | 14336
     assert create(halo.halo2(), 4096, 14336) == L.HALO_ERR_INVALID_ARGUMENT  # full-dim 14336 (hadamard.hpp:96-98)
-    assert create(halo.halo1(), 16, 48) == L.HALO_ERR_INVALID_ARGUMENT   # 48 = 2^4*3
-    assert create(halo.halo0(), 16, 48) == 0                            # no rotation needed
+    assert create(halo.halo1(), 16, 48) == 0                            # 48 = 12*4: Paley base 12
+    assert create(halo.halo1(), 16, 112) == L.HALO_ERR_INVALID_ARGUMENT  # 112 = 7*16: unsupported
+    assert create(halo.halo0(), 16, 112) == 0                           # no rotation needed
     s = halo.halo2()
     s.quantize_f = 0                                                     # exact path: no fallback
     assert create(s, 128, 256) == L.HALO_ERR_INVALID_ARGUMENT

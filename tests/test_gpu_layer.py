@@ -163,7 +163,7 @@ def test_nonfinite_input_raises(H, orc):
 
 def test_scheme_validation(H):
     # shape and scheme validation (test_halo_linear.cpp:386-409)
-    w = torch.zeros((16, 48), device="cuda")  # 48 = 2^4*3: not a power-of-two Hadamard dim
+    w = torch.zeros((16, 112), device="cuda")  # 112 = 7*16: not 2^k, 12*2^k or 20*2^k
     with pytest.raises(ValueError):
         H.HaloLinearLayer(w, H.halo1())
     H.HaloLinearLayer(w, H.halo0())
