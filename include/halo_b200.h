@@ -14,9 +14,10 @@
  *    storage); the caller owns them.  Nothing here allocates host copies.
  *  - Every call is stream-ordered and asynchronous; no host synchronisation
  *    happens on the hot path.  Scales live in device memory (float*).
- *  - had_block: power-of-two Hadamard block B; the transform is I (x) H_B.
- *    0 means "the full dimension", i.e. the reference's transform verbatim
- *    (hadamard.hpp:95-129; only power-of-two dimensions are built here).
+ *  - had_block: Hadamard block B (2^k, or 12*2^k / 20*2^k <= 20480 with the
+ *    reference's Paley bases); the transform is I (x) H_B.  0 means "the
+ *    full dimension", i.e. the reference's transform verbatim
+ *    (hadamard.hpp:62-129).
  *  - Errors are reported through halo_status; halo_last_error() returns a
  *    thread-local message.  Non-finite inputs are detected on the device and
  *    surface as HALO_ERR_NUMERIC from halo_ctx_check().
