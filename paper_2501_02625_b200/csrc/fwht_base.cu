@@ -180,21 +180,6 @@ void transpose(const void* in, int64_t rows, int64_t valid, int64_t cols, void* 
                static_cast<T*>(out));
 }
 
-void* bs_scratch(int slot, size_t bytes) {
-    static std::mutex mu;
-    static void* p[2] = {nullptr, nullptr};
-    static size_t cap[2] = {0, 0};
-    std::lock_guard<std::mutex> lk(mu);
-    if (bytes > cap[slot]) {
-        if (p[slot]) cudaFree(p[slot]);
-        p[slot] = nullptr;
-        cap[slot] = 0;
-        if (cudaMalloc(&p[slot], bytes) != cudaSuccess) return nullptr;
-        cap[slot] = bytes;
-    }
-    return p[slot];
-}
-
 thread_local int t_transpose_base = 0;
 
 template <typename InT, typename OutT>
@@ -270,9 +255,21 @@ bool cols_base(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64
     if (mode == 2 && (in_dtype != DT_F32 || !xout)) return false;
     const size_t esz = in_dtype == DT_BF16 ? 2 : 4;
     const int64_t n = rows_pad * cols;
-    void* t_in = bs_scratch(0, (size_t)n * esz);
-    void* t_out = bs_scratch(1, (size_t)n * (mode == 2 ? 4 : 1));
-    if (!t_in || !t_out) return false;
+    // stream-ordered scratch (transposed copies), freed after use
+    void *t_in = nullptr, *t_out = nullptr;
+    if (cudaMallocAsync(&t_in, (size_t)n * (mode == 2 ? 4 : esz), st) != cudaSuccess) return false;
+    if (cudaMallocAsync(&t_out, (size_t)n * (mode == 2 ? 4 : 1), st) != cudaSuccess) {
+        cudaFreeAsync(t_in, st);
+        return false;
+    }
+    struct Release {
+        void *a, *b;
+        cudaStream_t s;
+        ~Release() {
+            cudaFreeAsync(a, s);
+            cudaFreeAsync(b, s);
+        }
+    } release{t_in, t_out, st};
     if (esz == 2) transpose<__nv_bfloat16>(in, rows_pad, b, cols, t_in, st);
     else transpose<float>(in, rows_pad, b, cols, t_in, st);
     if (mode == 2) {

@@ -23,7 +23,6 @@
 #include "halo_internal.h"
 #include "sm100.cuh"
 
-#include <mutex>
 
 namespace halo_b200 {
 
@@ -218,22 +217,6 @@ __global__ void __launch_bounds__(128) k_cols_hi(const float* __restrict__ buf, 
     }
 }
 
-// grow-only fp32 scratch for the partial transform (one per process)
-float* cb_scratch(size_t elems) {
-    static std::mutex mu;
-    static float* p = nullptr;
-    static size_t cap = 0;
-    std::lock_guard<std::mutex> lk(mu);
-    if (elems > cap) {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        if (cudaMalloc(&p, elems * sizeof(float)) != cudaSuccess) return nullptr;
-        cap = elems;
-    }
-    return p;
-}
-
 template <int LBH, int FMT, int MODE>
 void cb_hi(const float* buf, int64_t rows_pad, int64_t cols, float norm, unsigned* amax, const float* sup,
            uint8_t* codes, unsigned* err, float* sout, cudaStream_t st, float* xout = nullptr, int64_t rows_out = 0) {
@@ -269,8 +252,12 @@ bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_
     if (mode > 2 || B < 512 || B > 16384 || (B & (B - 1)) || rows_pad % B || cols % 4) return false;
     if (mode == 2 && (in_dtype != DT_F32 || !xout)) return false;
     if ((uintptr_t)in % (in_dtype == DT_BF16 ? 8 : 16)) return false;
-    float* buf = cb_scratch((size_t)rows_pad * (size_t)cols);
-    if (!buf) return false;
+    // stream-ordered scratch for the partial transform: no sharing between
+    // streams or calls, returned to the pool after the last reader
+    float* buf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)rows_pad * (size_t)cols * sizeof(float), st) !=
+        cudaSuccess)
+        return false;
     int lb = 0;
     while ((int64_t(1) << lb) < B) ++lb;
     {
@@ -295,6 +282,7 @@ bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_
     default: cb_hi_dispatch<6>(mode, fmt, buf, rows_pad, cols, norm, ar, sr, cr, err, sro, st, xout, rows_out); break;
     }
     if (mode == 1 && cp) run_plain(in, in_dtype, b * cols, 1, fmt, ap, sp, cp, err, spo, st);
+    cudaFreeAsync(buf, st);
     return true;
 }
 
