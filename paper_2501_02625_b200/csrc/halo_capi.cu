@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -357,18 +358,21 @@ static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows,
 }
 
 namespace {
-// per-thread scratch for the free-function entry points
+// device scratch words (absmax, scale, error flag) for the free-function
+// entry points: one set per (host thread, stream), so calls on different
+// streams never share an absmax word
 struct FreeScratch {
-    Buffer dev, rows;
+    std::unordered_map<cudaStream_t, Buffer> dev, rows;
     ~FreeScratch() {
-        dev.release();
-        rows.release();
+        for (auto& kv : dev) kv.second.release();
+        for (auto& kv : rows) kv.second.release();
     }
 };
 thread_local FreeScratch t_scratch;
-DevScalars* free_scalars() {
-    if (t_scratch.dev.ensure(sizeof(DevScalars)) != HALO_OK) return nullptr;
-    return t_scratch.dev.as<DevScalars>();
+DevScalars* free_scalars(halo_stream_t stream) {
+    Buffer& b = t_scratch.dev[(cudaStream_t)stream];
+    if (b.ensure(sizeof(DevScalars)) != HALO_OK) return nullptr;
+    return b.as<DevScalars>();
 }
 }  // namespace
 
@@ -382,7 +386,7 @@ extern "C" halo_status halo_rotate_quantize(const void* a, int32_t a_dtype, int6
     int64_t B = 1;
     const bool rotate = had_block >= 0;
     if (rotate && resolve_block(cols, had_block, &B, "rotate_quantize") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
-    DevScalars* d = free_scalars();
+    DevScalars* d = free_scalars(stream);
     if (!d) return HALO_ERR_CUDA;
     return rotate_quantize_impl(a, a_dtype, rows, cols, B, rotate, format, supplied_scale, codes, &d->amax[0],
                                 scale_out, &d->err, (cudaStream_t)stream);
@@ -404,7 +408,7 @@ extern "C" halo_status halo_rotate_quantize_amax(const void* a, int32_t a_dtype,
     if (rows < 0 || cols <= 0 || cols % 16)
         return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: cols must be a positive multiple of 16");
     if (rows == 0) return HALO_OK;
-    DevScalars* d = free_scalars();
+    DevScalars* d = free_scalars(stream);
     if (!d) return HALO_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
     // the absmax word is the float's bit pattern (non-negative)
@@ -424,7 +428,7 @@ extern "C" halo_status halo_rotate_absmax(const void* a, int32_t a_dtype, int64_
                                           int64_t had_block, float* absmax_out, halo_stream_t stream) {
     if (!a || !absmax_out) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_absmax: null pointer");
     if (!valid_dtype(a_dtype) || cols <= 0 || cols % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_absmax: bad arguments");
-    DevScalars* d = free_scalars();
+    DevScalars* d = free_scalars(stream);
     if (!d) return HALO_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
     cudaMemsetAsync(&d->amax[0], 0, sizeof(unsigned), st);
@@ -471,7 +475,7 @@ extern "C" halo_status halo_left_rotate_quantize(const void* e, int32_t e_dtype,
     const int64_t b_pad = halo_padded_batch(b, had_block);
     int64_t B;
     if (resolve_block(b_pad, had_block, &B, "left_rotate_quantize") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
-    DevScalars* d = free_scalars();
+    DevScalars* d = free_scalars(stream);
     if (!d) return HALO_ERR_CUDA;
     return left_quant_impl(e, e_dtype, b, n, B, b_pad, format, codes_rot, codes_plain, &d->amax[SEH], &d->amax[SE],
                            scale_rot, scale_plain, &d->err, (cudaStream_t)stream);
@@ -546,9 +550,10 @@ extern "C" halo_status halo_rotate_quantize_rows(const void* a, int32_t a_dtype,
     int64_t B = 1;
     if (had_block >= 0 && resolve_block(cols, had_block, &B, "rotate_quantize_rows") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
     if (B > 256) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: Hadamard block must be <= 256");
-    DevScalars* d = free_scalars();
-    if (!d || t_scratch.rows.ensure((size_t)rows * sizeof(unsigned)) != HALO_OK) return HALO_ERR_CUDA;
-    if (!rows_v3_per_row(format, a_dtype, a, rows, cols, B, t_scratch.rows.as<unsigned>(), scales_out, codes, &d->err,
+    DevScalars* d = free_scalars(stream);
+    Buffer& arows = t_scratch.rows[(cudaStream_t)stream];
+    if (!d || arows.ensure((size_t)rows * sizeof(unsigned)) != HALO_OK) return HALO_ERR_CUDA;
+    if (!rows_v3_per_row(format, a_dtype, a, rows, cols, B, arows.as<unsigned>(), scales_out, codes, &d->err,
                          (cudaStream_t)stream))
         return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: operands must be 32 B aligned");
     return cuda_check("rotate_quantize_rows");
@@ -1117,7 +1122,7 @@ extern "C" halo_status halo_linear_export_inference_weights(halo_linear* l, uint
     if (l->s.granularity == HALO_GRAN_ROW)  // `scale` receives out_features floats
         return halo_rotate_quantize_rows(l->w, l->w_dtype, l->n, l->m, l->s.had_block, l->s.format_w, codes, scale,
                                          stream);
-    DevScalars* d = free_scalars();
+    DevScalars* d = free_scalars(stream);
     if (!d) return HALO_ERR_CUDA;
     return rotate_quantize_impl(l->w, l->w_dtype, l->n, l->m, B, true, l->s.format_w, nullptr, codes, &d->amax[SW],
                                 scale, &d->err, (cudaStream_t)stream);
