@@ -7,7 +7,9 @@ Every projection is a ``HaloLinearLayer`` (halo_linear.hpp semantics;
 HALO-0/1/2, INT8 or FP8-E4M3) wrapped in a torch.autograd.Function, so the
 block's backward runs the HALO backward kernels for the projections and
 torch autograd for the glue the reference does not cover (RMSNorm, RoPE,
-attention via scaled_dot_product_attention) — the block pattern of
+attention via scaled_dot_product_attention); the MLP runs as one
+mlp.HaloMLP (the library's SwiGLU and dX-add kernels, gate/up sharing one
+quantized X) — the block pattern of
 model.hpp:159-209 with the Llama attention added.  ``bf16=True`` builds the
 same block on torch.nn.functional.linear (cuBLAS) for the speed-up baseline.
 """
@@ -32,6 +34,24 @@ class _HaloLinearFn(torch.autograd.Function):
         r = mod.layer.backward(mod.sctx, dy.contiguous())
         mod.grad = r.grad_w if mod.grad is None else mod.grad + r.grad_w
         return r.e_x, None
+
+
+class _HaloMLPFn(torch.autograd.Function):
+    """The block's MLP through mlp.HaloMLP: the three HALO projections plus
+    the library's SwiGLU / dX-add kernels (one pass each) instead of torch's
+    silu / mul / autograd glue."""
+
+    @staticmethod
+    def forward(ctx, m, mlp):
+        ctx.mlp = mlp
+        return mlp.forward(m.contiguous())
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx, grads = ctx.mlp.backward(dy.contiguous())
+        for lin, g in zip(ctx.mlp.owners, grads):  # dW onto the block's gate / up / down
+            lin.grad = g if lin.grad is None else lin.grad + g
+        return dx, None
 
 
 class HaloLinear:
@@ -80,6 +100,11 @@ class LlamaBlock:
         self.gate = HaloLinear(w(inter, hidden), scheme, bf16)
         self.up = HaloLinear(w(inter, hidden), scheme, bf16)
         self.down = HaloLinear(w(hidden, inter), scheme, bf16)
+        self.mlp = None
+        if not bf16:
+            from .mlp import HaloMLP
+            self.mlp = HaloMLP(self.gate.w, self.up.w, self.down.w, scheme)
+            self.mlp.owners = (self.gate, self.up, self.down)
         self.n1 = torch.ones(hidden, device=device, requires_grad=True)
         self.n2 = torch.ones(hidden, device=device, requires_grad=True)
         pos = torch.arange(seq, device=device, dtype=torch.float32)
@@ -107,7 +132,10 @@ class LlamaBlock:
         att = att.transpose(1, 2).reshape(T, H)
         h = x + self.o(att)
         m = _rmsnorm(h, self.n2)
-        y = h + self.down(F.silu(self.gate(m)) * self.up(m))
+        if self.mlp is not None:
+            y = h + _HaloMLPFn.apply(m, self.mlp)
+        else:
+            y = h + self.down(F.silu(self.gate(m)) * self.up(m))
         return y
 
     def gemm_ops(self, tokens):

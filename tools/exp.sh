@@ -1,4 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python -m pytest tests/test_gpu_layer.py -q -x -k llama > gpurun_out/pytest_blk.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_blk.log
+timeout 1500 python tools/bench_block.py > gpurun_out/block.jsonl 2> gpurun_out/block.err; echo "rc=$?" >> gpurun_out/block.err
