@@ -70,7 +70,7 @@ typedef struct halo_placement {
 typedef struct halo_scheme {
     halo_placement F, E, G;
     int32_t format_x, format_w, format_e; /* halo_format */
-    int32_t granularity;                  /* HALO_GRAN_TENSOR, or HALO_GRAN_ROW: forward only (see halo_linear_forward) */
+    int32_t granularity;                  /* HALO_GRAN_TENSOR, or HALO_GRAN_ROW (INT8 / FP8; backward via the dequantized double products) */
     int32_t quantize_f, quantize_e, quantize_g;
     int32_t peft;
     int64_t had_block; /* 0 = full dimension (reference) */
@@ -224,7 +224,10 @@ HALO_API halo_status halo_linear_forward_shared(halo_linear* layer, const halo_c
                                        int32_t y_dtype, halo_stream_t stream);
 
 /* backward, halo_linear.hpp:305-439: e_y (b x n) -> e_x (b x m), grad_w
- * (n x m; may be NULL to skip G). */
+ * (n x m; may be NULL to skip G).  Granularity::row: the row scales sit on
+ * the contracted dim of E and G, so both products are the reference's
+ * dequantized double matmuls (quantize.hpp:377-379), bit-exact, on the FP64
+ * pipe; out_features % 256 == 0, no PEFT / sharded / scattered layers. */
 HALO_API halo_status halo_linear_backward(halo_linear* layer, const halo_ctx* ctx, const void* e_y, int32_t e_dtype,
                                  void* e_x, int32_t ex_dtype, void* grad_w, int32_t gw_dtype, halo_stream_t stream);
 

@@ -115,6 +115,7 @@ def ref():
         L.ref_linear.argtypes = [C.c_int, C.c_int, _ll, _ll, _ll, _ll, _f32p, _f32p, _f32p, _f32p,
                                  _f32p, _f32p, _f32p, C.POINTER(C.c_float), _f32p,
                                  C.POINTER(C.c_float)]
+        L.ref_linear_g.argtypes = [C.c_int, C.c_int, _ll, C.c_int] + L.ref_linear.argtypes[3:]
         L.ref_fsdp_gather.argtypes = [_ll, _f32p, _ll, _ll, C.c_int, C.c_int, _f32p,
                                       C.POINTER(C.c_float), _f64p]
         L.ref_reduce_scatter.argtypes = [_ll, _f32p, _ll, _ll, _f32p]
@@ -309,7 +310,10 @@ def ref_qmatmul(A, B, transpose_b, fmt, sa, sb):
     return out
 
 
-def ref_linear(level, fmt, block, X, W, EY):
+def ref_linear(level, fmt, block, X, W, EY, gran=0):
+    """The reference HaloLinearLayer forward+backward (gran 1 = Granularity::row():
+    per-row scales, dequantized double products, quantize.hpp:377-379);
+    sx / sw are the first scale of each operand."""
     X, W, EY = f32(X), f32(W), f32(EY)
     b, m = X.shape
     n = W.shape[0]
@@ -320,8 +324,8 @@ def ref_linear(level, fmt, block, X, W, EY):
     wq = np.zeros((n, m), np.float32)
     sx, sw = C.c_float(), C.c_float()
     L = ref()
-    _chk(L, L.ref_linear(level, fmt, block, b, m, n, X, W, EY, Y, EX, GW, xq, C.byref(sx), wq,
-                         C.byref(sw)))
+    _chk(L, L.ref_linear_g(level, fmt, block, gran, b, m, n, X, W, EY, Y, EX, GW, xq, C.byref(sx), wq,
+                           C.byref(sw)))
     return dict(Y=Y, EX=EX, GW=GW, xq=xq, sx=sx.value, wq=wq, sw=sw.value)
 
 

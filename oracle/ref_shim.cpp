@@ -160,13 +160,16 @@ int ref_qmatmul(const float* A, const float* B, long long M, long long N, long l
 // runs HaloLinearLayer verbatim (halo_linear.hpp:227-462); otherwise the
 // same sequence is composed from reference primitives with blocked
 // transforms, following error_path / gradient_path line by line.
-int ref_linear(int level, int fmt, long long block, long long b, long long m, long long n,
-               const float* X, const float* W, const float* EY, float* Y, float* EX, float* GW,
-               float* xq, float* sx, float* wq, float* sw) {
+// gran 0 = Granularity::tensor(), 1 = Granularity::row() (quantize.hpp:73-80);
+// sx / sw receive the first scale of each operand.
+int ref_linear_g(int level, int fmt, long long block, int gran, long long b, long long m, long long n,
+                 const float* X, const float* W, const float* EY, float* Y, float* EX, float* GW,
+                 float* xq, float* sx, float* wq, float* sw) {
     return guard([&] {
         const Tensor x = make(X, b, m), w = make(W, n, m), ey = make(EY, b, n);
-        const HaloScheme scheme = level == 0 ? halo0(fmt_of(fmt)) : level == 1 ? halo1(fmt_of(fmt))
-                                                                               : halo2(fmt_of(fmt));
+        const Granularity g = gran ? Granularity::row() : Granularity::tensor();
+        const HaloScheme scheme = level == 0 ? halo0(fmt_of(fmt), g) : level == 1 ? halo1(fmt_of(fmt), g)
+                                                                                 : halo2(fmt_of(fmt), g);
         if (block == 0) {
             HaloLinearLayer layer(w, scheme);
             SavedContext ctx;
@@ -181,7 +184,6 @@ int ref_linear(int level, int fmt, long long block, long long b, long long m, lo
             return;
         }
         const NumericFormat f = fmt_of(fmt);
-        const Granularity g = Granularity::tensor();
         // forward :288-299
         const QuantizedTensor qx = quantize(level ? right_blocked(x, block, false) : x, f, g);
         const QuantizedTensor qw = quantize(level ? right_blocked(w, block, false) : w, f, g);
@@ -210,6 +212,12 @@ int ref_linear(int level, int fmt, long long block, long long b, long long m, lo
         *sx = qx.scales[0];
         *sw = qw.scales[0];
     });
+}
+
+int ref_linear(int level, int fmt, long long block, long long b, long long m, long long n,
+               const float* X, const float* W, const float* EY, float* Y, float* EX, float* GW,
+               float* xq, float* sx, float* wq, float* sw) {
+    return ref_linear_g(level, fmt, block, 0, b, m, n, X, W, EY, Y, EX, GW, xq, sx, wq, sw);
 }
 
 // HQ-FSDP forward gather (hqfsdp.hpp:131-148, 204-237): codes of the padded

@@ -1,0 +1,153 @@
+// Granularity::row backward products (halo_linear.hpp:381-439 with
+// scheme.granularity = row).  Per-row scales of (WH)_Q and of E_Y's codes sit
+// on the CONTRACTED dim of the E and G products, so one rescale of an integer
+// accumulator cannot reproduce them; the reference dequantizes each operand
+// to T = float (double(code) * scale rounded to float, quantize.hpp:283-294)
+// and multiplies in double, k ascending per output (qmatmul :377-379,
+// tensor.hpp:127-144 / matmul_nt_acc / matmul_tn_acc).
+//
+// This kernel restates exactly that: the products of two floats are exact in
+// double, the accumulation runs k = 0..K-1 sequentially per output element in
+// double (one DFMA of an exact product == the reference's add), and the
+// result is rounded once to float -- bit-exact with the reference for any
+// shapes.  It runs on the FP64 pipe (the tensor cores have no double
+// accumulate of dequantized floats); the row-granularity backward is a
+// parity path, the HALO tensor-granularity GEMMs in gemm_sm100.cu are the
+// throughput path.
+//
+// Operand views: A(i,k) = deq(a[i*a_si + k*a_sk], as[i*as_si + k*as_sk]),
+// B(k,j) = deq(b[k*b_sk + j*b_sj], bs[k*bs_sk + j*bs_sj]); one of each scale
+// stride pair is 0 (per-row / per-column scales) -- so the transposed views
+// the backward needs (E^T for G, transpose_quantized :297-334) are strides,
+// not copies.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "halo_internal.h"
+#include "quant_round.cuh"
+#include "sm100.cuh"
+
+namespace halo_b200 {
+namespace {
+
+constexpr int DG_BM = 64, DG_BN = 64, DG_BK = 16, DG_THREADS = 256;
+
+template <int FMT>
+__device__ __forceinline__ float code_value(uint8_t c) {
+    if (FMT == FMT_INT8) return (float)(int8_t)c;
+    const float mag = e4m3_mag(c & 0x7Fu);
+    return (c & 0x80u) ? -mag : mag;
+}
+
+// deq (quantize.hpp:289): static_cast<float>(double(code) * double(scale))
+template <int FMT>
+__device__ __forceinline__ float deq(uint8_t c, float s) {
+    return __double2float_rn(__dmul_rn((double)code_value<FMT>(c), (double)s));
+}
+
+struct DeqView {
+    const uint8_t* codes;
+    const float* scale;
+    int64_t s0, s1;    // element strides (row index, k) for A; (k, col index) for B
+    int64_t ss0, ss1;  // scale strides, same index pair
+};
+
+template <int FMT>
+__global__ void __launch_bounds__(DG_THREADS) k_deq_gemm(DeqView A, DeqView B, float* __restrict__ C, int64_t M,
+                                                        int64_t N, int64_t K, int64_t ldc) {
+    __shared__ float As[DG_BK][DG_BM];
+    __shared__ float Bs[DG_BK][DG_BN];
+    const int tid = threadIdx.x;
+    const int64_t i0 = (int64_t)blockIdx.y * DG_BM, j0 = (int64_t)blockIdx.x * DG_BN;
+    const int tr = tid / 16, tc = tid % 16;  // 16 x 16 threads, 4 x 4 outputs each (strided by 16)
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    pdl_wait();
+    for (int64_t k0 = 0; k0 < K; k0 += DG_BK) {
+        // 1024 elements of each operand tile, 4 per thread; the fastest
+        // index follows the operand's unit stride so loads coalesce
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int idx = tid + e * DG_THREADS;
+            int ii, kk;
+            if (A.s1 == 1) { kk = idx % DG_BK; ii = idx / DG_BK; } else { ii = idx % DG_BM; kk = idx / DG_BM; }
+            const int64_t gi = i0 + ii, gk = k0 + kk;
+            float v = 0.f;
+            if (gi < M && gk < K) v = deq<FMT>(A.codes[gi * A.s0 + gk * A.s1], A.scale[gi * A.ss0 + gk * A.ss1]);
+            As[kk][ii] = v;
+            int jj;
+            if (B.s1 == 1) { jj = idx % DG_BN; kk = idx / DG_BN; } else { kk = idx % DG_BK; jj = idx / DG_BK; }
+            const int64_t gj = j0 + jj, gk2 = k0 + kk;
+            float w = 0.f;
+            if (gj < N && gk2 < K) w = deq<FMT>(B.codes[gk2 * B.s0 + gj * B.s1], B.scale[gk2 * B.ss0 + gj * B.ss1]);
+            Bs[kk][jj] = w;
+        }
+        __syncthreads();
+        const int kn = (int)(K - k0 < DG_BK ? K - k0 : DG_BK);
+        for (int kk = 0; kk < kn; ++kk) {  // k ascending: the reference's order
+            double a[4], b[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = (double)As[kk][tr + 16 * r];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) b[c] = (double)Bs[kk][tc + 16 * c];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+    pdl_trigger();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t i = i0 + tr + 16 * r;
+        if (i >= M) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int64_t j = j0 + tc + 16 * c;
+            if (j < N) C[i * ldc + j] = __double2float_rn(acc[r][c]);
+        }
+    }
+}
+
+// pad_rows (halo_linear.hpp:393-395) into fp32: rows [b, b_pad) are zero
+template <typename InT>
+__global__ void k_pad_f32(const InT* __restrict__ in, float* __restrict__ out, int64_t nin, int64_t nout) {
+    pdl_wait();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nout; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = i < nin ? (float)in[i] : 0.f;
+    pdl_trigger();
+}
+
+}  // namespace
+
+void pad_rows_f32(const void* in, int in_dtype, int64_t b, int64_t b_pad, int64_t cols, float* out, cudaStream_t st) {
+    const int64_t nout = b_pad * cols;
+    if (nout <= 0) return;
+    const unsigned grid = (unsigned)((nout + 255) / 256 < 148 * 16 ? (nout + 255) / 256 : 148 * 16);
+    if (in_dtype == DT_BF16)
+        launch_pdl(k_pad_f32<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(in), out,
+                   b * cols, nout);
+    else
+        launch_pdl(k_pad_f32<float>, dim3(grid), dim3(256), 0, st, static_cast<const float*>(in), out, b * cols, nout);
+}
+
+bool deq_gemm(int fmt, const uint8_t* a, const float* as, int64_t a_si, int64_t a_sk, int64_t as_si, int64_t as_sk,
+              const uint8_t* b, const float* bs, int64_t b_sk, int64_t b_sj, int64_t bs_sk, int64_t bs_sj, float* c,
+              int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
+    if (fmt != FMT_INT8 && fmt != FMT_E4M3) return false;
+    if (M <= 0 || N <= 0) return true;
+    const DeqView A{a, as, a_si, a_sk, as_si, as_sk}, B{b, bs, b_sk, b_sj, bs_sk, bs_sj};
+    const dim3 grid((unsigned)((N + DG_BN - 1) / DG_BN), (unsigned)((M + DG_BM - 1) / DG_BM));
+    if (fmt == FMT_INT8)
+        launch_pdl(k_deq_gemm<FMT_INT8>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
+    else
+        launch_pdl(k_deq_gemm<FMT_E4M3>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
+    return cudaPeekAtLastError() == cudaSuccess;
+}
+
+}  // namespace halo_b200

@@ -165,6 +165,7 @@ struct halo_ctx {
     // Granularity::row: per-token X scales, per-output-channel W scales and
     // the per-row absmax scratch
     Buffer xs_rows, ws_rows, amax_rows;
+    Buffer es_rows, ehs_rows;  // row-granularity backward: per-token E_Y / (H_b E_Y) scales
     bool row_gran = false;
     const uint8_t* wq_codes = nullptr;  // ctx.wq (own buffer or the layer's qweight)
     const float* wq_scale = nullptr;
@@ -184,7 +185,7 @@ struct halo_ctx {
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
         xq.release(); wq.release(); ehq.release(); eq.release(); wq2.release(); scratch.release();
-        gscratch.release(); dev.release(); xs_rows.release(); ws_rows.release(); amax_rows.release();
+        gscratch.release(); dev.release(); xs_rows.release(); ws_rows.release(); amax_rows.release(); es_rows.release(); ehs_rows.release();
     }
 };
 
@@ -955,17 +956,117 @@ static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows,
              nullptr, st);
 }
 
+// Granularity::row backward (halo_linear.hpp:381-439 with per-row scales).
+// The row scales of (WH)_Q / (E_Y)_Q / (H_b E_Y)_Q sit on the contracted dim
+// of the E and G products, so both run through qmatmul's dequantized double
+// path (quantize.hpp:377-379), restated bit-exactly by deq_gemm; the
+// quantizations are the per-row K1 (rows_v3_per_row), the transforms the same
+// K4 kernels as the tensor path.
+static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, int32_t e_dtype, void* e_x,
+                                 int32_t ex_dtype, void* grad_w, int32_t gw_dtype, cudaStream_t st) {
+    const halo_scheme& s = l->s;
+    const int64_t b = c->b, m = l->m, n = l->n;
+    const int fmt = s.format_e;
+    if (c->m != m || c->n != n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
+    if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
+    if (s.peft || l->scatter || c->wq_sharded)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row-granularity backward: no PEFT / sharded / scattered path");
+    // the saved operands are reused as in error_path / gradient_path (:390,
+    // :432): their rotation must be the one E and G ask for
+    if ((bool)s.E.right != c->wq_rotated || (bool)s.G.right != c->xq_rotated)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row-granularity backward needs the saved operand rotations");
+    if (fmt != HALO_FMT_INT8 && fmt != HALO_FMT_FP8_E4M3)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row granularity supports INT8 / FP8 E4M3");
+    if (n % 256) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row-granularity backward needs out_features % 256 == 0");
+    if (!grad_w && !e_x) return HALO_OK;
+    int64_t Bm = 1;
+    if ((s.E.right || s.G.right) && resolve_block(m, s.had_block, &Bm, "backward") != HALO_OK)
+        return HALO_ERR_INVALID_ARGUMENT;
+    DevScalars* d = c->d();
+    const bool left = s.E.left;
+    const int64_t b_pad = left ? halo_padded_batch(b, s.had_block) : b;
+    int64_t Bb = 1;
+    if (left && resolve_block(b_pad, s.had_block, &Bb, "backward (token dim)") != HALO_OK)
+        return HALO_ERR_INVALID_ARGUMENT;
+    c->b_pad = b_pad;
+    const int64_t mx = b_pad > n ? b_pad : n;
+    if (c->eq.ensure((size_t)(b * n)) != HALO_OK || c->es_rows.ensure((size_t)b * sizeof(float)) != HALO_OK ||
+        c->amax_rows.ensure((size_t)mx * sizeof(unsigned)) != HALO_OK ||
+        c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
+        return HALO_ERR_CUDA;
+    // (E_Y)_Q per token (:371); feeds E (no left rotation) and G
+    const bool plain = grad_w || !left;
+    if (plain) {
+        ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
+        if (!rows_v3_per_row(fmt, e_dtype, e_y, b, n, 1, c->amax_rows.as<unsigned>(), c->es_rows.as<float>(),
+                             c->eq.as<uint8_t>(), &d->err, st))
+            return fail(HALO_ERR_INVALID_ARGUMENT, "backward: row-granularity operands must be 32 B aligned");
+        ++l->ce;
+    }
+    float* P = c->scratch.as<float>();
+    // ---- error path (:381-413)
+    if (left) {
+        // (H_b pad(E_Y))_Q per padded token (:393-399)
+        if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->ehs_rows.ensure((size_t)b_pad * sizeof(float)) != HALO_OK ||
+            c->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
+            return HALO_ERR_CUDA;
+        float* T = c->gscratch.as<float>();
+        {
+            ProfScope ps(PC_K2, (double)b * n * dt_bytes(e_dtype) + (double)b_pad * n * 9, st);
+            pad_rows_f32(e_y, e_dtype, b, b_pad, n, T, st);
+            BaseScope orient(true);  // transform_left_h (:398)
+            run_cols(T, HALO_DTYPE_F32, b_pad, b_pad, n, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     T, b_pad, nullptr, nullptr, nullptr, st);
+            if (!rows_v3_per_row(fmt, HALO_DTYPE_F32, T, b_pad, n, 1, c->amax_rows.as<unsigned>(),
+                                 c->ehs_rows.as<float>(), c->ehq.as<uint8_t>(), &d->err, st))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "backward: row-granularity operands must be 32 B aligned");
+        }
+        ++l->ce;
+        if (e_x) {
+            {
+                ProfScope ps(PC_GEMM, 2.0 * (double)b_pad * m * n, st);
+                if (!deq_gemm(fmt, c->ehq.as<uint8_t>(), c->ehs_rows.as<float>(), n, 1, 1, 0, c->wq_codes, c->wq_scale,
+                              m, 1, 1, 0, P, b_pad, m, n, m, st))
+                    return fail(HALO_ERR_CUDA, "backward: E product launch failed");
+            }
+            // transform_left, take_rows(b) (:405-409), in place
+            ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
+            BaseScope orient(false);
+            run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     P, b, nullptr, nullptr, nullptr, st);
+        }
+    } else if (e_x) {
+        ProfScope ps(PC_GEMM, 2.0 * (double)b * m * n, st);
+        if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), n, 1, 1, 0, c->wq_codes, c->wq_scale, m, 1, 1,
+                      0, P, b, m, n, m, st))
+            return fail(HALO_ERR_CUDA, "backward: E product launch failed");
+    }
+    // transform_right_ht (:410-411) or the exact copy / convert
+    if (e_x) finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st);
+    // ---- gradient path (:418-439): G = transpose_quantized(eq) (XH)_Q [H^T];
+    // E_Y^T's scales become per-column (:312-316)
+    if (grad_w) {
+        if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+        float* G = c->gscratch.as<float>();
+        {
+            ProfScope ps(PC_GEMM, 2.0 * (double)n * m * b, st);
+            if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), 1, n, 0, 1, c->xq_codes(), c->xq_scale, m, 1,
+                          1, 0, G, n, m, b, m, st))
+                return fail(HALO_ERR_CUDA, "backward: G product launch failed");
+        }
+        finish_right(G, grad_w, gw_dtype, n, m, Bm, s.G.right, st);
+    }
+    return cuda_check("backward");
+}
+
 extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, const void* e_y, int32_t e_dtype,
                                             void* e_x, int32_t ex_dtype, void* grad_w, int32_t gw_dtype,
                                             halo_stream_t stream) {
     if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
     if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
-    if (c->row_gran)
-        return fail(HALO_ERR_INVALID_ARGUMENT,
-                    "halo layer: row-granularity backward puts W's / E_Y's row scales on the contracted dim of E / G; "
-                    "the reference dequantizes and multiplies in double there (quantize.hpp:377-379) and the device "
-                    "path has no full-precision fallback");
+    if (c->row_gran) return backward_rows(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
     if (c->m != l->m || c->n != l->n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
     if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");

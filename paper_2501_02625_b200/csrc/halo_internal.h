@@ -135,6 +135,15 @@ bool cols_v3(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t
 bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, int64_t B,
                      unsigned* amax_rows, float* row_scales, uint8_t* codes, unsigned* err, cudaStream_t st);
 
+// Granularity::row backward products (deq_gemm.cu): C[i,j] (fp32, ldc) =
+// sum_k deq(A(i,k)) * deq(B(k,j)) in double, k ascending (qmatmul's
+// dequantized path, quantize.hpp:377-379).  Views by element / scale strides.
+bool deq_gemm(int fmt, const uint8_t* a, const float* as, int64_t a_si, int64_t a_sk, int64_t as_si, int64_t as_sk,
+              const uint8_t* b, const float* bs, int64_t b_sk, int64_t b_sj, int64_t bs_sk, int64_t bs_sj, float* c,
+              int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st);
+// fp32 copy of a (b x cols) bf16 / fp32 tensor with zero rows up to b_pad
+void pad_rows_f32(const void* in, int in_dtype, int64_t b, int64_t b_pad, int64_t cols, float* out, cudaStream_t st);
+
 // K2 phase A of the MLP gate/up projections fused with the SwiGLU backward
 // (fwht_cols3.cu)
 bool cols_swiglu_absmax(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t b, int64_t rows_pad,
