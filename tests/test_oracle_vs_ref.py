@@ -28,6 +28,34 @@ def test_layer_bitexact(O, level, fmt, block, b, m, n):
     assert r["sx"] == o["sx"] and r["sw"] == o["sw"]
 
 
+def _seq_double_product(a, b):
+    """sum_k a[:, k] * b[k, :] in double, k ascending (tensor.hpp:127-144)."""
+    acc = np.zeros((a.shape[0], b.shape[1]), np.float64)
+    for k in range(a.shape[1]):
+        acc += a[:, k:k + 1] * b[k:k + 1, :]
+    return acc.astype(np.float32)
+
+
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_row_granularity_backward_is_dequantized_double_product(O, fmt):
+    """What csrc/deq_gemm.cu restates: with Granularity::row the reference's
+    E and G products dequantize each operand to float (double(code) * scale,
+    quantize.hpp:283-294) and accumulate in double, k ascending
+    (quantize.hpp:377-379); E_Y^T carries E_Y's row scales as column scales
+    (transpose_quantized, :297-334).  HALO-0 (no rotations) isolates it."""
+    b, m, n = 40, 64, 48
+    X = O.bf16_round(O.ref_randn(b, m, 71))
+    W = O.bf16_round(O.ref_randn(n, m, 72, 1 / np.sqrt(m)))
+    E = O.bf16_round(O.ref_randn(b, n, 73, 1e-3))
+    r = O.ref_linear(0, fmt, 0, X, W, E, gran=1)
+    deq = lambda c, s: (c.astype(np.float64) * s[:, None].astype(np.float64)).astype(np.float32).astype(np.float64)
+    xq, sx = O.ref_quantize(X, fmt, gran=1)
+    wq, sw = O.ref_quantize(W, fmt, gran=1)
+    eq, se = O.ref_quantize(E, fmt, gran=1)
+    assert np.array_equal(r["EX"], _seq_double_product(deq(eq, se), deq(wq, sw)))
+    assert np.array_equal(r["GW"], _seq_double_product(deq(eq, se).T, deq(xq, sx)))
+
+
 @pytest.mark.parametrize("block", [2, 8, 64, 256, 1024])
 def test_transforms(O, block):
     a = O.ref_randn(8, 1024, block)
