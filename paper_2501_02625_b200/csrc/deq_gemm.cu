@@ -31,7 +31,7 @@
 namespace halo_b200 {
 namespace {
 
-constexpr int DG_BM = 64, DG_BN = 64, DG_BK = 16, DG_THREADS = 256;
+constexpr int DG_BM = 128, DG_BN = 128, DG_BK = 16, DG_THREADS = 256, DG_TM = 8;
 
 template <int FMT>
 __device__ __forceinline__ float code_value(uint8_t c) {
@@ -40,10 +40,11 @@ __device__ __forceinline__ float code_value(uint8_t c) {
     return (c & 0x80u) ? -mag : mag;
 }
 
-// deq (quantize.hpp:289): static_cast<float>(double(code) * double(scale))
+// deq (quantize.hpp:289): static_cast<float>(double(code) * double(scale)),
+// kept as the double the reference's matmul_acc widens it to
 template <int FMT>
-__device__ __forceinline__ float deq(uint8_t c, float s) {
-    return __double2float_rn(__dmul_rn((double)code_value<FMT>(c), (double)s));
+__device__ __forceinline__ double deq(uint8_t c, float s) {
+    return (double)__double2float_rn(__dmul_rn((double)code_value<FMT>(c), (double)s));
 }
 
 struct DeqView {
@@ -53,61 +54,64 @@ struct DeqView {
     int64_t ss0, ss1;  // scale strides, same index pair
 };
 
+// 128 x 128 output tile per CTA, 8 x 8 per thread (rows tr + 16 r, columns
+// tc + 16 c): 16 LDS.64 feed 64 DFMA per k step.  Operands are dequantized
+// once per tile element into shared memory as doubles.
 template <int FMT>
 __global__ void __launch_bounds__(DG_THREADS) k_deq_gemm(DeqView A, DeqView B, float* __restrict__ C, int64_t M,
                                                         int64_t N, int64_t K, int64_t ldc) {
-    __shared__ float As[DG_BK][DG_BM];
-    __shared__ float Bs[DG_BK][DG_BN];
+    __shared__ double As[DG_BK][DG_BM];
+    __shared__ double Bs[DG_BK][DG_BN];
     const int tid = threadIdx.x;
     const int64_t i0 = (int64_t)blockIdx.y * DG_BM, j0 = (int64_t)blockIdx.x * DG_BN;
-    const int tr = tid / 16, tc = tid % 16;  // 16 x 16 threads, 4 x 4 outputs each (strided by 16)
-    double acc[4][4];
+    const int tr = tid / 16, tc = tid % 16;
+    double acc[DG_TM][DG_TM];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < DG_TM; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+        for (int c = 0; c < DG_TM; ++c) acc[r][c] = 0.0;
     pdl_wait();
     for (int64_t k0 = 0; k0 < K; k0 += DG_BK) {
-        // 1024 elements of each operand tile, 4 per thread; the fastest
+        // 2048 elements of each operand tile, 8 per thread; the fastest
         // index follows the operand's unit stride so loads coalesce
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < (DG_BM * DG_BK) / DG_THREADS; ++e) {
             const int idx = tid + e * DG_THREADS;
             int ii, kk;
             if (A.s1 == 1) { kk = idx % DG_BK; ii = idx / DG_BK; } else { ii = idx % DG_BM; kk = idx / DG_BM; }
             const int64_t gi = i0 + ii, gk = k0 + kk;
-            float v = 0.f;
+            double v = 0.0;
             if (gi < M && gk < K) v = deq<FMT>(A.codes[gi * A.s0 + gk * A.s1], A.scale[gi * A.ss0 + gk * A.ss1]);
             As[kk][ii] = v;
             int jj;
             if (B.s1 == 1) { jj = idx % DG_BN; kk = idx / DG_BN; } else { kk = idx % DG_BK; jj = idx / DG_BK; }
             const int64_t gj = j0 + jj, gk2 = k0 + kk;
-            float w = 0.f;
+            double w = 0.0;
             if (gj < N && gk2 < K) w = deq<FMT>(B.codes[gk2 * B.s0 + gj * B.s1], B.scale[gk2 * B.ss0 + gj * B.ss1]);
             Bs[kk][jj] = w;
         }
         __syncthreads();
         const int kn = (int)(K - k0 < DG_BK ? K - k0 : DG_BK);
         for (int kk = 0; kk < kn; ++kk) {  // k ascending: the reference's order
-            double a[4], b[4];
+            double a[DG_TM], b[DG_TM];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = (double)As[kk][tr + 16 * r];
+            for (int r = 0; r < DG_TM; ++r) a[r] = As[kk][tr + 16 * r];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) b[c] = (double)Bs[kk][tc + 16 * c];
+            for (int c = 0; c < DG_TM; ++c) b[c] = Bs[kk][tc + 16 * c];
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < DG_TM; ++r)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
+                for (int c = 0; c < DG_TM; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
         }
         __syncthreads();
     }
     pdl_trigger();
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < DG_TM; ++r) {
         const int64_t i = i0 + tr + 16 * r;
         if (i >= M) continue;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < DG_TM; ++c) {
             const int64_t j = j0 + tc + 16 * c;
             if (j < N) C[i * ldc + j] = __double2float_rn(acc[r][c]);
         }
