@@ -64,3 +64,37 @@ def test_layer_fuzz_int8_bitexact(H, orc, seed):
     assert np.array_equal(y.cpu().numpy(), want["Y"]), tag
     assert np.array_equal(back.e_x.cpu().numpy(), want["EX"]), tag
     assert np.array_equal(back.grad_w.cpu().numpy(), want["GW"]), tag
+
+
+@pytest.mark.parametrize("seed", list(range(10)))
+def test_layer_fuzz_row_granularity(H, orc, seed):
+    """Seeded shapes at Granularity::row against the unmodified reference
+    layer: Y within 1e-6 (tensor-core GEMM with per-row/per-channel scale
+    epilogue), E_X and grad_W bit-exact (deq_gemm.cu's double products)."""
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(500 + seed)
+    level = int(rng.integers(0, 3))
+    fmt = int(rng.integers(0, 2))
+    m = int(rng.choice([256, 512, 1024]))
+    n = int(rng.choice([256, 512]))
+    b = int(rng.integers(1, 400))
+    block = int(rng.choice([0, 64, 128, 256])) if m == 256 else int(rng.choice([64, 128, 256]))
+    X = orc.randn(b, m, seed)
+    X[:, int(rng.integers(0, m))] *= 30.0
+    W = orc.randn(n, m, seed + 1, 1.0 / np.sqrt(m))
+    E = orc.randn(b, n, seed + 2, 1e-3)
+    E[int(rng.integers(0, b))] *= 20.0
+    X, W, E = orc.bf16_round(X), orc.bf16_round(W), orc.bf16_round(E)
+    want = orc.ref_linear(level, fmt, block, X, W, E, gran=1)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16),
+                              getattr(H, f"halo{level}")(fmt, block, H.GRAN_ROW), out_dtype=torch.float32,
+                              grad_dtype=torch.float32)
+    ctx = H.SavedContext()
+    y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx).cpu().numpy()
+    back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
+    torch.cuda.synchronize()
+    tag = f"level={level} fmt={fmt} b={b} m={m} n={n} block={block}"
+    assert np.linalg.norm(y - want["Y"]) <= 1e-6 * np.linalg.norm(want["Y"]), tag
+    assert np.array_equal(back.e_x.cpu().numpy(), want["EX"]), tag
+    assert np.array_equal(back.grad_w.cpu().numpy(), want["GW"]), tag
