@@ -70,7 +70,7 @@ typedef struct halo_placement {
 typedef struct halo_scheme {
     halo_placement F, E, G;
     int32_t format_x, format_w, format_e; /* halo_format */
-    int32_t granularity;                  /* HALO_GRAN_TENSOR, or HALO_GRAN_ROW (INT8 / FP8; backward via the dequantized double products) */
+    int32_t granularity;                  /* HALO_GRAN_TENSOR, HALO_GRAN_ROW or HALO_GRAN_COLUMN (INT8 / FP8; see below) */
     int32_t quantize_f, quantize_e, quantize_g;
     int32_t peft;
     int64_t had_block; /* 0 = full dimension (reference) */
@@ -163,6 +163,7 @@ HALO_API halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int32
  * granularities are not on the device path. */
 #define HALO_GRAN_TENSOR 0
 #define HALO_GRAN_ROW 1
+#define HALO_GRAN_COLUMN 2 /* INT8 / FP8; every product is the dequantized double matmul (deq_gemm) */
 
 /* quantize(transform_right(a, block), fmt, Granularity::row()): one scale per
  * row (compute_scales per group, quantize.hpp:202-239); codes bit-exact.

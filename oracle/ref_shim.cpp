@@ -160,14 +160,14 @@ int ref_qmatmul(const float* A, const float* B, long long M, long long N, long l
 // runs HaloLinearLayer verbatim (halo_linear.hpp:227-462); otherwise the
 // same sequence is composed from reference primitives with blocked
 // transforms, following error_path / gradient_path line by line.
-// gran 0 = Granularity::tensor(), 1 = Granularity::row() (quantize.hpp:73-80);
+// gran 0 = Granularity::tensor(), 1 = ::row(), 2 = ::column() (quantize.hpp:73-80);
 // sx / sw receive the first scale of each operand.
 int ref_linear_g(int level, int fmt, long long block, int gran, long long b, long long m, long long n,
                  const float* X, const float* W, const float* EY, float* Y, float* EX, float* GW,
                  float* xq, float* sx, float* wq, float* sw) {
     return guard([&] {
         const Tensor x = make(X, b, m), w = make(W, n, m), ey = make(EY, b, n);
-        const Granularity g = gran ? Granularity::row() : Granularity::tensor();
+        const Granularity g = gran == 2 ? Granularity::column() : gran ? Granularity::row() : Granularity::tensor();
         const HaloScheme scheme = level == 0 ? halo0(fmt_of(fmt), g) : level == 1 ? halo1(fmt_of(fmt), g)
                                                                                  : halo2(fmt_of(fmt), g);
         if (block == 0) {

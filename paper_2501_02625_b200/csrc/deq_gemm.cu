@@ -127,6 +127,63 @@ __global__ void k_pad_f32(const InT* __restrict__ in, float* __restrict__ out, i
     pdl_trigger();
 }
 
+// Granularity::column quantization (quantize.hpp:202-280, group_of = j):
+// absmax per column, scale = absmax / format_max (1 for an all-zero
+// column), codes by the exact quantizers.  One thread per column and a chunk
+// of DG_RCH rows per CTA row: warps read 32 consecutive columns (coalesced).
+constexpr int DG_RCH = 64;
+
+template <typename InT>
+__global__ void __launch_bounds__(256) k_col_absmax(const InT* __restrict__ in, int64_t rows, int64_t cols,
+                                                   unsigned* __restrict__ amax, unsigned* err) {
+    pdl_wait();
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (j < cols) {
+        const int64_t r0 = (int64_t)blockIdx.y * DG_RCH;
+        const int64_t r1 = r0 + DG_RCH < rows ? r0 + DG_RCH : rows;
+        float m = 0.f;
+        uint32_t bad = 0;
+        for (int64_t r = r0; r < r1; ++r) {
+            const float v = (float)in[r * cols + j];
+            bad |= nonfinite_bits(v);
+            m = fmaxf(m, fabsf(v));
+        }
+        atomic_absmax(&amax[j], m);
+        if (bad) atomicOr(err, ERRF_NONFINITE);
+    }
+    pdl_trigger();
+}
+
+template <typename InT, int FMT>
+__global__ void __launch_bounds__(256) k_col_quant(const InT* __restrict__ in, int64_t rows, int64_t cols,
+                                                  const unsigned* __restrict__ amax, float* __restrict__ scales,
+                                                  uint8_t* __restrict__ codes) {
+    pdl_wait();
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (j < cols) {
+        float s, inv;
+        resolve_scale(&amax[j], nullptr, FMT, &s, &inv);
+        if (blockIdx.y == 0) scales[j] = s;
+        const int64_t r0 = (int64_t)blockIdx.y * DG_RCH;
+        const int64_t r1 = r0 + DG_RCH < rows ? r0 + DG_RCH : rows;
+        for (int64_t r = r0; r < r1; ++r) codes[r * cols + j] = quant1<FMT>((float)in[r * cols + j], s, inv);
+    }
+    pdl_trigger();
+}
+
+template <typename InT>
+static void col_quant_launch(int fmt, const InT* in, int64_t rows, int64_t cols, unsigned* amax, float* scales,
+                             uint8_t* codes, unsigned* err, cudaStream_t st) {
+    const dim3 grid((unsigned)((cols + 255) / 256), (unsigned)((rows + DG_RCH - 1) / DG_RCH));
+    launch_pdl(k_col_absmax<InT>, grid, dim3(256), 0, st, in, rows, cols, amax, err);
+    if (fmt == FMT_INT8)
+        launch_pdl(k_col_quant<InT, FMT_INT8>, grid, dim3(256), 0, st, in, rows, cols, (const unsigned*)amax, scales,
+                   codes);
+    else
+        launch_pdl(k_col_quant<InT, FMT_E4M3>, grid, dim3(256), 0, st, in, rows, cols, (const unsigned*)amax, scales,
+                   codes);
+}
+
 }  // namespace
 
 void pad_rows_f32(const void* in, int in_dtype, int64_t b, int64_t b_pad, int64_t cols, float* out, cudaStream_t st) {
@@ -151,6 +208,18 @@ bool deq_gemm(int fmt, const uint8_t* a, const float* as, int64_t a_si, int64_t 
         launch_pdl(k_deq_gemm<FMT_INT8>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
     else
         launch_pdl(k_deq_gemm<FMT_E4M3>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
+    return cudaPeekAtLastError() == cudaSuccess;
+}
+
+bool col_quantize(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, unsigned* amax, float* scales,
+                  uint8_t* codes, unsigned* err, cudaStream_t st) {
+    if (fmt != FMT_INT8 && fmt != FMT_E4M3) return false;
+    if (rows <= 0 || cols <= 0) return true;
+    cudaMemsetAsync(amax, 0, (size_t)cols * sizeof(unsigned), st);
+    if (in_dtype == DT_BF16)
+        col_quant_launch(fmt, static_cast<const __nv_bfloat16*>(in), rows, cols, amax, scales, codes, err, st);
+    else
+        col_quant_launch(fmt, static_cast<const float*>(in), rows, cols, amax, scales, codes, err, st);
     return cudaPeekAtLastError() == cudaSuccess;
 }
 

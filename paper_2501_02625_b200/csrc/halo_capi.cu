@@ -167,6 +167,7 @@ struct halo_ctx {
     Buffer xs_rows, ws_rows, amax_rows;
     Buffer es_rows, ehs_rows;  // row-granularity backward: per-token E_Y / (H_b E_Y) scales
     bool row_gran = false;
+    int32_t gran = HALO_GRAN_TENSOR;
     const uint8_t* wq_codes = nullptr;  // ctx.wq (own buffer or the layer's qweight)
     const float* wq_scale = nullptr;
     const float* xq_scale = nullptr;
@@ -587,8 +588,8 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
     if (!s.quantize_f || !s.quantize_e || !s.quantize_g)
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
-    if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW)
-        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: only tensor and row granularity are on the device path");
+    if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW && s.granularity != HALO_GRAN_COLUMN)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: tensor, row and column granularity are on the device path");
     if (s.granularity == HALO_GRAN_ROW && (m % 256 || (s.had_block ? s.had_block : m) > 256 ||
                                            !is_pow2(s.had_block ? s.had_block : m)))
         return fail(HALO_ERR_INVALID_ARGUMENT,
@@ -784,6 +785,9 @@ static halo_status quantize_weight(halo_linear* l, halo_ctx* c, bool rotated, Bu
     return HALO_OK;
 }
 
+static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
+                         cudaStream_t st);
+
 extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_t x_dtype, int64_t b, void* y,
                                            int32_t y_dtype, halo_ctx* c, halo_stream_t stream) {
     if (!l || !x || !y || !c) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
@@ -805,8 +809,64 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     int64_t B = 1;
     if (rot && resolve_block(l->m, s.had_block, &B, "forward") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
     c->row_gran = s.granularity == HALO_GRAN_ROW;
+    c->gran = s.granularity;
     c->xq_borrow = nullptr;
     c->had_block = s.had_block;
+    if (s.granularity == HALO_GRAN_COLUMN) {
+        // Granularity::column: X's and W's scales both sit on F's contracted
+        // dim, so Y is qmatmul's dequantized double product
+        // (quantize.hpp:377-379), restated bit-exactly by deq_gemm
+        if (l->qcodes || l->sharded)
+            return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: column granularity with installed qweight codes");
+        c->wq_sharded = false;
+        const int64_t m = l->m, n = l->n, rmax = b > n ? b : n;
+        const int64_t tmp = (rmax * m > b * n ? rmax * m : b * n) * (int64_t)sizeof(float);
+        if (c->xs_rows.ensure((size_t)m * sizeof(float)) != HALO_OK || c->ws_rows.ensure((size_t)m * sizeof(float)) != HALO_OK ||
+            c->amax_rows.ensure((size_t)m * sizeof(unsigned)) != HALO_OK || c->wq.ensure((size_t)(n * m)) != HALO_OK ||
+            c->gscratch.ensure((size_t)tmp) != HALO_OK || c->scratch.ensure((size_t)(rmax * m) * sizeof(float)) != HALO_OK)
+            return HALO_ERR_CUDA;
+        // quantize([A H], fmt, column) (:292-297)
+        auto quant_side = [&](const void* src, int32_t dt, int64_t rows, uint8_t* codes, float* scales) -> bool {
+            const void* q = src;
+            int32_t qdt = dt;
+            if (rot) {
+                float* T0 = c->gscratch.as<float>();
+                float* T1 = c->scratch.as<float>();
+                pad_rows_f32(src, dt, rows, rows, m, T0, st);
+                BaseScope h(false);  // transform_right (H)
+                run_rows(T0, HALO_DTYPE_F32, rows, m, B, 2, 0, nullptr, nullptr, nullptr, T1, HALO_DTYPE_F32, nullptr,
+                         nullptr, st);
+                q = T1;
+                qdt = HALO_DTYPE_F32;
+            }
+            return col_quantize(s.format_x, qdt, q, rows, m, c->amax_rows.as<unsigned>(), scales, codes, &d->err, st);
+        };
+        {
+            ProfScope ps(PC_K1, (double)b * l->m * (dt_bytes(x_dtype) + 1), st);
+            if (!quant_side(x, x_dtype, b, c->xq.as<uint8_t>(), c->xs_rows.as<float>()))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "forward: column-granularity quantization failed");
+        }
+        ++l->cx;
+        {
+            ProfScope ps(PC_K1, (double)n * m * (dt_bytes(l->w_dtype) + 1), st);
+            if (!quant_side(l->w, l->w_dtype, n, c->wq.as<uint8_t>(), c->ws_rows.as<float>()))
+                return fail(HALO_ERR_INVALID_ARGUMENT, "forward: column-granularity quantization failed");
+        }
+        ++l->cw;
+        c->wq_codes = c->wq.as<uint8_t>();
+        c->wq_scale = c->ws_rows.as<float>();
+        c->xq_scale = c->xs_rows.as<float>();
+        float* P = c->gscratch.as<float>();
+        {
+            ProfScope ps(PC_GEMM, 2.0 * (double)b * n * m, st);
+            if (!deq_gemm(s.format_x, c->xq.as<uint8_t>(), c->xs_rows.as<float>(), m, 1, 0, 1, c->wq_codes,
+                          c->wq_scale, 1, m, 1, 0, P, b, n, m, n, st))
+                return fail(HALO_ERR_CUDA, "forward: column-granularity product launch failed");
+        }
+        finish_right(P, y, y_dtype, b, n, 1, false, st);
+        c->valid = true;
+        return cuda_check("forward");
+    }
     if (c->row_gran) {
         // Granularity::row (quantize.hpp:73-132): X per token, W per output
         // channel -- both on non-contracted dims of F, so the integer GEMM
@@ -885,6 +945,8 @@ extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx
     if (!src->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared: source context has no forward");
     if (!valid_dtype(y_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
     const halo_scheme& s = l->s;
+    if (s.granularity == HALO_GRAN_COLUMN || src->gran == HALO_GRAN_COLUMN)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared: column granularity is not shared");
     if (src->m != l->m || src->fmt != s.format_x || src->xq_rotated != (bool)s.F.middle ||
         src->row_gran != (s.granularity == HALO_GRAN_ROW) || src->had_block != s.had_block)
         return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared: the source context's X quantizer differs from this layer's");
@@ -898,6 +960,7 @@ extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx
     c->fmt = s.format_x;
     c->xq_rotated = c->wq_rotated = s.F.middle;
     c->row_gran = src->row_gran;
+    c->gran = src->gran;
     c->had_block = s.had_block;
     c->xq_borrow = src->xq_codes();
     c->xq_scale = src->xq_scale;
@@ -977,8 +1040,23 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
     if ((bool)s.E.right != c->wq_rotated || (bool)s.G.right != c->xq_rotated)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row-granularity backward needs the saved operand rotations");
     if (fmt != HALO_FMT_INT8 && fmt != HALO_FMT_FP8_E4M3)
-        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row granularity supports INT8 / FP8 E4M3");
-    if (n % 256) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row-granularity backward needs out_features % 256 == 0");
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row / column granularity supports INT8 / FP8 E4M3");
+    // Granularity::column (c->gran): every scale vector indexes columns, and
+    // E_Y^T's column scales become row scales (transpose_quantized :317-320)
+    const bool col = c->gran == HALO_GRAN_COLUMN;
+    if (!col && n % 256)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: row-granularity backward needs out_features % 256 == 0");
+    auto gquant = [&](int32_t dt, const void* in, int64_t rows, float* scales, uint8_t* codes) -> bool {
+        unsigned* err = &c->d()->err;
+        return col ? col_quantize(fmt, dt, in, rows, n, c->amax_rows.as<unsigned>(), scales, codes, err, st)
+                   : rows_v3_per_row(fmt, dt, in, rows, n, 1, c->amax_rows.as<unsigned>(), scales, codes, err, st);
+    };
+    // scale strides (index pair of each product operand): per-row scales
+    // follow the operand's row, per-column its column
+    const int64_t e_si = col ? 0 : 1, e_sk = col ? 1 : 0;     // E / (H_b E) codes as A (i = token, k = out)
+    const int64_t w_sk = col ? 0 : 1, w_sj = col ? 1 : 0;     // (WH)_Q as B (k = out, j = in)
+    const int64_t g_si = col ? 1 : 0, g_sk = col ? 0 : 1;     // E^T as A (i = out, k = token)
+    const int64_t x_sk = col ? 0 : 1, x_sj = col ? 1 : 0;     // (XH)_Q as B (k = token, j = in)
     if (!grad_w && !e_x) return HALO_OK;
     int64_t Bm = 1;
     if ((s.E.right || s.G.right) && resolve_block(m, s.had_block, &Bm, "backward") != HALO_OK)
@@ -991,7 +1069,7 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
         return HALO_ERR_INVALID_ARGUMENT;
     c->b_pad = b_pad;
     const int64_t mx = b_pad > n ? b_pad : n;
-    if (c->eq.ensure((size_t)(b * n)) != HALO_OK || c->es_rows.ensure((size_t)b * sizeof(float)) != HALO_OK ||
+    if (c->eq.ensure((size_t)(b * n)) != HALO_OK || c->es_rows.ensure((size_t)mx * sizeof(float)) != HALO_OK ||
         c->amax_rows.ensure((size_t)mx * sizeof(unsigned)) != HALO_OK ||
         c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
         return HALO_ERR_CUDA;
@@ -999,8 +1077,7 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
     const bool plain = grad_w || !left;
     if (plain) {
         ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
-        if (!rows_v3_per_row(fmt, e_dtype, e_y, b, n, 1, c->amax_rows.as<unsigned>(), c->es_rows.as<float>(),
-                             c->eq.as<uint8_t>(), &d->err, st))
+        if (!gquant(e_dtype, e_y, b, c->es_rows.as<float>(), c->eq.as<uint8_t>()))
             return fail(HALO_ERR_INVALID_ARGUMENT, "backward: row-granularity operands must be 32 B aligned");
         ++l->ce;
     }
@@ -1008,7 +1085,7 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
     // ---- error path (:381-413)
     if (left) {
         // (H_b pad(E_Y))_Q per padded token (:393-399)
-        if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->ehs_rows.ensure((size_t)b_pad * sizeof(float)) != HALO_OK ||
+        if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->ehs_rows.ensure((size_t)mx * sizeof(float)) != HALO_OK ||
             c->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
             return HALO_ERR_CUDA;
         float* T = c->gscratch.as<float>();
@@ -1018,16 +1095,15 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
             BaseScope orient(true);  // transform_left_h (:398)
             run_cols(T, HALO_DTYPE_F32, b_pad, b_pad, n, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                      T, b_pad, nullptr, nullptr, nullptr, st);
-            if (!rows_v3_per_row(fmt, HALO_DTYPE_F32, T, b_pad, n, 1, c->amax_rows.as<unsigned>(),
-                                 c->ehs_rows.as<float>(), c->ehq.as<uint8_t>(), &d->err, st))
+            if (!gquant(HALO_DTYPE_F32, T, b_pad, c->ehs_rows.as<float>(), c->ehq.as<uint8_t>()))
                 return fail(HALO_ERR_INVALID_ARGUMENT, "backward: row-granularity operands must be 32 B aligned");
         }
         ++l->ce;
         if (e_x) {
             {
                 ProfScope ps(PC_GEMM, 2.0 * (double)b_pad * m * n, st);
-                if (!deq_gemm(fmt, c->ehq.as<uint8_t>(), c->ehs_rows.as<float>(), n, 1, 1, 0, c->wq_codes, c->wq_scale,
-                              m, 1, 1, 0, P, b_pad, m, n, m, st))
+                if (!deq_gemm(fmt, c->ehq.as<uint8_t>(), c->ehs_rows.as<float>(), n, 1, e_si, e_sk, c->wq_codes,
+                              c->wq_scale, m, 1, w_sk, w_sj, P, b_pad, m, n, m, st))
                     return fail(HALO_ERR_CUDA, "backward: E product launch failed");
             }
             // transform_left, take_rows(b) (:405-409), in place
@@ -1038,8 +1114,8 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
         }
     } else if (e_x) {
         ProfScope ps(PC_GEMM, 2.0 * (double)b * m * n, st);
-        if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), n, 1, 1, 0, c->wq_codes, c->wq_scale, m, 1, 1,
-                      0, P, b, m, n, m, st))
+        if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), n, 1, e_si, e_sk, c->wq_codes, c->wq_scale, m,
+                      1, w_sk, w_sj, P, b, m, n, m, st))
             return fail(HALO_ERR_CUDA, "backward: E product launch failed");
     }
     // transform_right_ht (:410-411) or the exact copy / convert
@@ -1051,8 +1127,8 @@ static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, i
         float* G = c->gscratch.as<float>();
         {
             ProfScope ps(PC_GEMM, 2.0 * (double)n * m * b, st);
-            if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), 1, n, 0, 1, c->xq_codes(), c->xq_scale, m, 1,
-                          1, 0, G, n, m, b, m, st))
+            if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), 1, n, g_si, g_sk, c->xq_codes(), c->xq_scale,
+                          m, 1, x_sk, x_sj, G, n, m, b, m, st))
                 return fail(HALO_ERR_CUDA, "backward: G product launch failed");
         }
         finish_right(G, grad_w, gw_dtype, n, m, Bm, s.G.right, st);
@@ -1066,7 +1142,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
     if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
-    if (c->row_gran) return backward_rows(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
+    if (c->row_gran || c->gran == HALO_GRAN_COLUMN) return backward_rows(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
     if (c->m != l->m || c->n != l->n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
     if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
@@ -1220,6 +1296,8 @@ extern "C" halo_status halo_linear_export_inference_weights(halo_linear* l, uint
         cudaMemcpyAsync(scale, l->qscale, sizeof(float), cudaMemcpyDeviceToDevice, st);
         return cuda_check("export");
     }
+    if (l->s.granularity == HALO_GRAN_COLUMN)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "export: column granularity is not exported");
     if (l->s.granularity == HALO_GRAN_ROW)  // `scale` receives out_features floats
         return halo_rotate_quantize_rows(l->w, l->w_dtype, l->n, l->m, l->s.had_block, l->s.format_w, codes, scale,
                                          stream);

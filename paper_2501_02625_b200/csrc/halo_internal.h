@@ -141,6 +141,9 @@ bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_
 bool deq_gemm(int fmt, const uint8_t* a, const float* as, int64_t a_si, int64_t a_sk, int64_t as_si, int64_t as_sk,
               const uint8_t* b, const float* bs, int64_t b_sk, int64_t b_sj, int64_t bs_sk, int64_t bs_sj, float* c,
               int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st);
+// quantize(A, fmt, Granularity::column()) (deq_gemm.cu): `cols` scales
+bool col_quantize(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, unsigned* amax, float* scales,
+                  uint8_t* codes, unsigned* err, cudaStream_t st);
 // fp32 copy of a (b x cols) bf16 / fp32 tensor with zero rows up to b_pad
 void pad_rows_f32(const void* in, int in_dtype, int64_t b, int64_t b_pad, int64_t cols, float* out, cudaStream_t st);
 

@@ -42,7 +42,7 @@ FP6_E3M2 = FMT_FP6_E3M2
 _DT = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16}
 
 
-GRAN_TENSOR, GRAN_ROW = 0, 1  # halo_b200.h HALO_GRAN_*
+GRAN_TENSOR, GRAN_ROW, GRAN_COLUMN = 0, 1, 2  # halo_b200.h HALO_GRAN_*
 
 
 def _stream():
@@ -270,11 +270,13 @@ class SavedContext:
         b = C.c_int64()
         check(lib().halo_ctx_saved(self._h, C.byref(xq), C.byref(sx), C.byref(wq), C.byref(sw), C.byref(b)))
         dt = code_dtype(layer.fmt)
-        rows = layer.scheme.granularity == GRAN_ROW
+        g = layer.scheme.granularity
+        nsx = b.value if g == GRAN_ROW else layer.in_features if g == GRAN_COLUMN else 1
+        nsw = layer.out_features if g == GRAN_ROW else layer.in_features if g == GRAN_COLUMN else 1
         return (_from_ptr(xq.value, (b.value, layer.in_features), dt),
-                _from_ptr(sx.value, (b.value if rows else 1,), torch.float32),
+                _from_ptr(sx.value, (nsx,), torch.float32),
                 _from_ptr(wq.value, (layer.out_features, layer.in_features), dt),
-                _from_ptr(sw.value, (layer.out_features if rows else 1,), torch.float32))
+                _from_ptr(sw.value, (nsw,), torch.float32))
 
     def error_operands(self, layer: "HaloLinearLayer"):
         ehq, seh, eq, se = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
