@@ -56,6 +56,26 @@ def test_row_granularity_backward_is_dequantized_double_product(O, fmt):
     assert np.array_equal(r["GW"], _seq_double_product(deq(eq, se).T, deq(xq, sx)))
 
 
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_column_granularity_is_dequantized_double_product(O, fmt):
+    """Granularity::column (quantize.hpp:73-132): one scale per column, all
+    three products dequantized double matmuls; E_Y^T's column scales become
+    row scales (transpose_quantized :317-320).  HALO-0 isolates it."""
+    b, m, n = 24, 32, 40
+    X = O.bf16_round(O.ref_randn(b, m, 81))
+    W = O.bf16_round(O.ref_randn(n, m, 82, 1 / np.sqrt(m)))
+    E = O.bf16_round(O.ref_randn(b, n, 83, 1e-3))
+    r = O.ref_linear(0, fmt, 0, X, W, E, gran=2)
+    deq = lambda c, s: (c.astype(np.float64) * s[None, :].astype(np.float64)).astype(np.float32).astype(np.float64)
+    xq, sx = O.ref_quantize(X, fmt, gran=2)
+    wq, sw = O.ref_quantize(W, fmt, gran=2)
+    eq, se = O.ref_quantize(E, fmt, gran=2)
+    assert sx.shape == (m,) and se.shape == (n,)
+    assert np.array_equal(r["Y"], _seq_double_product(deq(xq, sx), deq(wq, sw).T))
+    assert np.array_equal(r["EX"], _seq_double_product(deq(eq, se), deq(wq, sw)))
+    assert np.array_equal(r["GW"], _seq_double_product(deq(eq, se).T, deq(xq, sx)))
+
+
 @pytest.mark.parametrize("block", [2, 8, 64, 256, 1024])
 def test_transforms(O, block):
     a = O.ref_randn(8, 1024, block)
