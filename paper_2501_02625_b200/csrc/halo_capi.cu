@@ -1019,13 +1019,14 @@ static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows,
              nullptr, st);
 }
 
-// Granularity::row backward (halo_linear.hpp:381-439 with per-row scales).
-// The row scales of (WH)_Q / (E_Y)_Q / (H_b E_Y)_Q sit on the contracted dim
-// of the E and G products, so both run through qmatmul's dequantized double
-// path (quantize.hpp:377-379), restated bit-exactly by deq_gemm; the
-// quantizations are the per-row K1 (rows_v3_per_row), the transforms the same
-// K4 kernels as the tensor path.
-static halo_status backward_rows(halo_linear* l, halo_ctx* c, const void* e_y, int32_t e_dtype, void* e_x,
+// Granularity::row / ::column backward (halo_linear.hpp:381-439 with
+// per-row or per-column scales).  Some scale vector of (WH)_Q / (E_Y)_Q /
+// (H_b E_Y)_Q sits on the contracted dim of the E and G products, so both run
+// through qmatmul's dequantized double path (quantize.hpp:377-379), restated
+// bit-exactly by deq_gemm; the quantizations are the per-row K1
+// (rows_v3_per_row) or col_quantize, the transforms the same K4 kernels as
+// the tensor path.
+static halo_status backward_grouped(halo_linear* l, halo_ctx* c, const void* e_y, int32_t e_dtype, void* e_x,
                                  int32_t ex_dtype, void* grad_w, int32_t gw_dtype, cudaStream_t st) {
     const halo_scheme& s = l->s;
     const int64_t b = c->b, m = l->m, n = l->n;
@@ -1142,7 +1143,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
     if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
-    if (c->row_gran || c->gran == HALO_GRAN_COLUMN) return backward_rows(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
+    if (c->row_gran || c->gran == HALO_GRAN_COLUMN) return backward_grouped(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
     if (c->m != l->m || c->n != l->n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
     if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
