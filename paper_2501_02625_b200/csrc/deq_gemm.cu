@@ -31,7 +31,7 @@
 namespace halo_b200 {
 namespace {
 
-constexpr int DG_BM = 128, DG_BN = 128, DG_BK = 16, DG_THREADS = 256, DG_TM = 8;
+constexpr int DG_TM = 8, DG_TN = 4, DG_BM = 16 * DG_TM, DG_BN = 16 * DG_TN, DG_BK = 32, DG_THREADS = 256;
 
 template <int FMT>
 __device__ __forceinline__ float code_value(uint8_t c) {
@@ -54,26 +54,27 @@ struct DeqView {
     int64_t ss0, ss1;  // scale strides, same index pair
 };
 
-// 128 x 128 output tile per CTA, 8 x 8 per thread (rows tr + 16 r, columns
-// tc + 16 c): 16 LDS.64 feed 64 DFMA per k step.  Operands are dequantized
-// once per tile element into shared memory as doubles.
+// 128 x 64 output tile per CTA, 8 x 4 per thread (rows tr + 16 r, columns
+// tc + 16 c): 12 LDS.64 feed 32 DFMA per k step, and two CTAs fit an SM so
+// one's operand staging overlaps the other's DFMAs.  Operands are
+// dequantized once per tile element into shared memory as doubles.
 template <int FMT>
-__global__ void __launch_bounds__(DG_THREADS) k_deq_gemm(DeqView A, DeqView B, float* __restrict__ C, int64_t M,
+__global__ void __launch_bounds__(DG_THREADS, 2) k_deq_gemm(DeqView A, DeqView B, float* __restrict__ C, int64_t M,
                                                         int64_t N, int64_t K, int64_t ldc) {
     __shared__ double As[DG_BK][DG_BM];
     __shared__ double Bs[DG_BK][DG_BN];
     const int tid = threadIdx.x;
     const int64_t i0 = (int64_t)blockIdx.y * DG_BM, j0 = (int64_t)blockIdx.x * DG_BN;
     const int tr = tid / 16, tc = tid % 16;
-    double acc[DG_TM][DG_TM];
+    double acc[DG_TM][DG_TN];
 #pragma unroll
     for (int r = 0; r < DG_TM; ++r)
 #pragma unroll
-        for (int c = 0; c < DG_TM; ++c) acc[r][c] = 0.0;
+        for (int c = 0; c < DG_TN; ++c) acc[r][c] = 0.0;
     pdl_wait();
     for (int64_t k0 = 0; k0 < K; k0 += DG_BK) {
-        // 2048 elements of each operand tile, 8 per thread; the fastest
-        // index follows the operand's unit stride so loads coalesce
+        // the operand tiles, the fastest index following the operand's
+        // unit stride so loads coalesce
 #pragma unroll
         for (int e = 0; e < (DG_BM * DG_BK) / DG_THREADS; ++e) {
             const int idx = tid + e * DG_THREADS;
@@ -83,25 +84,29 @@ __global__ void __launch_bounds__(DG_THREADS) k_deq_gemm(DeqView A, DeqView B, f
             double v = 0.0;
             if (gi < M && gk < K) v = deq<FMT>(A.codes[gi * A.s0 + gk * A.s1], A.scale[gi * A.ss0 + gk * A.ss1]);
             As[kk][ii] = v;
-            int jj;
+        }
+#pragma unroll
+        for (int e = 0; e < (DG_BN * DG_BK) / DG_THREADS; ++e) {
+            const int idx = tid + e * DG_THREADS;
+            int jj, kk;
             if (B.s1 == 1) { jj = idx % DG_BN; kk = idx / DG_BN; } else { kk = idx % DG_BK; jj = idx / DG_BK; }
-            const int64_t gj = j0 + jj, gk2 = k0 + kk;
+            const int64_t gj = j0 + jj, gk = k0 + kk;
             double w = 0.0;
-            if (gj < N && gk2 < K) w = deq<FMT>(B.codes[gk2 * B.s0 + gj * B.s1], B.scale[gk2 * B.ss0 + gj * B.ss1]);
+            if (gj < N && gk < K) w = deq<FMT>(B.codes[gk * B.s0 + gj * B.s1], B.scale[gk * B.ss0 + gj * B.ss1]);
             Bs[kk][jj] = w;
         }
         __syncthreads();
         const int kn = (int)(K - k0 < DG_BK ? K - k0 : DG_BK);
         for (int kk = 0; kk < kn; ++kk) {  // k ascending: the reference's order
-            double a[DG_TM], b[DG_TM];
+            double a[DG_TM], b[DG_TN];
 #pragma unroll
             for (int r = 0; r < DG_TM; ++r) a[r] = As[kk][tr + 16 * r];
 #pragma unroll
-            for (int c = 0; c < DG_TM; ++c) b[c] = Bs[kk][tc + 16 * c];
+            for (int c = 0; c < DG_TN; ++c) b[c] = Bs[kk][tc + 16 * c];
 #pragma unroll
             for (int r = 0; r < DG_TM; ++r)
 #pragma unroll
-                for (int c = 0; c < DG_TM; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
+                for (int c = 0; c < DG_TN; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
         }
         __syncthreads();
     }
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(DG_THREADS) k_deq_gemm(DeqView A, DeqView B, f
         const int64_t i = i0 + tr + 16 * r;
         if (i >= M) continue;
 #pragma unroll
-        for (int c = 0; c < DG_TM; ++c) {
+        for (int c = 0; c < DG_TN; ++c) {
             const int64_t j = j0 + tc + 16 * c;
             if (j < N) C[i * ldc + j] = __double2float_rn(acc[r][c]);
         }
