@@ -990,6 +990,7 @@ ShardScope::~ShardScope() {
     t_shard_b = nullptr;
     t_scatter_c = nullptr;
 }
+bool ShardScope::active() { return t_shard_a || t_shard_b || t_scatter_c; }
 
 bool encode_scatter_maps(void* const* recv, int parts, int slot, int64_t len, int64_t cols, CUtensorMap* out) {
     auto enc = get_encode();

@@ -104,6 +104,30 @@ __global__ void __launch_bounds__(256) k_rank_mean(const float* __restrict__ rec
     }
 }
 
+
+// INT8 contractions longer than the s32 TMEM accumulator can hold exactly
+// (K*127^2 >= 2^31): K slices of raw s32 accumulators summed in int64, as the
+// reference accumulates (quantize.hpp:358-371), then its double epilogue
+// float(double(acc) * (double(sa) * double(sb))) (:370).
+__global__ void __launch_bounds__(256) k_acc_s64(const int* __restrict__ part, long long* __restrict__ acc,
+                                                 int64_t n, int first) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        acc[i] = (first ? 0LL : acc[i]) + (long long)part[i];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_epi_s64(const long long* __restrict__ acc, const float* __restrict__ sa,
+                                                 const float* __restrict__ sb, T* __restrict__ out, int64_t n) {
+    const double ss = (double)*sa * (double)*sb;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float c = (float)((double)acc[i] * ss);
+        if constexpr (sizeof(T) == 4) out[i] = c;
+        else out[i] = __float2bfloat16_rn(c);
+    }
+}
+
 static unsigned ew_grid(int64_t n) {
     int64_t want = (n / 8 + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * 8;
@@ -138,6 +162,18 @@ void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype
         k_rank_mean<__nv_bfloat16><<<grid, 256, 0, st>>>(recv, world, n, static_cast<__nv_bfloat16*>(out));
     else
         k_rank_mean<float><<<grid, 256, 0, st>>>(recv, world, n, static_cast<float*>(out));
+}
+
+void run_acc_s64(const int* part, long long* acc, int64_t n, int first, cudaStream_t st) {
+    k_acc_s64<<<ew_grid(n * 8), 256, 0, st>>>(part, acc, n, first);
+}
+
+void run_epi_s64(const long long* acc, const float* sa, const float* sb, void* out, int dtype, int64_t n,
+                 cudaStream_t st) {
+    if (dtype == DT_BF16)
+        k_epi_s64<__nv_bfloat16><<<ew_grid(n * 8), 256, 0, st>>>(acc, sa, sb, static_cast<__nv_bfloat16*>(out), n);
+    else
+        k_epi_s64<float><<<ew_grid(n * 8), 256, 0, st>>>(acc, sa, sb, static_cast<float*>(out), n);
 }
 
 }  // namespace halo_b200

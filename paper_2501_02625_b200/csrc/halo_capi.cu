@@ -218,15 +218,68 @@ struct halo_linear {
     }
 };
 
+// The INT8 GEMM accumulates in s32 TMEM: exact while K*127^2 < 2^31, i.e.
+// K <= 133,144.  The reference accumulates in int64 (quantize.hpp:358-371),
+// so longer contractions -- the G GEMM over more than 131072 tokens -- run
+// as K slices of raw s32 accumulators summed in int64, then the reference's
+// double epilogue.  The slices need row offsets along K, i.e. MN-major
+// operands (the G GEMM's layout); K-major operands that long are rejected.
+constexpr int64_t kI8SliceK = 131072;
+
+namespace {
+struct SplitScratch {
+    Buffer s32, s64, f32;
+    ~SplitScratch() {
+        s32.release();
+        s64.release();
+        f32.release();
+    }
+};
+thread_local SplitScratch t_split;
+}  // namespace
+
+// returns as run_gemm; out_f32: epilogue into this fp32 buffer instead of out
+static int gemm_i8_split(const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
+                         int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st) {
+    if (a_kmajor || b_kmajor || out_kind == 2 || ShardScope::active()) return -1;
+    const size_t mn = (size_t)M * (size_t)N;
+    if (t_split.s32.ensure(mn * 4) != HALO_OK || t_split.s64.ensure(mn * 8) != HALO_OK) return (int)cudaErrorMemoryAllocation;
+    for (int64_t k0 = 0; k0 < K; k0 += kI8SliceK) {
+        const int64_t kc = K - k0 < kI8SliceK ? K - k0 : kI8SliceK;
+        const int r = run_gemm(HALO_FMT_INT8, A + k0 * M, B + k0 * N, M, N, kc, 0, 0, sa, sb, t_split.s32.p, 2, st);
+        if (r != 0) return r;
+        run_acc_s64(t_split.s32.as<int>(), t_split.s64.as<long long>(), (int64_t)mn, k0 == 0, st);
+    }
+    run_epi_s64(t_split.s64.as<long long>(), sa, sb, out, out_kind == 1 ? HALO_DTYPE_BF16 : HALO_DTYPE_F32,
+                (int64_t)mn, st);
+    return 0;
+}
+
 static int prof_gemm(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                      int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, cudaStream_t st) {
     ProfScope ps(PC_GEMM, 2.0 * (double)M * (double)N * (double)K, st);
+    if (fmt == HALO_FMT_INT8 && K > kI8SliceK)
+        return gemm_i8_split(A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, out, out_kind, st);
     return run_gemm(fmt, A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, out, out_kind, st);
 }
 
 static int prof_gemm_x(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                        int b_kmajor, const float* sa, const float* sb, void* out, int out_kind, int64_t xf_block,
                        int out_trans, int64_t n_valid, cudaStream_t st) {
+    if (fmt == HALO_FMT_INT8 && K > kI8SliceK) {
+        // sliced products into fp32, then the standalone right transform
+        if (out_trans) return -1;
+        if (t_split.f32.ensure((size_t)M * (size_t)N * 4) != HALO_OK) return (int)cudaErrorMemoryAllocation;
+        {
+            ProfScope ps(PC_GEMM, 2.0 * (double)M * (double)N * (double)K, st);
+            const int r = gemm_i8_split(A, B, M, N, K, a_kmajor, b_kmajor, sa, sb, t_split.f32.p, 0, st);
+            if (r != 0) return r;
+        }
+        ProfScope ps(PC_K4, (double)M * N * (4 + (out_kind == 1 ? 2 : 4)), st);
+        run_rows(t_split.f32.p, HALO_DTYPE_F32, M, N, xf_block, 2, 0, nullptr, nullptr, nullptr, out,
+                 out_kind == 1 ? HALO_DTYPE_BF16 : HALO_DTYPE_F32, nullptr, nullptr, st);
+        return 0;
+    }
     ProfScope ps(PC_GEMM, 2.0 * (double)M * (double)N * (double)K, st);
     int lb = 0;
     while ((int64_t(1) << lb) < xf_block) ++lb;
@@ -512,6 +565,10 @@ extern "C" halo_status halo_qmatmul(int32_t format, const uint8_t* a, int32_t a_
     if (!a || !b || !out || !scale_a || !scale_b) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: null pointer");
     if (!valid_gemm_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad format");
     if (out_kind < 0 || out_kind > 2) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: bad out kind");
+    if (format == HALO_FMT_INT8 && K > kI8SliceK && (out_kind == HALO_OUT_S32 || a_kmajor || b_kmajor))
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "qmatmul: INT8 with K > 131072 needs MN-major operands and a float output (s32 accumulators "
+                    "would overflow; the product is summed in int64 over K slices)");
     const int r = prof_gemm(format, a, b, M, N, K, a_kmajor, b_kmajor, scale_a, scale_b, out, out_kind,
                            (cudaStream_t)stream);
     if (r == -1) return fail(HALO_ERR_INVALID_ARGUMENT, "qmatmul: unsupported shape (strides must be multiples of 16 B)");
@@ -590,10 +647,11 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
                     "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
     if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW && s.granularity != HALO_GRAN_COLUMN)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: tensor, row and column granularity are on the device path");
-    if (s.granularity == HALO_GRAN_ROW && (m % 256 || (s.had_block ? s.had_block : m) > 256 ||
+    if (s.granularity == HALO_GRAN_ROW && (m % 256 || n % 256 || (s.had_block ? s.had_block : m) > 256 ||
                                            !is_pow2(s.had_block ? s.had_block : m)))
         return fail(HALO_ERR_INVALID_ARGUMENT,
-                    "halo layer: row granularity needs in_features % 256 == 0 and a Hadamard block <= 256");
+                    "halo layer: row granularity needs in_features % 256 == 0, out_features % 256 == 0 (the "
+                    "per-row error quantizer of the backward) and a Hadamard block <= 256");
     if (!valid_format(s.format_x) || s.format_x != s.format_w || s.format_x != s.format_e)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: X/W/E formats must agree and be int8, fp8_e4m3 or fp6_e3m2");
     if (s.format_x == HALO_FMT_FP6_E3M2 && s.granularity != HALO_GRAN_TENSOR)
@@ -1338,10 +1396,13 @@ extern "C" halo_status halo_ctx_saved(const halo_ctx* c, const uint8_t** xq, con
 extern "C" halo_status halo_ctx_error_operands(const halo_ctx* c, const uint8_t** ehq, const float** seh,
                                                const uint8_t** eq, const float** se, int64_t* b_pad) {
     if (!c || !c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: no forward context");
+    // row / column granularity: the scale vectors of the last backward
+    // (per token for ROW: b_pad / b floats; per column for COLUMN: out_features)
+    const bool grouped = c->gran != HALO_GRAN_TENSOR;
     if (ehq) *ehq = c->ehq.as<uint8_t>();
-    if (seh) *seh = &c->d()->scale[SEH];
+    if (seh) *seh = grouped ? c->ehs_rows.as<float>() : &c->d()->scale[SEH];
     if (eq) *eq = c->eq.as<uint8_t>();
-    if (se) *se = &c->d()->scale[SE];
+    if (se) *se = grouped ? c->es_rows.as<float>() : &c->d()->scale[SE];
     if (b_pad) *b_pad = c->b_pad;
     return HALO_OK;
 }

@@ -68,6 +68,7 @@ struct ScatterSpec {
 struct ShardScope {
     ShardScope(const ShardSpec* a, const ShardSpec* b, const ScatterSpec* c = nullptr);
     ~ShardScope();
+    static bool active();  // sharded / scattered operands installed on this thread
 };
 // receive buffers recv[i] = [parts][len][cols] fp32 of rank i; maps for slot `slot`
 bool encode_scatter_maps(void* const* recv, int parts, int slot, int64_t len, int64_t cols, CUtensorMap* out);
@@ -167,5 +168,9 @@ void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void
 void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st);
 // out[i] = T(sum_w double(recv[w*n + i]) / world), n % 4 == 0
 void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st);
+// INT8 split-K: acc (+)= part (int64 sum of s32 slices); out = T(double(acc) * (double(*sa) * double(*sb)))
+void run_acc_s64(const int* part, long long* acc, int64_t n, int first, cudaStream_t st);
+void run_epi_s64(const long long* acc, const float* sa, const float* sb, void* out, int dtype, int64_t n,
+                 cudaStream_t st);
 
 }  // namespace halo_b200

@@ -460,6 +460,19 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
                 raise HaloLogicError("backward_regather: no saved forward scales")
             self.ledger.backward_gathers += 1  # served in place: the codes never left
             self.ledger.backward_consumers += 1
+        if self.check_stale:
+            # backward_regather's stale check (hqfsdp.hpp:256-259): the codes
+            # read in place were quantized under the forward's absmax; raise
+            # if any rank's master shard changed since (flag max over ranks)
+            ops = CudaOps()
+            stale = torch.zeros(1, dtype=torch.float32, device=self.params[0].master.device)
+            for p in self.params:
+                am = ops.absmax(p.master, self.block, self.rotate).reshape(1).float()
+                stale = torch.maximum(stale, (am != p.local_absmax.reshape(1).float()).float())
+            if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+                dist.all_reduce(stale, op=dist.ReduceOp.MAX, group=self.group)
+            if float(stale.item()) != 0.0:
+                raise HaloLogicError("backward_regather: saved scales are stale (weights changed since the forward)")
         # G GEMMs stored every rank's fp32 partial rows into their owners'
         # receive slots; once all ranks are past them, each owner takes the
         # rank-order double mean of its rows (hqfsdp.hpp:288-292)

@@ -285,11 +285,15 @@ class SavedContext:
                                             C.byref(bp)))
         dt = code_dtype(layer.fmt)
         b = layer._last_b
+        g = layer.scheme.granularity
+        # scale vectors: per token (ROW), per output column (COLUMN), else one
+        n_se = b if g == GRAN_ROW else layer.out_features if g == GRAN_COLUMN else 1
+        n_seh = bp.value if g == GRAN_ROW else layer.out_features if g == GRAN_COLUMN else 1
         out = {"eq": _from_ptr(eq.value, (b, layer.out_features), dt),
-               "se": _from_ptr(se.value, (1,), torch.float32)}
+               "se": _from_ptr(se.value, (n_se,), torch.float32)}
         if layer.scheme.E.left:
             out["ehq"] = _from_ptr(ehq.value, (bp.value, layer.out_features), dt)
-            out["seh"] = _from_ptr(seh.value, (1,), torch.float32)
+            out["seh"] = _from_ptr(seh.value, (n_seh,), torch.float32)
         return out
 
     def check(self):

@@ -37,6 +37,8 @@ class HaloMLP:
         # SwiGLU forward fused with the down projection's absmax pass
         # (halo_swiglu_forward_absmax, bit-exact; off: measured slower, see DESIGN)
         self.fuse_fwd = os.environ.get("HALO_MLP_FUSE_FWD", "0") == "1"
+        # tests: a dict here collects the step's intermediate tensors
+        self.trace = None
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         g = self.gate.forward(x, self.ctx[0])
@@ -50,7 +52,10 @@ class HaloMLP:
         else:
             check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
         self._act = (g, u)
-        return self.down.forward(h, self.ctx[2])
+        y = self.down.forward(h, self.ctx[2])
+        if self.trace is not None:
+            self.trace.update(g=g, u=u, h=h, y=y)
+        return y
 
     def backward(self, dy: torch.Tensor, need_grad_w: bool = True):
         """Returns (dx, (dW_gate, dW_up, dW_down))."""
@@ -70,6 +75,8 @@ class HaloMLP:
         dx = torch.empty_like(bg.e_x)
         check(lib().halo_add(halo._ptr(bg.e_x), halo._ptr(bu.e_x), halo._ptr(dx), DTYPE_BF16, dx.numel(),
                              halo._stream()))
+        if self.trace is not None:
+            self.trace.update(dh=bd.e_x, dg=dg, du=du, ex_gate=bg.e_x, ex_up=bu.e_x)
         return dx, (bg.grad_w, bu.grad_w, bd.grad_w)
 
     def gemm_ops(self, tokens: int) -> float:

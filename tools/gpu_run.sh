@@ -32,6 +32,22 @@ for w in $what; do
     prof_gemm)
       timeout 600 ncu --set full --clock-control none -k regex:k_gemm -s 3 -c 3 \
         -f -o gpurun_out/prof_gemm python tools/bench_kernels.py gemm --reps 1 > gpurun_out/prof_gemm.log 2>&1 ;;
+    cpuref_cfg1)
+      # one host core, ~9 min: runs in the background while the GPU work proceeds
+      (timeout 1500 taskset -c 0 python tools/cpu_ref_cfg1.py > gpurun_out/cpu_ref_cfg1.json 2> gpurun_out/cpu_ref_cfg1.err) &
+      CPUREF_PID=$! ;;
+    bench_cfg1)
+      timeout 600 python bench.py --config cfg1 > gpurun_out/bench_cfg1.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_cfg1.log ;;
+    traffic)
+      timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+        -k regex:k_gemm --csv --log-file gpurun_out/gemm_traffic.csv python tools/prof_step.py 1 > gpurun_out/traffic.log 2>&1
+      echo "traffic rc=$?" >> gpurun_out/traffic.log ;;
+    sanitize)
+      for tool in memcheck racecheck synccheck; do
+        timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_small.py \
+          > gpurun_out/sanitize_$tool.log 2>&1
+        echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log
+      done ;;
     launches)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python tools/prof_step.py 2 > gpurun_out/launches.log 2>&1
@@ -43,6 +59,7 @@ for w in $what; do
         -f -o gpurun_out/prof_fwht python tools/prof_step.py 1 > gpurun_out/prof_fwht.log 2>&1 ;;
   esac
 done
+if [ -n "${CPUREF_PID:-}" ]; then wait $CPUREF_PID; fi
 # keep reps small enough to travel back (64 MiB cap): export raw CSV, drop big reps
 for r in gpurun_out/*.ncu-rep; do
   [ -f "$r" ] || continue
