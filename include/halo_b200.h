@@ -311,6 +311,17 @@ HALO_API halo_status halo_ipc_close(void* ptr);
 HALO_API halo_status halo_peer_sync(void* const* mailboxes, int32_t world, int32_t rank, uint32_t epoch,
                                     const float* amax_in, float* amax_out, halo_stream_t stream);
 
+/* ------------------------------------------------ optimizer (HQ-FSDP) */
+/* AdamWT::step for one parameter (trainer.hpp:104-160), e.g. this rank's
+ * row shard of a master weight in the HQ-FSDP training loop
+ * (hqfsdp.hpp:340-411): m, v (fp32 state, n each) and param (bf16 or fp32)
+ * updated in place from grad (bf16 or fp32) in IEEE double as the reference
+ * writes it; lr = lr_at(t), bc1 = 1 - beta1^t, bc2 = 1 - beta2^t (:127-131).
+ * n % 4 == 0; 16 B aligned pointers. */
+HALO_API halo_status halo_adamw_step(void* param, int32_t p_dtype, const void* grad, int32_t g_dtype, float* m,
+                                     float* v, int64_t n, double lr, double beta1, double beta2, double eps,
+                                     double weight_decay, double bc1, double bc2, halo_stream_t stream);
+
 /* ------------------------------------------------------------- profiling */
 /* Kernel classes: 0 K1 row-FWHT+quantize, 1 K2 column-FWHT+dual quantize,
  * 2 K3 tcgen05 GEMM, 3 K4 output un-rotation, 4 elementwise glue.

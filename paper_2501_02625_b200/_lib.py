@@ -152,6 +152,8 @@ def lib():
                "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
                "halo_reduce_scatter_shard"):
         getattr(L, fn).restype = C.c_int
+    L.halo_adamw_step.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _i64] + [C.c_double] * 7 + [_vp]
+    L.halo_adamw_step.restype = C.c_int
     L.halo_profile_enable.argtypes = [C.c_int]
     L.halo_profile_read.argtypes = [C.POINTER(Profile)]
     for fn in ("halo_swiglu_forward", "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
@@ -200,4 +202,5 @@ EXPORTS = (
     "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
     "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
     "halo_reduce_scatter_shard", "halo_rotate_quantize_amax", "halo_swiglu_forward_absmax",
+    "halo_adamw_step",
 )

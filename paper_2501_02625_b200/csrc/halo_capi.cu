@@ -399,6 +399,13 @@ static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows,
                                         unsigned* amax_word, float* scale_out, unsigned* err, cudaStream_t st,
                                         bool have_amax = false) {
     const double n = (double)rows * (double)cols;
+    if (!supplied && !have_amax && rotate) {
+        // both phases in one launch, the re-read served from L2 (fwht3.cu v5)
+        ProfScope ps(PC_K1, n * (dt_bytes(dt) + 1), st);
+        if (rows_fused(fmt, dt, a, rows * cols, B, amax_word, codes, err, scale_out, st))
+            return cuda_check("rotate_quantize");
+        ps.r.work = 0.0;  // not applicable: nothing launched, the two-phase path books the bytes
+    }
     if (!supplied && !have_amax) {
         cudaMemsetAsync(amax_word, 0, sizeof(unsigned), st);
         ProfScope ps(PC_K1, 0.0, st);  // phase A: its bytes are booked on phase B
@@ -1543,6 +1550,20 @@ extern "C" halo_status halo_add(const void* a, const void* b, void* out, int32_t
     ProfScope ps(PC_GLUE, (double)n * 3 * dt_bytes(dtype), st);
     run_add(a, b, out, dtype, n, st);
     return cuda_check("add");
+}
+
+extern "C" halo_status halo_adamw_step(void* param, int32_t p_dtype, const void* grad, int32_t g_dtype, float* m,
+                                       float* v, int64_t n, double lr, double beta1, double beta2, double eps,
+                                       double weight_decay, double bc1, double bc2, halo_stream_t stream) {
+    if (!param || !grad || !m || !v) return fail(HALO_ERR_INVALID_ARGUMENT, "adamw: null pointer");
+    if (!valid_dtype(p_dtype) || !valid_dtype(g_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "adamw: bad dtype");
+    if (n < 0 || n % 4) return fail(HALO_ERR_INVALID_ARGUMENT, "adamw: n must be a non-negative multiple of 4");
+    if (!(bc1 > 0.0) || !(bc2 > 0.0)) return fail(HALO_ERR_INVALID_ARGUMENT, "adamw: bias corrections must be > 0");
+    if (n == 0) return HALO_OK;
+    ProfScope ps(PC_GLUE, (double)n * (2 * dt_bytes(p_dtype) + dt_bytes(g_dtype) + 16), (cudaStream_t)stream);
+    run_adamw(param, p_dtype, grad, g_dtype, m, v, n, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
+              (cudaStream_t)stream);
+    return cuda_check("adamw");
 }
 
 extern "C" halo_status halo_profile_enable(int on) {

@@ -24,6 +24,11 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
               uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
               float* scale_rot_out, float* scale_plain_out, cudaStream_t st);
 
+// K1 phases A + B in one cooperative launch (fwht3.cu v5); false = not
+// applicable (n % 1024, B outside 2..256, alignment), run the two phases
+bool rows_fused(int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, uint8_t* codes,
+                unsigned* err, float* scale_out, cudaStream_t st);
+
 // un-rotated absmax / quantize
 void run_plain(const void* in, int in_dtype, int64_t n, int mode, int fmt, unsigned* amax, const float* supplied,
                uint8_t* codes, unsigned* err, float* scale_out, cudaStream_t st);
@@ -168,6 +173,9 @@ void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void
 void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st);
 // out[i] = T(sum_w double(recv[w*n + i]) / world), n % 4 == 0
 void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st);
+// AdamWT::step on one parameter (trainer.hpp:104-160), n % 4 == 0
+void run_adamw(void* p, int p_dtype, const void* g, int g_dtype, float* m, float* v, int64_t n, double lr, double b1,
+               double b2, double eps, double wd, double bc1, double bc2, cudaStream_t st);
 // INT8 split-K: acc (+)= part (int64 sum of s32 slices); out = T(double(acc) * (double(*sa) * double(*sb)))
 void run_acc_s64(const int* part, long long* acc, int64_t n, int first, cudaStream_t st);
 void run_epi_s64(const long long* acc, const float* sa, const float* sb, void* out, int dtype, int64_t n,
