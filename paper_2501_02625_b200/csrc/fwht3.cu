@@ -28,7 +28,6 @@
 //     absmax word (every FWHT output of a block containing Inf/NaN is
 //     non-finite), so no separate finiteness pass is needed.
 #include <cstdlib>
-#include <unordered_map>
 
 #include "common.cuh"
 #include "halo_internal.h"
@@ -575,234 +574,6 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
         core.row_flush(seg0, err);
     }
     core.reduce(absmax, err);
-}
-
-// ---------------------------- v5: both phases in one persistent launch
-// A per-tensor scale needs the global absmax before any code (quantize.hpp:
-// 202-280), which the v4 path pays with two launches and two HBM reads of
-// the input.  v5 runs phase A and phase B in ONE cooperative launch with
-// every CTA resident: each warp owns a CONTIGUOUS range of 1024-element
-// chunks, reads it ascending in phase A (absmax), the grid meets at a
-// device-wide barrier (per-CTA partial maxima, no atomics, no memset), and
-// phase B walks the same range DESCENDING -- the chunks phase A read last
-// are the ones still in the 126 MB L2, so phase B's re-read is served from
-// L2 for tensors up to about the L2 size and for the most recent part of
-// larger ones.  Same RowsCore arithmetic as v4: codes / scale bit-identical.
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-template <int LB, typename InT, int FMT>
-__global__ void __launch_bounds__(128) k_rows_v5(const __grid_constant__ CUtensorMap tm, int64_t n, float norm,
-                                                 float* part, unsigned* bar, unsigned* absmax_out,
-                                                 uint8_t* __restrict__ codes, unsigned* err, float* scale_out) {
-    using C = V4Cfg<InT>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ float red[C::WARPS];
-    __shared__ unsigned amax_s;
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int k = l >> 3, p = l & 7;
-    uint8_t* stages = smem + w * C::STAGES * C::STAGE_BYTES;
-    float4* xch = reinterpret_cast<float4*>(smem + C::WARPS * C::STAGES * C::STAGE_BYTES + w * C::XCH_BYTES);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::WARPS * (C::STAGES * C::STAGE_BYTES + C::XCH_BYTES)) +
-                     w * C::STAGES;
-    const int64_t nchunks = (n + 1023) >> 10;
-    const int64_t G = (int64_t)gridDim.x * C::WARPS;
-    const int64_t gw = (int64_t)blockIdx.x * C::WARPS + w;
-    const int64_t lo = gw * nchunks / G, hi = (gw + 1) * nchunks / G;  // this warp's contiguous range
-    const int64_t cnt = hi - lo;
-    if (l == 0) {
-        if (w == 0) tma_prefetch_desc(&tm);
-        for (int s = 0; s < C::STAGES; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    // the ring streams 2*cnt chunk reads: phase A's lo..hi-1, then phase
-    // B's hi-1..lo; slot/parity keep running across the phase boundary
-    auto chunk_of = [&](int64_t j) { return j < cnt ? lo + j : hi - 1 - (j - cnt); };
-    auto issue = [&](int64_t j) {
-        const int s = (int)(j % C::STAGES);
-        mbar_expect_tx(&bars[s], C::STAGE_BYTES);
-        tma_load_2d(stages + s * C::STAGE_BYTES, &tm, &bars[s], 0, (int)(chunk_of(j) * C::CHUNK_ROWS));
-    };
-    if (l == 0)
-        for (int64_t j = 0; j < C::STAGES && j < cnt; ++j) issue(j);
-    __syncwarp();
-
-    // ---------------- phase A: absmax of the rotated range
-    {
-        RowsCore<LB, 0, V3_ABSMAX, false, float> ca;
-        ca.init(nullptr, nullptr, norm, err, nullptr);
-        for (int64_t j = 0; j < cnt; ++j) {
-            const int s = (int)(j % C::STAGES);
-            mbar_wait(&bars[s], (uint32_t)(j / C::STAGES) & 1u);
-            float2 v[16];
-            v4_read<InT>(stages + s * C::STAGE_BYTES, k, p, v);
-            ca.phase1(v);
-            __syncwarp();
-            // refills never run ahead into phase B: its first chunk is only
-            // known to be needed once the barrier is passed (no deadlock on a
-            // ring slot the barrier waits behind)
-            if (l == 0 && j + C::STAGES < cnt) issue(j + C::STAGES);
-            ca.finish(v, chunk_of(j) << 10, n, k, p, xch, nullptr, (float*)nullptr);
-        }
-        float m = ca.amax;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max3nan(m, __shfl_xor_sync(0xffffffffu, m, o), 0.f);
-        if (l == 0) red[w] = m;
-    }
-    __syncthreads();
-    // ---------------- grid barrier on the per-CTA partial maxima
-    if (threadIdx.x == 0) {
-        float m = red[0];
-#pragma unroll
-        for (int i = 1; i < C::WARPS; ++i) m = max3nan(m, red[i], 0.f);
-        part[blockIdx.x] = m * norm;  // max(fl(|x|*norm)) == fl(max|x|*norm)
-        __threadfence();
-        atomicAdd(&bar[0], 1u);
-        while (ld_acquire_gpu(&bar[0]) < gridDim.x) __nanosleep(64);
-    }
-    __syncthreads();
-    {
-        float m = 0.f;
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) m = max3nan(m, __ldcg(part + i), 0.f);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max3nan(m, __shfl_xor_sync(0xffffffffu, m, o), 0.f);
-        if (l == 0) red[w] = m;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float t = red[0];
-#pragma unroll
-            for (int i = 1; i < C::WARPS; ++i) t = max3nan(t, red[i], 0.f);
-            const float a = fabsf(t);
-            amax_s = __float_as_uint(a);
-            if (blockIdx.x == 0) {
-                *absmax_out = amax_s;
-                if (!(t <= 3.402823466e38f)) atomicOr(err, ERRF_NONFINITE);
-            }
-            // depart: the last CTA out re-arms the barrier for the next launch
-            if (atomicAdd(&bar[1], 1u) == gridDim.x - 1) {
-                bar[0] = 0u;
-                bar[1] = 0u;
-            }
-        }
-        __syncthreads();
-    }
-    // ---------------- phase B: quantize, range walked backwards (L2-warm first)
-    RowsCore<LB, FMT, V3_QUANT, false, float> cb;
-    cb.init(&amax_s, nullptr, norm, err, scale_out);
-    if (l == 0)
-        for (int64_t j = cnt; j < cnt + C::STAGES && j < 2 * cnt; ++j) issue(j);
-    __syncwarp();
-    for (int64_t j = cnt; j < 2 * cnt; ++j) {
-        const int s = (int)(j % C::STAGES);
-        mbar_wait(&bars[s], (uint32_t)(j / C::STAGES) & 1u);
-        const int64_t c = chunk_of(j);
-        float2 v[16];
-        v4_read<InT>(stages + s * C::STAGE_BYTES, k, p, v);
-        cb.phase1(v);
-        __syncwarp();
-        if (l == 0 && j + C::STAGES < 2 * cnt) issue(j + C::STAGES);
-        cb.finish(v, c << 10, n, k, p, xch, codes, (float*)nullptr);
-    }
-}
-
-namespace {
-// per-stream barrier words + partial maxima of the v5 launches (zeroed once;
-// every launch leaves its barrier re-armed)
-struct V5Scratch {
-    void* p = nullptr;
-    size_t bytes = 0;
-};
-thread_local std::unordered_map<cudaStream_t, V5Scratch> t_v5;
-
-template <int LB, typename InT, int FMT>
-bool launch_v5(const InT* in, int64_t n, unsigned* amax, uint8_t* codes, unsigned* err, float* sout, cudaStream_t st) {
-    using C = V4Cfg<InT>;
-    auto kern = k_rows_v5<LB, InT, FMT>;
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * C::WARPS, C::SMEM);
-        if (per_sm < 1) return false;
-    }
-    const int64_t nchunks = (n + 1023) / 1024;
-    int64_t grid = (int64_t)num_sms() * per_sm;
-    // at least STAGES chunks per warp keeps the ring useful; small tensors
-    // get fewer CTAs (still all resident)
-    const int64_t want = (nchunks + C::WARPS * C::STAGES - 1) / (C::WARPS * C::STAGES);
-    if (grid > want) grid = want < 1 ? 1 : want;
-    V5Scratch& sc = t_v5[st];
-    const size_t need = 256 + (size_t)grid * sizeof(float);
-    if (sc.bytes < need) {
-        if (sc.p) {
-            cudaStreamSynchronize(st);
-            cudaFree(sc.p);
-        }
-        sc.p = nullptr;
-        sc.bytes = 0;
-        if (cudaMalloc(&sc.p, need) != cudaSuccess) return false;
-        cudaMemsetAsync(sc.p, 0, need, st);
-        sc.bytes = need;
-    }
-    unsigned* bar = static_cast<unsigned*>(sc.p);
-    float* part = reinterpret_cast<float*>(static_cast<uint8_t*>(sc.p) + 256);
-    CUtensorMap tm;
-    if (!encode_2d_sw128(&tm, sizeof(InT) == 4 ? 0 : 1, in, C::ROW_ELEMS, n / C::ROW_ELEMS, C::CHUNK_ROWS)) return false;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(32 * C::WARPS);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the grid barrier cannot deadlock
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, tm, n, hadamard_norm(int64_t(1) << LB), part, bar, amax, codes, err,
-                              sout) == cudaSuccess;
-}
-
-int k1_fused_on() {
-    static const int on = [] {
-        const char* e = getenv("HALO_K1_FUSED");
-        return e ? atoi(e) : 1;
-    }();
-    return on;
-}
-}  // namespace
-
-// K1 (phase A + phase B) in one launch: per-tensor absmax scale, B = 2^lb
-// <= 256, bf16 / fp32 input, INT8 / E4M3 / E3M2 codes.  False: not
-// applicable (the caller runs the two-launch path).
-bool rows_fused(int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, uint8_t* codes,
-                unsigned* err, float* sout, cudaStream_t st) {
-    if (!k1_fused_on() || k1_version() < 4) return false;
-    if (B < 2 || B > 256 || (B & (B - 1)) || n % 1024) return false;
-    if ((uintptr_t)in % 16 || (uintptr_t)codes % 32) return false;
-    int lb = 0;
-    while ((int64_t(1) << lb) < B) ++lb;
-#define HALO_V5(LBv)                                                                                              \
-    case LBv:                                                                                                     \
-        if (in_dtype == DT_BF16) {                                                                                \
-            auto pi = static_cast<const __nv_bfloat16*>(in);                                                      \
-            if (fmt == FMT_INT8) return launch_v5<LBv, __nv_bfloat16, FMT_INT8>(pi, n, amax, codes, err, sout, st); \
-            if (fmt == FMT_E3M2) return launch_v5<LBv, __nv_bfloat16, FMT_E3M2>(pi, n, amax, codes, err, sout, st); \
-            return launch_v5<LBv, __nv_bfloat16, FMT_E4M3>(pi, n, amax, codes, err, sout, st);                    \
-        } else {                                                                                                  \
-            auto pf = static_cast<const float*>(in);                                                              \
-            if (fmt == FMT_INT8) return launch_v5<LBv, float, FMT_INT8>(pf, n, amax, codes, err, sout, st);       \
-            if (fmt == FMT_E3M2) return launch_v5<LBv, float, FMT_E3M2>(pf, n, amax, codes, err, sout, st);       \
-            return launch_v5<LBv, float, FMT_E4M3>(pf, n, amax, codes, err, sout, st);                            \
-        }
-    switch (lb) {
-        HALO_V5(1) HALO_V5(2) HALO_V5(3) HALO_V5(4) HALO_V5(5) HALO_V5(6) HALO_V5(7) HALO_V5(8)
-    default: return false;
-    }
-#undef HALO_V5
 }
 
 // ------------------------------------------ SwiGLU forward + K1 phase A

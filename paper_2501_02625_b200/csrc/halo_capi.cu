@@ -399,13 +399,6 @@ static halo_status rotate_quantize_impl(const void* a, int32_t dt, int64_t rows,
                                         unsigned* amax_word, float* scale_out, unsigned* err, cudaStream_t st,
                                         bool have_amax = false) {
     const double n = (double)rows * (double)cols;
-    if (!supplied && !have_amax && rotate) {
-        // both phases in one launch, the re-read served from L2 (fwht3.cu v5)
-        ProfScope ps(PC_K1, n * (dt_bytes(dt) + 1), st);
-        if (rows_fused(fmt, dt, a, rows * cols, B, amax_word, codes, err, scale_out, st))
-            return cuda_check("rotate_quantize");
-        ps.r.work = 0.0;  // not applicable: nothing launched, the two-phase path books the bytes
-    }
     if (!supplied && !have_amax) {
         cudaMemsetAsync(amax_word, 0, sizeof(unsigned), st);
         ProfScope ps(PC_K1, 0.0, st);  // phase A: its bytes are booked on phase B

@@ -24,11 +24,6 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
               uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
               float* scale_rot_out, float* scale_plain_out, cudaStream_t st);
 
-// K1 phases A + B in one cooperative launch (fwht3.cu v5); false = not
-// applicable (n % 1024, B outside 2..256, alignment), run the two phases
-bool rows_fused(int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, uint8_t* codes,
-                unsigned* err, float* scale_out, cudaStream_t st);
-
 // un-rotated absmax / quantize
 void run_plain(const void* in, int in_dtype, int64_t n, int mode, int fmt, unsigned* amax, const float* supplied,
                uint8_t* codes, unsigned* err, float* scale_out, cudaStream_t st);

@@ -100,9 +100,9 @@ class CudaOps:
         from . import halo
         return halo.rotate_absmax(a, had_block, rotate)
 
-    def quantize(self, a: torch.Tensor, had_block: int, fmt: int, scale: torch.Tensor, rotate: bool):
+    def quantize(self, a: torch.Tensor, had_block: int, fmt: int, scale: torch.Tensor, rotate: bool, out=None):
         from . import halo
-        codes, _ = halo.rotate_quantize(a, had_block, fmt, scale=scale, rotate=rotate)
+        codes, _ = halo.rotate_quantize(a, had_block, fmt, scale=scale, rotate=rotate, out=out)
         return codes
 
 
@@ -192,8 +192,13 @@ def quantized_all_gather(p: ShardedParam, apply_hadamard: bool, ledger: CommLedg
 def _gather_with_scale(p, apply_hadamard, ledger, had_block, group, ops, out=None):
     """hqfsdp.hpp:184-196: quantize the local rotated rows under the agreed
     scale, gather the codes, book the bytes."""
-    codes = ops.quantize(p.master, had_block, p.format, p.global_scale, apply_hadamard)
-    full = _gather(codes, group, out)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1 and out is not None and isinstance(ops, CudaOps):
+        # a world of one: the local codes ARE the gathered tensor
+        full = ops.quantize(p.master, had_block, p.format, p.global_scale, apply_hadamard, out=out.view(p.master.shape))
+    else:
+        codes = ops.quantize(p.master, had_block, p.format, p.global_scale, apply_hadamard)
+        full = _gather(codes, group, out)
     elems = full.numel()
     ledger.record(ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
     ledger.bf16_gather_payload += 2 * elems
@@ -201,12 +206,20 @@ def _gather_with_scale(p, apply_hadamard, ledger, had_block, group, ops, out=Non
 
 
 def backward_regather(p: ShardedParam, apply_hadamard: bool, ledger: CommLedger, check_stale: bool = True,
-                      had_block: int = 0, group=None, ops=None, out: torch.Tensor | None = None):
-    """Backward gather under the saved forward scale (hqfsdp.hpp:243-266)."""
+                      had_block: int = 0, group=None, ops=None, out: torch.Tensor | None = None,
+                      stale_flag: torch.Tensor | None = None):
+    """Backward gather under the saved forward scale (hqfsdp.hpp:243-266).
+    stale_flag (device fp32 [1]): the stale-weight check is accumulated
+    there without a host sync (the caller reduces and tests it once, see
+    check_stale_flag); otherwise it raises here."""
     if not p.scales_valid:
         raise HaloLogicError("backward_regather: no saved forward scales")
     ops = ops or CudaOps()
-    if check_stale:
+    if check_stale and stale_flag is not None:
+        am = ops.absmax(p.master, had_block, apply_hadamard).reshape(1).float()
+        saved = p.local_absmax[p.rank].reshape(1).float() if p.local_absmax.numel() > 1 else p.local_absmax.reshape(1)
+        torch.maximum(stale_flag, (am != saved).float(), out=stale_flag)
+    elif check_stale:
         am = float(ops.absmax(p.master, had_block, apply_hadamard).reshape(-1)[0])
         stale = torch.tensor([1.0 if am != float(p.local_absmax[p.rank]) else 0.0])
         if dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -218,22 +231,40 @@ def backward_regather(p: ShardedParam, apply_hadamard: bool, ledger: CommLedger,
     return _gather_with_scale(p, apply_hadamard, ledger, had_block, group, ops, out)
 
 
+def check_stale_flag(stale_flag: torch.Tensor, group=None):
+    """Raise HaloLogicError if any rank's accumulated stale flag is set
+    (backward_regather's check, hqfsdp.hpp:256-259, reduced once)."""
+    f = stale_flag.clone()
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+    if float(f.item()) != 0.0:
+        raise HaloLogicError("backward_regather: saved scales are stale (weights changed since the forward gather)")
+
+
 def reduce_scatter_grads(grad: torch.Tensor, p: ShardedParam, ledger: CommLedger, group=None) -> torch.Tensor:
     """hqfsdp.hpp:271-300: mean over ranks, scattered by row range.  `grad`
     is this rank's full (rows x cols) gradient; padding rows are zero and the
     returned shard has shard_rows rows (rows past full_rows stay zero)."""
     if tuple(grad.shape) != (p.full_rows, p.cols):
         raise ValueError("reduce_scatter_grads: gradient shape mismatch")
-    padded = torch.zeros((p.shard_rows * p.world, p.cols), dtype=grad.dtype, device=grad.device)
-    padded[: p.full_rows] = grad
-    out = torch.empty((p.shard_rows, p.cols), dtype=grad.dtype, device=grad.device)
     world = p.world
+    if p.pad_rows == 0:
+        if world == 1:  # a world of one owns every row: the mean is the gradient itself
+            ledger.record(ledger.reduce_scatter, 2 * grad.numel(), world)
+            return grad
+        padded = grad.contiguous()
+    else:
+        padded = torch.zeros((p.shard_rows * p.world, p.cols), dtype=grad.dtype, device=grad.device)
+        padded[: p.full_rows] = grad
+    out = torch.empty((p.shard_rows, p.cols), dtype=grad.dtype, device=grad.device)
     if world == 1:
         out.copy_(padded)
     elif dist.get_backend(group) == "nccl":
         dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=group)
         out.div_(world)
     else:  # gloo has no reduce_scatter: all-reduce then slice
+        if padded is grad:
+            padded = grad.clone()  # never sum into the caller's gradient
         dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
         out.copy_(padded[p.rank * p.shard_rows:(p.rank + 1) * p.shard_rows])
         out.div_(world)

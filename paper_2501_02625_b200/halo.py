@@ -121,7 +121,7 @@ def padded_batch(b: int, had_block: int) -> int:
 # --------------------------------------------------------------- primitives
 
 def rotate_quantize(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, scale: torch.Tensor | None = None,
-                    rotate: bool = True):
+                    rotate: bool = True, out: torch.Tensor | None = None):
     """``quantize(transform_right(a, spec), fmt, tensor, scales)`` fused.
 
     Returns ``(codes, scale)``: codes int8 (INT8) or uint8 OCP-E4M3 bytes of
@@ -129,7 +129,9 @@ def rotate_quantize(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, scale:
     used verbatim (quantize.hpp:259-266)."""
     _need_cuda(a, scale)
     rows, cols = a.shape
-    codes = torch.empty((rows, cols), dtype=code_dtype(fmt), device=a.device)
+    codes = torch.empty((rows, cols), dtype=code_dtype(fmt), device=a.device) if out is None else out
+    if tuple(codes.shape) != (rows, cols) or codes.element_size() != 1 or not codes.is_contiguous():
+        raise ValueError("rotate_quantize: out must be a contiguous (rows x cols) code buffer")
     s_out = scale.clone() if scale is not None else torch.empty(1, dtype=torch.float32, device=a.device)
     check(lib().halo_rotate_quantize(_ptr(a), _dt(a), rows, cols, had_block if rotate else -1, fmt,
                                      _ptr(scale), _ptr(codes), _ptr(s_out), _stream()))

@@ -21,6 +21,9 @@ for w in $what; do
       timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log ;;
     kern)
       timeout 600 python tools/bench_kernels.py > gpurun_out/kern.log 2>&1; echo "kern rc=$?" >> gpurun_out/kern.log ;;
+    k1ab)
+      timeout 600 python tools/bench_kernels.py k1 > gpurun_out/k1_fused.log 2>&1
+      HALO_K1_FUSED=0 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/k1_twophase.log 2>&1 ;;
     kern_v2)
       HALO_K1_VERSION=2 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/kern_v2.log 2>&1 ;;
     prof_k1)
