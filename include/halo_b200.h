@@ -49,7 +49,8 @@ typedef enum halo_status {
     HALO_ERR_NUMERIC = 2,
     HALO_ERR_LOGIC = 3,
     HALO_ERR_CUDA = 4,
-    HALO_ERR_NCCL = 5
+    HALO_ERR_NCCL = 5,
+    HALO_ERR_IO = 6 /* io_error, tensor_io.hpp:25-27 */
 } halo_status;
 
 /* NumericFormat ids, quantize.hpp:22-29 (FP6/MX/BF16/IDENTITY emulation is
@@ -310,6 +311,22 @@ HALO_API halo_status halo_ipc_close(void* ptr);
  * hqfsdp.hpp:172-196 and orders shard writes before peer reads. */
 HALO_API halo_status halo_peer_sync(void* const* mailboxes, int32_t world, int32_t rank, uint32_t epoch,
                                     const float* amax_in, float* amax_out, halo_stream_t stream);
+
+/* ------------------------------------------------ quantized tensor files */
+/* write_quantized_tensor / read_quantized_tensor (quantize.hpp:405-474) in
+ * the reference's HALT container (tensor_io.hpp:1-135): a file written here
+ * is read by the reference and vice versa.  HOST buffers in the device code
+ * layouts (INT8 bytes, OCP E4M3 bytes, E3M2 codes in bits 7:2); granularity
+ * HALO_GRAN_TENSOR (1 scale), _ROW (rows), _COLUMN (cols).  FP8 / FP6 codes
+ * travel as f32 grid values (the reference's QF32 payload); reading a value
+ * off the grid, a block / mx granularity or an emulation-only format fails
+ * with HALO_ERR_IO. */
+HALO_API halo_status halo_quantized_tensor_write(const char* path, int32_t format, int32_t granularity, int64_t rows,
+                                                 int64_t cols, const uint8_t* codes, const float* scales,
+                                                 int64_t n_scales);
+HALO_API halo_status halo_quantized_tensor_info(const char* path, int32_t* format, int32_t* granularity,
+                                                int64_t* rows, int64_t* cols, int64_t* n_scales);
+HALO_API halo_status halo_quantized_tensor_read(const char* path, uint8_t* codes, float* scales);
 
 /* ------------------------------------------------ optimizer (HQ-FSDP) */
 /* AdamWT::step for one parameter (trainer.hpp:104-160), e.g. this rank's

@@ -369,3 +369,28 @@ def ref_inject_outliers(a, channels, mag, axis_rows=False):
 
 def ref_time_linear(level, fmt, block, b, m, n, threads=1):
     return ref().ref_time_linear(level, fmt, block, b, m, n, threads)
+
+
+def ref_write_quantized(path, codes, scales, fmt, gran=0):
+    """The reference's write_quantized_tensor (quantize.hpp:405-430)."""
+    codes, scales = f32(codes), f32(np.atleast_1d(scales))
+    L = ref()
+    L.ref_write_quantized.argtypes = [C.c_char_p, C.c_int, C.c_int, _ll, _ll, _f32p, _f32p, _ll]
+    _chk(L, L.ref_write_quantized(str(path).encode(), fmt, gran, codes.shape[0], codes.shape[1], codes, scales,
+                                  scales.size))
+
+
+def ref_read_quantized(path):
+    """The reference's read_quantized_tensor (quantize.hpp:432-474) ->
+    (codes as float values, scales, fmt, granularity kind)."""
+    L = ref()
+    L.ref_read_quantized_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int)] * 2 + [C.POINTER(_ll)] * 3
+    L.ref_read_quantized.argtypes = [C.c_char_p, _f32p, _f32p]
+    f, g = C.c_int(), C.c_int()
+    r, c, n = _ll(), _ll(), _ll()
+    _chk(L, L.ref_read_quantized_info(str(path).encode(), C.byref(f), C.byref(g), C.byref(r), C.byref(c),
+                                      C.byref(n)))
+    codes = np.zeros((r.value, c.value), np.float32)
+    scales = np.zeros(n.value, np.float32)
+    _chk(L, L.ref_read_quantized(str(path).encode(), codes, scales))
+    return codes, scales, f.value, g.value

@@ -297,4 +297,40 @@ double ref_time_linear(int level, int fmt, long long block, long long b, long lo
     return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// write_quantized_tensor / read_quantized_tensor (quantize.hpp:405-474):
+// codes as the reference's float code values, granularity kind 0/1/2
+int ref_write_quantized(const char* path, int fmt, int gran, long long rows, long long cols, const float* codes,
+                        const float* scales, long long nscales) {
+    return guard([&] {
+        QuantizedTensor q;
+        q.format = static_cast<NumericFormat>(fmt);
+        q.granularity.kind = static_cast<GranularityKind>(gran);
+        q.rows = rows;
+        q.cols = cols;
+        q.codes.assign(codes, codes + rows * cols);
+        q.scales.assign(scales, scales + nscales);
+        write_quantized_tensor(std::string(path), q);
+    });
+}
+
+int ref_read_quantized_info(const char* path, int* fmt, int* gran, long long* rows, long long* cols,
+                            long long* nscales) {
+    return guard([&] {
+        const QuantizedTensor q = read_quantized_tensor(std::string(path));
+        *fmt = static_cast<int>(q.format);
+        *gran = static_cast<int>(q.granularity.kind);
+        *rows = q.rows;
+        *cols = q.cols;
+        *nscales = static_cast<long long>(q.scales.size());
+    });
+}
+
+int ref_read_quantized(const char* path, float* codes, float* scales) {
+    return guard([&] {
+        const QuantizedTensor q = read_quantized_tensor(std::string(path));
+        std::memcpy(codes, q.codes.data(), sizeof(float) * q.codes.size());
+        std::memcpy(scales, q.scales.data(), sizeof(float) * q.scales.size());
+    });
+}
+
 } // extern "C"

@@ -17,6 +17,8 @@ HALO_ERR_INVALID_ARGUMENT = 1
 HALO_ERR_NUMERIC = 2
 HALO_ERR_LOGIC = 3
 HALO_ERR_CUDA = 4
+HALO_ERR_NCCL = 5
+HALO_ERR_IO = 6
 
 FMT_INT8 = 0
 FMT_FP8_E4M3 = 1
@@ -32,6 +34,14 @@ class HaloNumericError(ArithmeticError):
 
 class HaloLogicError(RuntimeError):
     """std::logic_error (hqfsdp.hpp:246-259: missing / stale scales)."""
+
+
+class HaloIOError(RuntimeError):
+    """io_error (tensor_io.hpp:25-27): tensor file open / format / truncation."""
+
+
+class HaloNcclError(RuntimeError):
+    """A failed NCCL call of the HQ-FSDP data plane."""
 
 
 class HaloCudaError(RuntimeError):
@@ -154,6 +164,11 @@ def lib():
         getattr(L, fn).restype = C.c_int
     L.halo_adamw_step.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _i64] + [C.c_double] * 7 + [_vp]
     L.halo_adamw_step.restype = C.c_int
+    L.halo_quantized_tensor_write.argtypes = [C.c_char_p, _i32, _i32, _i64, _i64, _vp, _vp, _i64]
+    L.halo_quantized_tensor_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int32)] * 2 + [C.POINTER(_i64)] * 3
+    L.halo_quantized_tensor_read.argtypes = [C.c_char_p, _vp, _vp]
+    for fn in ("halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read"):
+        getattr(L, fn).restype = C.c_int
     L.halo_profile_enable.argtypes = [C.c_int]
     L.halo_profile_read.argtypes = [C.POINTER(Profile)]
     for fn in ("halo_swiglu_forward", "halo_swiglu_backward", "halo_swiglu_backward_absmax", "halo_add", "halo_profile_enable",
@@ -182,6 +197,10 @@ def check(rc: int):
         raise ValueError(msg)
     if rc == HALO_ERR_NUMERIC:
         raise HaloNumericError(msg)
+    if rc == HALO_ERR_IO:
+        raise HaloIOError(msg)
+    if rc == HALO_ERR_NCCL:
+        raise HaloNcclError(msg)
     if rc == HALO_ERR_LOGIC:
         raise HaloLogicError(msg)
     raise HaloCudaError(msg)
@@ -202,5 +221,5 @@ EXPORTS = (
     "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
     "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
     "halo_reduce_scatter_shard", "halo_rotate_quantize_amax", "halo_swiglu_forward_absmax",
-    "halo_adamw_step",
+    "halo_adamw_step", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
 )

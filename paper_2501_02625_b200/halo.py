@@ -246,6 +246,37 @@ def qmatmul(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: to
     return c
 
 
+# ------------------------------------------------------ quantized tensor files
+
+def write_quantized_tensor(path: str, codes: torch.Tensor, scales: torch.Tensor, fmt: int = INT8,
+                           granularity: int = GRAN_TENSOR):
+    """write_quantized_tensor (quantize.hpp:405-430): the reference's HALT
+    file of device codes (any device; copied to the host) and their scales."""
+    c = codes.detach().contiguous().cpu()
+    sc = scales.detach().float().contiguous().cpu()
+    rows, cols = c.shape
+    check(lib().halo_quantized_tensor_write(str(path).encode(), fmt, granularity, rows, cols, c.data_ptr(),
+                                            sc.data_ptr(), sc.numel()))
+
+
+def read_quantized_tensor(path: str, device=None):
+    """read_quantized_tensor (quantize.hpp:432-474) -> (codes, scales, fmt,
+    granularity) in the device code layout (on `device` if given)."""
+    f, g = C.c_int32(), C.c_int32()
+    r, c, n = C.c_int64(), C.c_int64(), C.c_int64()
+    p = str(path).encode()
+    check(lib().halo_quantized_tensor_info(p, C.byref(f), C.byref(g), C.byref(r), C.byref(c), C.byref(n)))
+    fmt = f.value
+    if fmt not in (INT8, FP8_E4M3, FP6_E3M2):
+        raise _lib.HaloIOError("read_quantized_tensor: format has no device code layout")
+    codes = torch.empty((r.value, c.value), dtype=code_dtype(fmt))
+    scales = torch.empty(n.value, dtype=torch.float32)
+    check(lib().halo_quantized_tensor_read(p, codes.data_ptr(), scales.data_ptr()))
+    if device is not None:
+        codes, scales = codes.to(device), scales.to(device)
+    return codes, scales, fmt, g.value
+
+
 # -------------------------------------------------------------------- layer
 
 class SavedContext:
@@ -441,12 +472,15 @@ class HaloLinearLayer:
                                          _DT[self.grad_dtype], _stream()))
         return BackwardResult(e_x, g)
 
-    def export_inference_weights(self):
-        """(WH)_Q codes and scale (halo_linear.hpp:332-338)."""
+    def export_inference_weights(self, path: str | None = None):
+        """(WH)_Q codes and scale (halo_linear.hpp:332-338); with `path`, also
+        written as the reference's quantized tensor file (quantize.hpp:405-430)."""
         codes = torch.empty((self.out_features, self.in_features), dtype=code_dtype(self.fmt), device=self.w.device)
         rows = self.scheme.granularity == GRAN_ROW
         scale = torch.empty(self.out_features if rows else 1, dtype=torch.float32, device=self.w.device)
         check(lib().halo_linear_export_inference_weights(self._h, _ptr(codes), _ptr(scale), _stream()))
+        if path is not None:
+            write_quantized_tensor(path, codes, scale, self.fmt, GRAN_ROW if rows else GRAN_TENSOR)
         return codes, scale
 
     def counters(self) -> Counters:

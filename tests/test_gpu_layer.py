@@ -274,3 +274,20 @@ def test_peft_layer(H, orc, fmt):
     wq, ws = orc.quantize(orc.fwht_rows(W, block), fmt)
     assert s.item() == ws[0]
     assert np.array_equal(codes.cpu().numpy().view(np.uint8), orc.codes_to_bytes(wq, fmt).view(np.uint8))
+
+
+@pytest.mark.parametrize("fmt", [0, 1, 2])
+def test_export_file_reads_in_reference(H, orc, tmp_path, fmt):
+    """export_inference_weights -> quantized tensor file (quantize.hpp:405-430)
+    -> the unmodified reference reader: codes == quantize(transform_right(W))."""
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n, m, block = 256, 512, 256
+    _, W, _ = inputs(orc, 64, m, n, seed=21)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16), H.halo2(fmt, block))
+    path = tmp_path / "w.halt"
+    layer.export_inference_weights(path)
+    vals, scales, f, g = orc.ref_read_quantized(path)
+    want, ws = orc.quantize(orc.fwht_rows(W, block), fmt)
+    assert (f, g) == (fmt, 0)
+    assert np.array_equal(vals, want) and scales[0] == ws[0]

@@ -24,6 +24,14 @@ for w in $what; do
     k1ab)
       timeout 600 python tools/bench_kernels.py k1 > gpurun_out/k1_fused.log 2>&1
       HALO_K1_FUSED=0 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/k1_twophase.log 2>&1 ;;
+    train)
+      timeout 900 python -m pytest tests/test_gpu_train.py -x -q > gpurun_out/pytest_train.log 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_train.log
+      timeout 600 python bench.py --config cfg5 --layers 4 --steps 3 --warmup 3 > gpurun_out/bench_cfg5_l4.log 2>&1
+      echo "rc=$?" >> gpurun_out/bench_cfg5_l4.log ;;
+    cfg5)
+      timeout 1200 python bench.py --config cfg5 --steps 5 --warmup 3 > gpurun_out/bench_cfg5.log 2>&1
+      echo "rc=$?" >> gpurun_out/bench_cfg5.log ;;
     kern_v2)
       HALO_K1_VERSION=2 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/kern_v2.log 2>&1 ;;
     prof_k1)
