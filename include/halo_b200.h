@@ -328,6 +328,29 @@ HALO_API halo_status halo_quantized_tensor_info(const char* path, int32_t* forma
                                                 int64_t* rows, int64_t* cols, int64_t* n_scales);
 HALO_API halo_status halo_quantized_tensor_read(const char* path, uint8_t* codes, float* scales);
 
+/* ------------------------------------------------- transformer block glue */
+/* RMSNorm (rmsnorm.hpp:27-100): y = x * r * gain, r = 1/sqrt(S/D + eps),
+ * S = sum x^2 in double, D = dim if `mean` (Llama) else 1 -- mean = 0,
+ * eps = 0 is the reference's x/||x|| (a zero row then gives non-finite y,
+ * which the next HALO quantizer reports as HALO_ERR_NUMERIC; the reference
+ * raises numeric_error).  x bf16 [rows x dim], gain fp32 [dim], y bf16 or
+ * fp32, rstd (fp32 [rows], may be NULL) saved for the backward. */
+HALO_API halo_status halo_rmsnorm_forward(const void* x, const float* gain, void* y, int32_t y_dtype, float* rstd,
+                                          int64_t rows, int64_t dim, int32_t mean, double eps, halo_stream_t stream);
+/* rmsnorm_backward + rmsnorm_gain_gradient (rmsnorm.hpp:52-100):
+ * dx = r g dy - (r^3 x / D) sum(g dy x) (bf16), dgain = sum_rows dy x r (fp32,
+ * deterministic order); dy bf16 or fp32. */
+HALO_API halo_status halo_rmsnorm_backward(const void* x, const void* dy, int32_t dy_dtype, const float* gain,
+                                           const float* rstd, void* dx, float* dgain, int64_t rows, int64_t dim,
+                                           int32_t mean, halo_stream_t stream);
+/* Rotary embedding over fused qkv rows [rows x heads*head_dim] (bf16): the
+ * first rot_heads heads (q and k) rotated by (cos, sin) pairs of
+ * cos_sin[(row % seq) * head_dim/2 + i] (fp32 interleaved), the rest (v)
+ * copied; backward = the transpose rotation.  in may not alias out. */
+HALO_API halo_status halo_rope_qkv(const void* in, void* out, const float* cos_sin, int64_t rows, int32_t seq,
+                                   int32_t rot_heads, int32_t heads, int32_t head_dim, int32_t backward,
+                                   halo_stream_t stream);
+
 /* ------------------------------------------------ optimizer (HQ-FSDP) */
 /* AdamWT::step for one parameter (trainer.hpp:104-160), e.g. this rank's
  * row shard of a master weight in the HQ-FSDP training loop

@@ -394,3 +394,17 @@ def ref_read_quantized(path):
     scales = np.zeros(n.value, np.float32)
     _chk(L, L.ref_read_quantized(str(path).encode(), codes, scales))
     return codes, scales, f.value, g.value
+
+
+def ref_rmsnorm(x, gain, e):
+    """The reference's rmsnorm_forward / _backward / rmsnorm_gain_gradient
+    (rmsnorm.hpp:27-100) -> (y, dx, dgain); x, e [rows x dim], gain [dim]."""
+    x, e, gain = f32(x), f32(e), f32(np.asarray(gain).reshape(1, -1))
+    rows, dim = x.shape
+    y = np.zeros_like(x)
+    dx = np.zeros_like(x)
+    dg = np.zeros((1, dim), np.float32)
+    L = ref()
+    L.ref_rmsnorm.argtypes = [_f32p, _f32p, _f32p, _ll, _ll, _f32p, _f32p, _f32p]
+    _chk(L, L.ref_rmsnorm(x, gain, e, rows, dim, y, dx, dg))
+    return y, dx, dg[0]

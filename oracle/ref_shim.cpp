@@ -16,6 +16,7 @@
 #include <halo/halo_linear.hpp>
 #include <halo/hqfsdp.hpp>
 #include <halo/quantize.hpp>
+#include <halo/rmsnorm.hpp>
 #include <halo/tensor.hpp>
 
 #include <chrono>
@@ -330,6 +331,17 @@ int ref_read_quantized(const char* path, float* codes, float* scales) {
         const QuantizedTensor q = read_quantized_tensor(std::string(path));
         std::memcpy(codes, q.codes.data(), sizeof(float) * q.codes.size());
         std::memcpy(scales, q.scales.data(), sizeof(float) * q.scales.size());
+    });
+}
+
+// rmsnorm_forward / rmsnorm_backward / rmsnorm_gain_gradient (rmsnorm.hpp:27-100)
+int ref_rmsnorm(const float* x, const float* gain, const float* e, long long rows, long long dim, float* y,
+                float* dx, float* dgain) {
+    return guard([&] {
+        const Tensor X = make(x, rows, dim), G = make(gain, 1, dim), E = make(e, rows, dim);
+        put(rmsnorm_forward(X, &G), y);
+        put(rmsnorm_backward(X, E, &G), dx);
+        put(rmsnorm_gain_gradient(X, E), dgain);
     });
 }
 

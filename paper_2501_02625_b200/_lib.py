@@ -164,6 +164,11 @@ def lib():
         getattr(L, fn).restype = C.c_int
     L.halo_adamw_step.argtypes = [_vp, _i32, _vp, _i32, _vp, _vp, _i64] + [C.c_double] * 7 + [_vp]
     L.halo_adamw_step.restype = C.c_int
+    L.halo_rmsnorm_forward.argtypes = [_vp, _vp, _vp, _i32, _vp, _i64, _i64, _i32, C.c_double, _vp]
+    L.halo_rmsnorm_backward.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _vp]
+    L.halo_rope_qkv.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]
+    for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv"):
+        getattr(L, fn).restype = C.c_int
     L.halo_quantized_tensor_write.argtypes = [C.c_char_p, _i32, _i32, _i64, _i64, _vp, _vp, _i64]
     L.halo_quantized_tensor_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int32)] * 2 + [C.POINTER(_i64)] * 3
     L.halo_quantized_tensor_read.argtypes = [C.c_char_p, _vp, _vp]
@@ -221,5 +226,5 @@ EXPORTS = (
     "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
     "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
     "halo_reduce_scatter_shard", "halo_rotate_quantize_amax", "halo_swiglu_forward_absmax",
-    "halo_adamw_step", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
+    "halo_adamw_step", "halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
 )

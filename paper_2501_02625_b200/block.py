@@ -71,14 +71,95 @@ class HaloLinear:
         return _HaloLinearFn.apply(x, self)
 
 
-def _rmsnorm(x, w, eps=1e-5):
+def _rmsnorm_torch(x, w, eps=1e-5):
     xf = x.float()
     return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w).to(x.dtype)
 
 
-def _rope(t, cos, sin):
-    t1, t2 = t[..., : t.shape[-1] // 2], t[..., t.shape[-1] // 2:]
-    return torch.cat((t1 * cos - t2 * sin, t2 * cos + t1 * sin), dim=-1)
+class _RMSNormFn(torch.autograd.Function):
+    """Llama RMSNorm on the library kernel (halo_rmsnorm_forward / _backward:
+    one pass each; rmsnorm.hpp:27-100 with the 1/dim mean and eps)."""
+
+    @staticmethod
+    def forward(ctx, x, w, eps):
+        from ._lib import DTYPE_BF16, check, lib
+        x = x.contiguous()
+        rows, dim = x.shape
+        y = torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        check(lib().halo_rmsnorm_forward(halo._ptr(x), halo._ptr(w), halo._ptr(y), DTYPE_BF16, halo._ptr(rstd), rows,
+                                         dim, 1, eps, halo._stream()))
+        ctx.save_for_backward(x, w, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        from ._lib import check, lib
+        x, w, rstd = ctx.saved_tensors
+        dy = dy.contiguous()
+        rows, dim = x.shape
+        dx = torch.empty_like(x)
+        dw = torch.empty(dim, dtype=torch.float32, device=x.device)
+        check(lib().halo_rmsnorm_backward(halo._ptr(x), halo._ptr(dy), halo._dt(dy), halo._ptr(w), halo._ptr(rstd),
+                                          halo._ptr(dx), halo._ptr(dw), rows, dim, 1, halo._stream()))
+        return dx, dw, None
+
+
+def _rmsnorm(x, w, eps=1e-5):
+    return _RMSNormFn.apply(x, w, eps)
+
+
+class _RopeQKVFn(torch.autograd.Function):
+    """RoPE on the q and k heads of the fused qkv output (halo_rope_qkv), one
+    pass forward and backward."""
+
+    @staticmethod
+    def forward(ctx, qkv, cs, seq, rot_heads, heads, hd):
+        from ._lib import check, lib
+        qkv = qkv.contiguous()
+        out = torch.empty_like(qkv)
+        check(lib().halo_rope_qkv(halo._ptr(qkv), halo._ptr(out), halo._ptr(cs), qkv.shape[0], seq, rot_heads, heads,
+                                  hd, 0, halo._stream()))
+        ctx.cs, ctx.args = cs, (seq, rot_heads, heads, hd)
+        return out
+
+    @staticmethod
+    def backward(ctx, d):
+        from ._lib import check, lib
+        d = d.contiguous()
+        seq, rot_heads, heads, hd = ctx.args
+        out = torch.empty_like(d)
+        check(lib().halo_rope_qkv(halo._ptr(d), halo._ptr(out), halo._ptr(ctx.cs), d.shape[0], seq, rot_heads, heads,
+                                  hd, 1, halo._stream()))
+        return out, None, None, None, None, None
+
+
+def rope_table(seq, hd, device, theta=500000.0):
+    """(cos, sin) of pos * inv_freq_i, fp32, [seq, hd/2, 2] (Llama-3 theta)."""
+    pos = torch.arange(seq, device=device, dtype=torch.float64)
+    inv = 1.0 / (theta ** (torch.arange(0, hd, 2, device=device, dtype=torch.float64) / hd))
+    ang = torch.outer(pos, inv)
+    return torch.stack((ang.cos(), ang.sin()), -1).float().contiguous()
+
+
+def attention_block(x, qkv_fn, o_fn, mlp_fn, n1, n2, cs, seq, heads, kv_heads):
+    """The Llama block on given projections (shared by LlamaBlock and the
+    HQ-FSDP stack, train.HqFsdpLlama):
+        h = x + O(attn(RoPE(QKV(rmsnorm(x)))));  y = h + MLP(rmsnorm(h))"""
+    T, H = x.shape
+    B = T // seq
+    hd = H // heads
+    a = _rmsnorm(x, n1)
+    qkv = _RopeQKVFn.apply(qkv_fn(a), cs, seq, heads + kv_heads, heads + 2 * kv_heads, hd)
+    nq, nk = heads * hd, kv_heads * hd
+    q = qkv[:, :nq].view(B, seq, heads, hd).transpose(1, 2)
+    k = qkv[:, nq:nq + nk].view(B, seq, kv_heads, hd).transpose(1, 2)
+    v = qkv[:, nq + nk:].view(B, seq, kv_heads, hd).transpose(1, 2)
+    att = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+    att = att.transpose(1, 2).reshape(T, H)
+    h = x + o_fn(att)
+    m = _rmsnorm(h, n2)
+    return h + mlp_fn(m)
 
 
 class LlamaBlock:
@@ -107,36 +188,18 @@ class LlamaBlock:
             self.mlp.owners = (self.gate, self.up, self.down)
         self.n1 = torch.ones(hidden, device=device, requires_grad=True)
         self.n2 = torch.ones(hidden, device=device, requires_grad=True)
-        pos = torch.arange(seq, device=device, dtype=torch.float32)
-        inv = 1.0 / (500000.0 ** (torch.arange(0, hd, 2, device=device, dtype=torch.float32) / hd))
-        ang = torch.outer(pos, inv)
-        self.cos = torch.cat((ang.cos(), ang.cos()), -1).to(bf)[None, None, :, : hd // 2]
-        self.sin = torch.cat((ang.sin(), ang.sin()), -1).to(bf)[None, None, :, : hd // 2]
+        self.cs = rope_table(seq, hd, device)
 
     def linears(self):
         return (self.qkv, self.o, self.gate, self.up, self.down)
 
     def forward(self, x):
         """x: [batch * seq, hidden] bf16 (requires_grad for the backward)."""
-        T, H = x.shape
-        B = T // self.seq
-        hd, nh, nkv = self.hd, self.heads, self.kv
-        a = _rmsnorm(x, self.n1)
-        qkv = self.qkv(a)
-        q, k, v = qkv.split([nh * hd, nkv * hd, nkv * hd], dim=-1)
-        q = q.view(B, self.seq, nh, hd).transpose(1, 2)
-        k = k.view(B, self.seq, nkv, hd).transpose(1, 2)
-        v = v.view(B, self.seq, nkv, hd).transpose(1, 2)
-        q, k = _rope(q, self.cos, self.sin), _rope(k, self.cos, self.sin)
-        att = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
-        att = att.transpose(1, 2).reshape(T, H)
-        h = x + self.o(att)
-        m = _rmsnorm(h, self.n2)
         if self.mlp is not None:
-            y = h + _HaloMLPFn.apply(m, self.mlp)
+            mlp_fn = lambda m: _HaloMLPFn.apply(m, self.mlp)  # noqa: E731
         else:
-            y = h + self.down(F.silu(self.gate(m)) * self.up(m))
-        return y
+            mlp_fn = lambda m: self.down(F.silu(self.gate(m)) * self.up(m))  # noqa: E731
+        return attention_block(x, self.qkv, self.o, mlp_fn, self.n1, self.n2, self.cs, self.seq, self.heads, self.kv)
 
     def gemm_ops(self, tokens):
         """6*b*m*n over the five projections (the quantized GEMM work)."""

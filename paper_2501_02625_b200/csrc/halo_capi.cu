@@ -1545,6 +1545,46 @@ extern "C" halo_status halo_add(const void* a, const void* b, void* out, int32_t
     return cuda_check("add");
 }
 
+extern "C" halo_status halo_rmsnorm_forward(const void* x, const float* gain, void* y, int32_t y_dtype, float* rstd,
+                                            int64_t rows, int64_t dim, int32_t mean, double eps, halo_stream_t stream) {
+    if (!x || !gain || !y || !valid_dtype(y_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "rmsnorm: bad arguments");
+    if (rows < 0 || dim <= 0 || dim % 8 || !(eps >= 0.0)) return fail(HALO_ERR_INVALID_ARGUMENT, "rmsnorm: dim must be a positive multiple of 8, eps >= 0");
+    if (rows == 0) return HALO_OK;
+    ProfScope ps(PC_GLUE, (double)rows * dim * (2 + dt_bytes(y_dtype)), (cudaStream_t)stream);
+    run_rmsnorm_fwd(x, gain, y, y_dtype, rstd, rows, (int)dim, mean != 0, eps, (cudaStream_t)stream);
+    return cuda_check("rmsnorm_forward");
+}
+
+namespace {
+thread_local std::unordered_map<cudaStream_t, Buffer> t_norm_scratch;
+}
+
+extern "C" halo_status halo_rmsnorm_backward(const void* x, const void* dy, int32_t dy_dtype, const float* gain,
+                                             const float* rstd, void* dx, float* dgain, int64_t rows, int64_t dim,
+                                             int32_t mean, halo_stream_t stream) {
+    if (!x || !dy || !gain || !rstd || !dx || !dgain || !valid_dtype(dy_dtype))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rmsnorm_backward: bad arguments");
+    if (rows < 0 || dim <= 0 || dim % 8) return fail(HALO_ERR_INVALID_ARGUMENT, "rmsnorm_backward: dim must be a positive multiple of 8");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (rows == 0) return cudaMemsetAsync(dgain, 0, sizeof(float) * dim, st) == cudaSuccess ? HALO_OK : cuda_check("rmsnorm_backward");
+    Buffer& sc = t_norm_scratch[st];
+    if (sc.ensure((size_t)rmsnorm_bwd_scratch(rows, (int)dim) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+    ProfScope ps(PC_GLUE, (double)rows * dim * (2 + dt_bytes(dy_dtype) + 2), st);
+    run_rmsnorm_bwd(x, dy, dy_dtype, gain, rstd, dx, dgain, sc.as<float>(), rows, (int)dim, mean != 0, st);
+    return cuda_check("rmsnorm_backward");
+}
+
+extern "C" halo_status halo_rope_qkv(const void* in, void* out, const float* cos_sin, int64_t rows, int32_t seq,
+                                     int32_t rot_heads, int32_t heads, int32_t head_dim, int32_t backward,
+                                     halo_stream_t stream) {
+    if (!in || !out || !cos_sin) return fail(HALO_ERR_INVALID_ARGUMENT, "rope: null pointer");
+    if (rows < 0 || seq <= 0 || head_dim % 16 || rot_heads < 0 || rot_heads > heads)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rope: head_dim % 16, 0 <= rot_heads <= heads, seq > 0");
+    ProfScope ps(PC_GLUE, (double)rows * heads * head_dim * 4, (cudaStream_t)stream);
+    run_rope(in, out, cos_sin, rows, seq, rot_heads, heads, head_dim, backward != 0, (cudaStream_t)stream);
+    return cuda_check("rope_qkv");
+}
+
 extern "C" halo_status halo_adamw_step(void* param, int32_t p_dtype, const void* grad, int32_t g_dtype, float* m,
                                        float* v, int64_t n, double lr, double beta1, double beta2, double eps,
                                        double weight_decay, double bc1, double bc2, halo_stream_t stream) {

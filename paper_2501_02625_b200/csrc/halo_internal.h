@@ -168,6 +168,14 @@ void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void
 void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st);
 // out[i] = T(sum_w double(recv[w*n + i]) / world), n % 4 == 0
 void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st);
+// Llama block glue (llama_glue.cu)
+bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, float* rstd, int64_t rows, int dim,
+                     bool mean, double eps, cudaStream_t st);
+bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* gain, const float* rstd, void* dx,
+                     float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st);
+int64_t rmsnorm_bwd_scratch(int64_t rows, int dim);
+bool run_rope(const void* in, void* out, const float* cs, int64_t rows, int seq, int nrot, int nall, int hd,
+              bool backward, cudaStream_t st);
 // AdamWT::step on one parameter (trainer.hpp:104-160), n % 4 == 0
 void run_adamw(void* p, int p_dtype, const void* g, int g_dtype, float* m, float* v, int64_t n, double lr, double b1,
                double b2, double eps, double wd, double bc1, double bc2, cudaStream_t st);

@@ -1,0 +1,227 @@
+// llama_glue.cu — the transformer-block glue around the HALO projections,
+// one HBM pass each (the eager torch chains they replace launch 6-12 kernels
+// apiece): RMSNorm forward / backward (with the gain gradient) and rotary
+// position embedding applied to the fused qkv projection output.
+//
+// RMSNorm (rmsnorm.hpp:27-100): y = x * r * g, r = 1/sqrt(S/D + eps) with
+// S = sum_j x_j^2 accumulated in double, D = dim when `mean` (Llama) or 1
+// (the reference's x/||x||, eps 0).  y is evaluated in double as the
+// reference does (double(x) * r, then * double(g)) and rounded to the output
+// type.  Backward: dx_k = r g_k dy_k - (r^3 x_k / D) * sum_j g_j dy_j x_j
+// (= rmsnorm_backward's (e' - x_hat <x_hat, e'>) / ||x|| for D = 1, eps 0),
+// dg_j = sum_rows dy_j x_j r (rmsnorm_gain_gradient) via per-CTA partial rows
+// reduced in a fixed order (deterministic).
+//
+// RoPE (Llama-3, theta 500000): on each query / key head of the qkv row
+// [q heads | k heads | v heads] x head_dim, pairs (i, i + hd/2):
+//   o1 = t1 c - t2 s,  o2 = t2 c + t1 s,   c, s = cos / sin(pos * inv_freq_i)
+// in fp32 from a per-(position, i) fp32 table; v passes through.  Backward is
+// the transpose rotation.
+#include "common.cuh"
+#include "halo_internal.h"
+#include "sm100.cuh"
+
+namespace halo_b200 {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int NORM_WARPS = 8;
+
+// one warp per row; a lane owns 8-element groups g = lane, lane + 32, ...
+template <typename OutT>
+__global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bfloat16* __restrict__ x,
+                                                                  const float* __restrict__ gain, OutT* __restrict__ y,
+                                                                  float* __restrict__ rstd, int64_t rows, int dim,
+                                                                  double div, double eps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * NORM_WARPS + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const __nv_bfloat16* xr = x + row * dim;
+    double s = 0.0;
+    for (int c = lane * 8; c < dim; c += 256) {
+        float v[8];
+        load8(xr + c, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += (double)v[j] * (double)v[j];
+    }
+    s = warp_sum(s);
+    // a zero row with eps == 0 (rmsnorm.hpp:35-36 raises numeric_error) gives
+    // r = inf and non-finite outputs, which the next HALO quantizer flags
+    const double r = 1.0 / sqrt(s / div + eps);
+    if (lane == 0 && rstd) rstd[row] = (float)r;
+    OutT* yr = y + row * dim;
+    for (int c = lane * 8; c < dim; c += 256) {
+        float v[8], o[8];
+        load8(xr + c, v);
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + c));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + c) + 1);
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = (float)(((double)v[j] * r) * (double)g[j]);
+        if constexpr (sizeof(OutT) == 2) store8(reinterpret_cast<__nv_bfloat16*>(yr + c), o);
+        else store8(reinterpret_cast<float*>(yr + c), o);
+    }
+}
+
+// dx per row (one warp per row, BWD_RPW rows per warp); then the CTA's
+// gain-gradient partial row, sum over its rows of dy * x * r in a fixed row
+// order (deterministic; the rows are re-read from L2), to part[blockIdx.x]
+constexpr int BWD_RPW = 4;
+template <typename DyT>
+__global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bfloat16* __restrict__ x,
+                                                                  const DyT* __restrict__ dy,
+                                                                  const float* __restrict__ gain,
+                                                                  const float* __restrict__ rstd,
+                                                                  __nv_bfloat16* __restrict__ dx,
+                                                                  float* __restrict__ part, int64_t rows, int dim,
+                                                                  double div) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * NORM_WARPS * BWD_RPW;
+    for (int i = 0; i < BWD_RPW; ++i) {
+        const int64_t row = row0 + (int64_t)w * BWD_RPW + i;
+        if (row >= rows) break;
+        const __nv_bfloat16* xr = x + row * dim;
+        const DyT* dr = dy + row * dim;
+        const double r = (double)rstd[row];
+        double dot = 0.0;
+        for (int c = lane * 8; c < dim; c += 256) {
+            float v[8], d[8];
+            load8(xr + c, v);
+            load8(dr + c, d);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dot += (double)__ldg(gain + c + j) * (double)d[j] * (double)v[j];
+        }
+        dot = warp_sum(dot);
+        const double k = r * r * r * dot / div;
+        for (int c = lane * 8; c < dim; c += 256) {
+            float v[8], d[8], o[8];
+            load8(xr + c, v);
+            load8(dr + c, d);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = (float)(r * (double)__ldg(gain + c + j) * (double)d[j] - k * (double)v[j]);
+            store8(dx + row * dim + c, o);
+        }
+    }
+    // gain-gradient partial: thread owns columns, rows in ascending order
+    const int64_t nr = rows - row0 < (int64_t)NORM_WARPS * BWD_RPW ? rows - row0 : (int64_t)NORM_WARPS * BWD_RPW;
+    for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+        double s = 0.0;
+        for (int64_t i = 0; i < nr; ++i) {
+            const int64_t row = row0 + i;
+            s += (double)ldf(dy + row * dim + c) * (double)ldf(x + row * dim + c) * (double)rstd[row];
+        }
+        part[(int64_t)blockIdx.x * dim + c] = (float)s;
+    }
+}
+
+__global__ void k_sum_rows(const float* __restrict__ part, int nparts, int dim, float* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= dim) return;
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += (double)part[(int64_t)i * dim + c];
+    out[c] = (float)s;
+}
+
+// RoPE over the qkv rows: one thread per (row, head of q/k, 8-pair group)
+__global__ void __launch_bounds__(256) k_rope(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                              const float* __restrict__ cs, int64_t rows, int seq, int nrot,
+                                              int nall, int hd, int backward) {
+    const int half = hd / 2, groups = half / 8;
+    const int64_t per_row = (int64_t)nall * groups;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * per_row) return;
+    const int64_t row = idx / per_row;
+    const int rem = (int)(idx % per_row);
+    const int head = rem / groups, g = rem % groups;
+    const int64_t base = row * (int64_t)nall * hd + (int64_t)head * hd + g * 8;
+    float t1[8], t2[8], o1[8], o2[8];
+    load8(in + base, t1);
+    load8(in + base + half, t2);
+    if (head < nrot) {
+        const int pos = (int)(row % seq);
+        const float* c = cs + ((int64_t)pos * half + g * 8) * 2;  // (cos, sin) pairs
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float cj = c[2 * j], sj = c[2 * j + 1];
+            if (!backward) {
+                o1[j] = t1[j] * cj - t2[j] * sj;
+                o2[j] = t2[j] * cj + t1[j] * sj;
+            } else {
+                o1[j] = t1[j] * cj + t2[j] * sj;
+                o2[j] = t2[j] * cj - t1[j] * sj;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            o1[j] = t1[j];
+            o2[j] = t2[j];
+        }
+    }
+    store8(out + base, o1);
+    store8(out + base + half, o2);
+}
+
+}  // namespace
+
+bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, float* rstd, int64_t rows, int dim,
+                     bool mean, double eps, cudaStream_t st) {
+    if (dim % 8 || dim <= 0) return false;
+    const unsigned grid = (unsigned)((rows + NORM_WARPS - 1) / NORM_WARPS);
+    const double div = mean ? (double)dim : 1.0;
+    if (y_dtype == DT_BF16)
+        k_rmsnorm_fwd<__nv_bfloat16><<<grid, 32 * NORM_WARPS, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(x), gain, static_cast<__nv_bfloat16*>(y), rstd, rows, dim, div, eps);
+    else
+        k_rmsnorm_fwd<float><<<grid, 32 * NORM_WARPS, 0, st>>>(static_cast<const __nv_bfloat16*>(x), gain,
+                                                              static_cast<float*>(y), rstd, rows, dim, div, eps);
+    return true;
+}
+
+bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* gain, const float* rstd, void* dx,
+                     float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st) {
+    if (dim % 8 || dim <= 0) return false;
+    const unsigned grid = (unsigned)((rows + NORM_WARPS * BWD_RPW - 1) / (NORM_WARPS * BWD_RPW));
+    const double div = mean ? (double)dim : 1.0;
+    if (dy_dtype == DT_BF16)
+        k_rmsnorm_bwd<__nv_bfloat16><<<grid, 32 * NORM_WARPS, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), gain, rstd,
+            static_cast<__nv_bfloat16*>(dx), scratch, rows, dim, div);
+    else
+        k_rmsnorm_bwd<float><<<grid, 32 * NORM_WARPS, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+                                                              static_cast<const float*>(dy), gain, rstd,
+                                                              static_cast<__nv_bfloat16*>(dx), scratch, rows, dim,
+                                                              div);
+    k_sum_rows<<<(dim + 255) / 256, 256, 0, st>>>(scratch, (int)grid, dim, dgain);
+    return true;
+}
+
+// scratch floats run_rmsnorm_bwd needs
+int64_t rmsnorm_bwd_scratch(int64_t rows, int dim) {
+    return (rows + NORM_WARPS * BWD_RPW - 1) / (NORM_WARPS * BWD_RPW) * (int64_t)dim;
+}
+
+bool run_rope(const void* in, void* out, const float* cs, int64_t rows, int seq, int nrot, int nall, int hd,
+              bool backward, cudaStream_t st) {
+    if (hd % 16 || nrot > nall || seq <= 0) return false;
+    const int64_t n = rows * (int64_t)nall * (hd / 16);
+    if (n == 0) return true;
+    k_rope<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in),
+                                                        static_cast<__nv_bfloat16*>(out), cs, rows, seq, nrot, nall,
+                                                        hd, backward ? 1 : 0);
+    return true;
+}
+
+}  // namespace halo_b200

@@ -38,7 +38,7 @@ import torch.distributed as dist
 
 from . import fsdp, halo
 from ._lib import DTYPE_BF16, DTYPE_F32, check, lib
-from .block import HaloLinear, _HaloMLPFn, _rmsnorm, _rope
+from .block import HaloLinear, _HaloMLPFn, attention_block, rope_table
 
 
 @dataclass
@@ -183,12 +183,7 @@ class HqFsdpLlama:
         self.ready = [torch.cuda.Event() for _ in range(2)]
         self.ledger = fsdp.CommLedger()
         self.stale = torch.zeros(1, dtype=torch.float32, device=self.device)
-        hd = dims.head_dim
-        pos = torch.arange(dims.seq, device=self.device, dtype=torch.float32)
-        inv = 1.0 / (500000.0 ** (torch.arange(0, hd, 2, device=self.device, dtype=torch.float32) / hd))
-        ang = torch.outer(pos, inv)
-        self.cos = ang.cos().to(bf)[None, None]
-        self.sin = ang.sin().to(bf)[None, None]
+        self.cs = rope_table(dims.seq, dims.head_dim, self.device)
 
     # ------------------------------------------------------------ weights
     def _fetch(self, l: int, regather: bool):
@@ -223,24 +218,11 @@ class HqFsdpLlama:
 
     # -------------------------------------------------------------- block
     def _block(self, x: torch.Tensor, l: int) -> torch.Tensor:
-        """Llama block (block.LlamaBlock.forward) on the installed codes."""
+        """Llama block (block.attention_block) on the installed codes."""
         d = self.d
-        T, H = x.shape
-        B = T // d.seq
-        hd, nh, nkv = d.head_dim, d.heads, d.kv_heads
         n1, n2 = self.norms[l]
-        a = _rmsnorm(x, n1)
-        qkv = self.lin["qkv"](a)
-        q, k, v = qkv.split([nh * hd, nkv * hd, nkv * hd], dim=-1)
-        q = q.view(B, d.seq, nh, hd).transpose(1, 2)
-        k = k.view(B, d.seq, nkv, hd).transpose(1, 2)
-        v = v.view(B, d.seq, nkv, hd).transpose(1, 2)
-        q, k = _rope(q, self.cos, self.sin), _rope(k, self.cos, self.sin)
-        att = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
-        att = att.transpose(1, 2).reshape(T, H)
-        h = x + self.lin["o"](att)
-        m = _rmsnorm(h, n2)
-        return h + _HaloMLPFn.apply(m, self.mlp)
+        return attention_block(x, self.lin["qkv"], self.lin["o"], lambda m: _HaloMLPFn.apply(m, self.mlp), n1, n2,
+                               self.cs, d.seq, d.heads, d.kv_heads)
 
     def _zero_grads(self):
         for lin in self.lin.values():

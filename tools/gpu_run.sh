@@ -32,6 +32,8 @@ for w in $what; do
     cfg5)
       timeout 1200 python bench.py --config cfg5 --steps 5 --warmup 3 > gpurun_out/bench_cfg5.log 2>&1
       echo "rc=$?" >> gpurun_out/bench_cfg5.log ;;
+    prof_cfg5)
+      timeout 600 python tools/prof_cfg5.py 4 > gpurun_out/prof_cfg5.log 2>&1 ;;
     kern_v2)
       HALO_K1_VERSION=2 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/kern_v2.log 2>&1 ;;
     prof_k1)
