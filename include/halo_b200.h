@@ -362,6 +362,45 @@ HALO_API halo_status halo_adamw_step(void* param, int32_t p_dtype, const void* g
                                      float* v, int64_t n, double lr, double beta1, double beta2, double eps,
                                      double weight_decay, double bc1, double bc2, halo_stream_t stream);
 
+/* --------------------------------------- HQ-FSDP data plane over NCCL */
+/* The weight protocol of hqfsdp.hpp:172-300 between real ranks (one process
+ * per GPU), stream-ordered, NCCL resolved at run time (libnccl.so.2).
+ * Every rank owns rows [rank*shard_rows, (rank+1)*shard_rows) of a weight
+ * padded to world*shard_rows rows (shard, :131-148). */
+typedef struct halo_fsdp halo_fsdp;
+#define HALO_FSDP_ID_BYTES 128 /* ncclUniqueId */
+HALO_API halo_status halo_fsdp_get_unique_id(void* id);
+HALO_API halo_status halo_fsdp_create(const void* id, int32_t world, int32_t rank, halo_fsdp** out);
+HALO_API halo_status halo_fsdp_destroy(halo_fsdp* f);
+HALO_API halo_status halo_fsdp_world(const halo_fsdp* f, int32_t* world, int32_t* rank);
+/* quantized_all_gather (:204-237): absmax of the rotated shard, max over
+ * ranks, shared scale compute_scales(max) (device, scale_out), codes of the
+ * local rows under it, all-gather: gathered = (world*shard_rows x cols)
+ * codes, bit-identical to a single-process quantize of the rotated padded
+ * weight.  local_absmax_out (device float, may be NULL) keeps this rank's
+ * absmax for the backward's stale check. */
+HALO_API halo_status halo_fsdp_quantized_all_gather(halo_fsdp* f, const void* shard, int32_t dtype, int64_t shard_rows,
+                                                    int64_t cols, int64_t had_block, int32_t format,
+                                                    uint8_t* gathered, float* scale_out, float* local_absmax_out,
+                                                    halo_stream_t stream);
+/* backward_regather (:243-266): the same codes under the saved forward
+ * scale, no scale traffic; with saved_local_absmax and stale_flag, a shard
+ * whose absmax changed since the forward sets *stale_flag (device u32; the
+ * reference throws std::logic_error, :256-259 -- test the flag once). */
+HALO_API halo_status halo_fsdp_backward_regather(halo_fsdp* f, const void* shard, int32_t dtype, int64_t shard_rows,
+                                                 int64_t cols, int64_t had_block, int32_t format, const float* scale,
+                                                 const float* saved_local_absmax, uint32_t* stale_flag,
+                                                 uint8_t* gathered, halo_stream_t stream);
+/* reduce_scatter_grads (:271-300): shard_out (shard_rows x cols) = this
+ * rank's rows of sum_ranks(grad) / world; grad (world*shard_rows x cols)
+ * f32 or bf16 (NCCL's reduction order; the reference sums in double in rank
+ * order -- tolerance parity). */
+HALO_API halo_status halo_fsdp_reduce_scatter(halo_fsdp* f, const void* grad, int32_t dtype, int64_t shard_rows,
+                                              int64_t cols, void* shard_out, halo_stream_t stream);
+/* mean over ranks in place (replicated parameters' gradients, e.g. norm gains) */
+HALO_API halo_status halo_fsdp_all_reduce_mean(halo_fsdp* f, void* buf, int32_t dtype, int64_t n,
+                                               halo_stream_t stream);
+
 /* ------------------------------------------------------------- profiling */
 /* Kernel classes: 0 K1 row-FWHT+quantize, 1 K2 column-FWHT+dual quantize,
  * 2 K3 tcgen05 GEMM, 3 K4 output un-rotation, 4 elementwise glue.

@@ -169,6 +169,18 @@ def lib():
     L.halo_rope_qkv.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]
     for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv"):
         getattr(L, fn).restype = C.c_int
+    L.halo_fsdp_get_unique_id.argtypes = [_vp]
+    L.halo_fsdp_create.argtypes = [_vp, _i32, _i32, C.POINTER(_vp)]
+    L.halo_fsdp_destroy.argtypes = [_vp]
+    L.halo_fsdp_world.argtypes = [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.halo_fsdp_quantized_all_gather.argtypes = [_vp, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp]
+    L.halo_fsdp_backward_regather.argtypes = [_vp, _vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]
+    L.halo_fsdp_reduce_scatter.argtypes = [_vp, _vp, _i32, _i64, _i64, _vp, _vp]
+    L.halo_fsdp_all_reduce_mean.argtypes = [_vp, _vp, _i32, _i64, _vp]
+    for fn in ("halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
+               "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
+               "halo_fsdp_all_reduce_mean"):
+        getattr(L, fn).restype = C.c_int
     L.halo_quantized_tensor_write.argtypes = [C.c_char_p, _i32, _i32, _i64, _i64, _vp, _vp, _i64]
     L.halo_quantized_tensor_info.argtypes = [C.c_char_p] + [C.POINTER(C.c_int32)] * 2 + [C.POINTER(_i64)] * 3
     L.halo_quantized_tensor_read.argtypes = [C.c_char_p, _vp, _vp]
@@ -227,4 +239,7 @@ EXPORTS = (
     "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
     "halo_reduce_scatter_shard", "halo_rotate_quantize_amax", "halo_swiglu_forward_absmax",
     "halo_adamw_step", "halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
+    "halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
+    "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
+    "halo_fsdp_all_reduce_mean",
 )

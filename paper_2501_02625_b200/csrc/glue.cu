@@ -176,4 +176,25 @@ void run_epi_s64(const long long* acc, const float* sa, const float* sb, void* o
         k_epi_s64<float><<<ew_grid(n * 8), 256, 0, st>>>(acc, sa, sb, static_cast<float*>(out), n);
 }
 
+// HQ-FSDP helpers: stale-scale flag (hqfsdp.hpp:256-259) and the 1/world
+// of the gradient mean after a reduce-scatter (:288-292)
+__global__ void k_flag_neq(const float* a, const float* b, unsigned* flag) {
+    if (!(*a == *b)) atomicOr(flag, 1u);
+}
+void run_flag_neq(const float* a, const float* b, unsigned* flag, cudaStream_t st) { k_flag_neq<<<1, 1, 0, st>>>(a, b, flag); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_scale_mul(T* p, int64_t n, float k) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if constexpr (sizeof(T) == 4) p[i] = p[i] * k;
+        else p[i] = __float2bfloat16_rn(__bfloat162float(p[i]) * k);
+    }
+}
+void run_scale_mul(void* buf, int dtype, int64_t n, float k, cudaStream_t st) {
+    if (n <= 0) return;
+    if (dtype == DT_BF16) k_scale_mul<__nv_bfloat16><<<ew_grid(n * 8), 256, 0, st>>>(static_cast<__nv_bfloat16*>(buf), n, k);
+    else k_scale_mul<float><<<ew_grid(n * 8), 256, 0, st>>>(static_cast<float*>(buf), n, k);
+}
+
 }  // namespace halo_b200

@@ -5,9 +5,9 @@
 //
 // RMSNorm (rmsnorm.hpp:27-100): y = x * r * g, r = 1/sqrt(S/D + eps) with
 // S = sum_j x_j^2 accumulated in double, D = dim when `mean` (Llama) or 1
-// (the reference's x/||x||, eps 0).  y is evaluated in double as the
-// reference does (double(x) * r, then * double(g)) and rounded to the output
-// type.  Backward: dx_k = r g_k dy_k - (r^3 x_k / D) * sum_j g_j dy_j x_j
+// (the reference's x/||x||, eps 0).  In the reference form y (and dx) are
+// evaluated in double as rmsnorm.hpp does (double(x) * r, then *
+// double(g)); the Llama form multiplies in fp32.  Backward: dx_k = r g_k dy_k - (r^3 x_k / D) * sum_j g_j dy_j x_j
 // (= rmsnorm_backward's (e' - x_hat <x_hat, e'>) / ||x|| for D = 1, eps 0),
 // dg_j = sum_rows dy_j x_j r (rmsnorm_gain_gradient) via per-CTA partial rows
 // reduced in a fixed order (deterministic).
@@ -25,12 +25,6 @@ namespace halo_b200 {
 
 namespace {
 
-template <typename T>
-__device__ __forceinline__ float ldf(const T* p);
-template <>
-__device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
-template <>
-__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -40,7 +34,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 constexpr int NORM_WARPS = 8;
 
 // one warp per row; a lane owns 8-element groups g = lane, lane + 32, ...
-template <typename OutT>
+// EXACT (the reference form): y = float(double(x) * r * double(g)) as
+// rmsnorm.hpp:38-42; otherwise (Llama) the fp32 product (x * r) * g.
+template <typename OutT, bool EXACT>
 __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bfloat16* __restrict__ x,
                                                                   const float* __restrict__ gain, OutT* __restrict__ y,
                                                                   float* __restrict__ rstd, int64_t rows, int dim,
@@ -61,6 +57,7 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bflo
     // r = inf and non-finite outputs, which the next HALO quantizer flags
     const double r = 1.0 / sqrt(s / div + eps);
     if (lane == 0 && rstd) rstd[row] = (float)r;
+    const float rf = (float)r;
     OutT* yr = y + row * dim;
     for (int c = lane * 8; c < dim; c += 256) {
         float v[8], o[8];
@@ -69,17 +66,22 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bflo
         const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + c) + 1);
         const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = (float)(((double)v[j] * r) * (double)g[j]);
+        for (int j = 0; j < 8; ++j) {
+            if constexpr (EXACT) o[j] = (float)(((double)v[j] * r) * (double)g[j]);
+            else o[j] = (v[j] * rf) * g[j];
+        }
         if constexpr (sizeof(OutT) == 2) store8(reinterpret_cast<__nv_bfloat16*>(yr + c), o);
         else store8(reinterpret_cast<float*>(yr + c), o);
     }
 }
 
-// dx per row (one warp per row, BWD_RPW rows per warp); then the CTA's
-// gain-gradient partial row, sum over its rows of dy * x * r in a fixed row
-// order (deterministic; the rows are re-read from L2), to part[blockIdx.x]
-constexpr int BWD_RPW = 4;
-template <typename DyT>
+// A CTA owns BWD_ROWS rows.  Phase 1 (warp per row): dot = sum_j g dy x
+// (double) and r -> shared memory.  Phase 2 (column-parallel, coalesced 16 B
+// per thread and row): dx for every (row, column) and the gain-gradient
+// partial sum over the CTA's rows in a fixed order (deterministic), written
+// to part[blockIdx.x].  The second read of x / dy hits L2.
+constexpr int BWD_ROWS = 32;
+template <typename DyT, bool EXACT>
 __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bfloat16* __restrict__ x,
                                                                   const DyT* __restrict__ dy,
                                                                   const float* __restrict__ gain,
@@ -87,42 +89,68 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bflo
                                                                   __nv_bfloat16* __restrict__ dx,
                                                                   float* __restrict__ part, int64_t rows, int dim,
                                                                   double div) {
+    __shared__ double kr[BWD_ROWS];
+    __shared__ double rr[BWD_ROWS];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row0 = (int64_t)blockIdx.x * NORM_WARPS * BWD_RPW;
-    for (int i = 0; i < BWD_RPW; ++i) {
-        const int64_t row = row0 + (int64_t)w * BWD_RPW + i;
-        if (row >= rows) break;
+    const int64_t row0 = (int64_t)blockIdx.x * BWD_ROWS;
+    const int nr = (int)(rows - row0 < BWD_ROWS ? rows - row0 : BWD_ROWS);
+    for (int i = w; i < nr; i += NORM_WARPS) {
+        const int64_t row = row0 + i;
         const __nv_bfloat16* xr = x + row * dim;
         const DyT* dr = dy + row * dim;
-        const double r = (double)rstd[row];
         double dot = 0.0;
         for (int c = lane * 8; c < dim; c += 256) {
             float v[8], d[8];
             load8(xr + c, v);
             load8(dr + c, d);
+            const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + c));
+            const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + c) + 1);
+            const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-            for (int j = 0; j < 8; ++j) dot += (double)__ldg(gain + c + j) * (double)d[j] * (double)v[j];
+            for (int j = 0; j < 8; ++j) dot += (double)g[j] * (double)d[j] * (double)v[j];
         }
         dot = warp_sum(dot);
-        const double k = r * r * r * dot / div;
-        for (int c = lane * 8; c < dim; c += 256) {
-            float v[8], d[8], o[8];
-            load8(xr + c, v);
-            load8(dr + c, d);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = (float)(r * (double)__ldg(gain + c + j) * (double)d[j] - k * (double)v[j]);
-            store8(dx + row * dim + c, o);
+        if (lane == 0) {
+            const double r = (double)rstd[row];
+            rr[i] = r;
+            kr[i] = r * r * r * dot / div;
         }
     }
-    // gain-gradient partial: thread owns columns, rows in ascending order
-    const int64_t nr = rows - row0 < (int64_t)NORM_WARPS * BWD_RPW ? rows - row0 : (int64_t)NORM_WARPS * BWD_RPW;
-    for (int c = threadIdx.x; c < dim; c += blockDim.x) {
-        double s = 0.0;
-        for (int64_t i = 0; i < nr; ++i) {
-            const int64_t row = row0 + i;
-            s += (double)ldf(dy + row * dim + c) * (double)ldf(x + row * dim + c) * (double)rstd[row];
+    __syncthreads();
+    for (int c = threadIdx.x * 8; c < dim; c += blockDim.x * 8) {
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + c));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + c) + 1);
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        double accd[EXACT ? 8 : 1];
+        if constexpr (EXACT) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) accd[j] = 0.0;
         }
-        part[(int64_t)blockIdx.x * dim + c] = (float)s;
+        for (int i = 0; i < nr; ++i) {
+            const int64_t row = row0 + i;
+            float v[8], d[8], o[8];
+            load8(x + row * dim + c, v);
+            load8(dy + row * dim + c, d);
+            const double r = rr[i], k = kr[i];
+            const float rf = (float)r, kf = (float)k;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if constexpr (EXACT) {
+                    o[j] = (float)(r * (double)g[j] * (double)d[j] - k * (double)v[j]);
+                    accd[j] += (double)d[j] * (double)v[j] * r;
+                } else {
+                    o[j] = rf * g[j] * d[j] - kf * v[j];
+                    acc[j] += d[j] * v[j] * rf;
+                }
+            }
+            store8(dx + row * dim + c, o);
+        }
+        if constexpr (EXACT) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = (float)accd[j];
+        }
+        store8(part + (int64_t)blockIdx.x * dim + c, acc);
     }
 }
 
@@ -181,36 +209,38 @@ bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, flo
     if (dim % 8 || dim <= 0) return false;
     const unsigned grid = (unsigned)((rows + NORM_WARPS - 1) / NORM_WARPS);
     const double div = mean ? (double)dim : 1.0;
-    if (y_dtype == DT_BF16)
-        k_rmsnorm_fwd<__nv_bfloat16><<<grid, 32 * NORM_WARPS, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(x), gain, static_cast<__nv_bfloat16*>(y), rstd, rows, dim, div, eps);
-    else
-        k_rmsnorm_fwd<float><<<grid, 32 * NORM_WARPS, 0, st>>>(static_cast<const __nv_bfloat16*>(x), gain,
-                                                              static_cast<float*>(y), rstd, rows, dim, div, eps);
+    auto xp = static_cast<const __nv_bfloat16*>(x);
+    // the reference form (x/||x||, eps 0) evaluates y in double like rmsnorm.hpp
+    const bool exact = !mean;
+#define HALO_NF(T, E) k_rmsnorm_fwd<T, E><<<grid, 32 * NORM_WARPS, 0, st>>>(xp, gain, static_cast<T*>(y), rstd, rows, dim, div, eps)
+    if (y_dtype == DT_BF16) {
+        if (exact) HALO_NF(__nv_bfloat16, true); else HALO_NF(__nv_bfloat16, false);
+    } else {
+        if (exact) HALO_NF(float, true); else HALO_NF(float, false);
+    }
+#undef HALO_NF
     return true;
 }
+
+int64_t rmsnorm_bwd_scratch(int64_t rows, int dim) { return (rows + BWD_ROWS - 1) / BWD_ROWS * (int64_t)dim; }
 
 bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* gain, const float* rstd, void* dx,
                      float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st) {
     if (dim % 8 || dim <= 0) return false;
-    const unsigned grid = (unsigned)((rows + NORM_WARPS * BWD_RPW - 1) / (NORM_WARPS * BWD_RPW));
+    const unsigned grid = (unsigned)((rows + BWD_ROWS - 1) / BWD_ROWS);
     const double div = mean ? (double)dim : 1.0;
-    if (dy_dtype == DT_BF16)
-        k_rmsnorm_bwd<__nv_bfloat16><<<grid, 32 * NORM_WARPS, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), gain, rstd,
-            static_cast<__nv_bfloat16*>(dx), scratch, rows, dim, div);
-    else
-        k_rmsnorm_bwd<float><<<grid, 32 * NORM_WARPS, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
-                                                              static_cast<const float*>(dy), gain, rstd,
-                                                              static_cast<__nv_bfloat16*>(dx), scratch, rows, dim,
-                                                              div);
+    auto xp = static_cast<const __nv_bfloat16*>(x);
+    auto dxp = static_cast<__nv_bfloat16*>(dx);
+    const bool exact = !mean;
+#define HALO_NB(T, E) k_rmsnorm_bwd<T, E><<<grid, 32 * NORM_WARPS, 0, st>>>(xp, static_cast<const T*>(dy), gain, rstd, dxp, scratch, rows, dim, div)
+    if (dy_dtype == DT_BF16) {
+        if (exact) HALO_NB(__nv_bfloat16, true); else HALO_NB(__nv_bfloat16, false);
+    } else {
+        if (exact) HALO_NB(float, true); else HALO_NB(float, false);
+    }
+#undef HALO_NB
     k_sum_rows<<<(dim + 255) / 256, 256, 0, st>>>(scratch, (int)grid, dim, dgain);
     return true;
-}
-
-// scratch floats run_rmsnorm_bwd needs
-int64_t rmsnorm_bwd_scratch(int64_t rows, int dim) {
-    return (rows + NORM_WARPS * BWD_RPW - 1) / (NORM_WARPS * BWD_RPW) * (int64_t)dim;
 }
 
 bool run_rope(const void* in, void* out, const float* cs, int64_t rows, int seq, int nrot, int nall, int hd,

@@ -106,6 +106,111 @@ class CudaOps:
         return codes
 
 
+class NcclDataPlane:
+    """The C++ HQ-FSDP data plane of this rank (halo_fsdp_*, csrc/hqfsdp_nccl.cpp:
+    NCCL resolved at run time): quantized_all_gather / backward_regather /
+    reduce_scatter_grads as stream-ordered library calls, no host syncs.  The
+    communicator's unique id is broadcast over `group` (any backend); with
+    torch.distributed uninitialised it is a world of one."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+        from ._lib import check, lib
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            check(lib().halo_fsdp_get_unique_id(uid))
+        if self.world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        check(lib().halo_fsdp_create(uid, self.world, self.rank, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        from ._lib import lib
+        if getattr(self, "_h", None):
+            lib().halo_fsdp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+    @staticmethod
+    def _blk(p, rotate, had_block):
+        return had_block if rotate else -1
+
+    def gather(self, p: "ShardedParam", rotate: bool, had_block: int, out: torch.Tensor, ledger: "CommLedger"):
+        """quantized_all_gather (hqfsdp.hpp:204-237) into `out`."""
+        from . import halo
+        from ._lib import check, lib
+        if p.local_absmax is None or p.local_absmax.numel() != 1:
+            p.local_absmax = torch.empty(1, dtype=torch.float32, device=p.master.device)
+        if p.global_scale is None or p.global_scale.numel() != 1:
+            p.global_scale = torch.empty(1, dtype=torch.float32, device=p.master.device)
+        check(lib().halo_fsdp_quantized_all_gather(self._h, halo._ptr(p.master), halo._dt(p.master), p.shard_rows,
+                                                   p.cols, self._blk(p, rotate, had_block), p.format, halo._ptr(out),
+                                                   halo._ptr(p.global_scale), halo._ptr(p.local_absmax),
+                                                   halo._stream()))
+        p.scales_valid = True
+        ledger.record(ledger.scale_reduce, K_SCALE_BYTES, p.world)
+        elems = out.numel()
+        ledger.record(ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
+        ledger.bf16_gather_payload += 2 * elems
+        return out, p.global_scale
+
+    def regather(self, p: "ShardedParam", rotate: bool, had_block: int, out: torch.Tensor, ledger: "CommLedger",
+                 stale_flag: torch.Tensor | None = None):
+        """backward_regather (hqfsdp.hpp:243-266); stale_flag: int32 [1]."""
+        from . import halo
+        from ._lib import check, lib
+        if not p.scales_valid:
+            raise HaloLogicError("backward_regather: no saved forward scales")
+        check(lib().halo_fsdp_backward_regather(self._h, halo._ptr(p.master), halo._dt(p.master), p.shard_rows,
+                                                p.cols, self._blk(p, rotate, had_block), p.format,
+                                                halo._ptr(p.global_scale),
+                                                halo._ptr(p.local_absmax) if stale_flag is not None else None,
+                                                halo._ptr(stale_flag), halo._ptr(out), halo._stream()))
+        ledger.backward_gathers += 1
+        elems = out.numel()
+        ledger.record(ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
+        ledger.bf16_gather_payload += 2 * elems
+        return out, p.global_scale
+
+    def reduce_scatter(self, grad: torch.Tensor, p: "ShardedParam", ledger: "CommLedger") -> torch.Tensor:
+        """reduce_scatter_grads (hqfsdp.hpp:271-300): this rank's rows of the mean."""
+        from . import halo
+        from ._lib import check, lib
+        if tuple(grad.shape) != (p.full_rows, p.cols):
+            raise ValueError("reduce_scatter_grads: gradient shape mismatch")
+        if p.world == 1 and p.pad_rows == 0:
+            ledger.record(ledger.reduce_scatter, 2 * grad.numel(), 1)
+            return grad
+        if p.pad_rows:
+            padded = torch.zeros((p.shard_rows * p.world, p.cols), dtype=grad.dtype, device=grad.device)
+            padded[: p.full_rows] = grad
+        else:
+            padded = grad.contiguous()
+        out = torch.empty((p.shard_rows, p.cols), dtype=grad.dtype, device=grad.device)
+        check(lib().halo_fsdp_reduce_scatter(self._h, halo._ptr(padded), halo._dt(padded), p.shard_rows, p.cols,
+                                             halo._ptr(out), halo._stream()))
+        ledger.record(ledger.reduce_scatter, 2 * padded.numel(), p.world)
+        return out
+
+    def all_reduce_mean(self, t: torch.Tensor):
+        from . import halo
+        from ._lib import check, lib
+        check(lib().halo_fsdp_all_reduce_mean(self._h, halo._ptr(t), halo._dt(t), t.numel(), halo._stream()))
+        return t
+
+
 # ------------------------------------------------------------- sharding --
 
 @dataclass

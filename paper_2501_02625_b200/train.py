@@ -126,7 +126,8 @@ class HqFsdpLlama:
     HQ-FSDP shards (see the module docstring)."""
 
     def __init__(self, dims: LlamaDims, scheme, group=None, seed: int = 0, device="cuda",
-                 check_stale: bool = True, prefetch: bool = True, opt: AdamWConfig | None = None):
+                 check_stale: bool = True, prefetch: bool = True, opt: AdamWConfig | None = None,
+                 data_plane: str = "native"):
         self.d = dims
         self.scheme = scheme
         self.group = group
@@ -182,7 +183,12 @@ class HqFsdpLlama:
         self.comm = torch.cuda.Stream(device=self.device)
         self.ready = [torch.cuda.Event() for _ in range(2)]
         self.ledger = fsdp.CommLedger()
-        self.stale = torch.zeros(1, dtype=torch.float32, device=self.device)
+        # the collectives: the library's C++ NCCL data plane (halo_fsdp_*) or
+        # torch.distributed (the protocol functions of fsdp.py)
+        if data_plane not in ("native", "torch"):
+            raise ValueError("data_plane: 'native' or 'torch'")
+        self.plane = fsdp.NcclDataPlane(group) if data_plane == "native" else None
+        self.stale = torch.zeros(1, dtype=torch.int32 if self.plane else torch.float32, device=self.device)
         self.cs = rope_table(dims.seq, dims.head_dim, self.device)
 
     # ------------------------------------------------------------ weights
@@ -197,15 +203,21 @@ class HqFsdpLlama:
         with torch.cuda.stream(side):
             for name in WEIGHTS:
                 p = self.masters[l][name]
+                out = self.codes[slot][name]
                 if regather:
-                    codes, scale = fsdp.backward_regather(p, self.rotate, self.ledger, self.check_stale, self.block,
-                                                          self.group, out=self.codes[slot][name],
-                                                          stale_flag=self.stale)
+                    if self.plane is not None:
+                        codes, scale = self.plane.regather(p, self.rotate, self.block, out, self.ledger,
+                                                           self.stale if self.check_stale else None)
+                    else:
+                        codes, scale = fsdp.backward_regather(p, self.rotate, self.ledger, self.check_stale,
+                                                              self.block, self.group, out=out, stale_flag=self.stale)
                     # one regather, two consumers: recompute forward + backward
                     self.ledger.backward_consumers += 2
+                elif self.plane is not None:
+                    codes, scale = self.plane.gather(p, self.rotate, self.block, out, self.ledger)
                 else:
                     codes, scale = fsdp.quantized_all_gather(p, self.rotate, self.ledger, self.block, self.group,
-                                                             out=self.codes[slot][name])
+                                                             out=out)
                 self.scales[slot][name] = scale
             self.ready[slot].record(side)
 
@@ -276,13 +288,19 @@ class HqFsdpLlama:
             base = l * (len(WEIGHTS) + 2)
             for j, name in enumerate(WEIGHTS):
                 p = self.masters[l][name]
-                gshard = fsdp.reduce_scatter_grads(grads[name], p, self.ledger, self.group)
+                if self.plane is not None:
+                    gshard = self.plane.reduce_scatter(grads[name], p, self.ledger)
+                else:
+                    gshard = fsdp.reduce_scatter_grads(grads[name], p, self.ledger, self.group)
                 self.opt.update(base + j, gshard)
             for j, n in enumerate((n1, n2)):
                 ng = n.grad
                 if self.world > 1:
-                    dist.all_reduce(ng, group=self.group)
-                    ng.div_(self.world)
+                    if self.plane is not None:
+                        self.plane.all_reduce_mean(ng)
+                    else:
+                        dist.all_reduce(ng, group=self.group)
+                        ng.div_(self.world)
                 n.requires_grad_(False)
                 self.opt.update(base + len(WEIGHTS) + j, ng)
                 n.grad = None
@@ -304,6 +322,8 @@ class HqFsdpLlama:
 
     def close(self):
         torch.cuda.synchronize(self.device)
+        if self.plane is not None:
+            self.plane.close()
 
 
 class _GradSink:

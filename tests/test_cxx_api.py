@@ -44,3 +44,31 @@ def test_cxx_api_layer_on_gpu(orc, tmp_path):
     assert np.array_equal(np.fromfile(tmp_path / "Y.out", np.float32).reshape(b, n), want["Y"])
     assert np.array_equal(np.fromfile(tmp_path / "EX.out", np.float32).reshape(b, m), want["EX"])
     assert np.array_equal(np.fromfile(tmp_path / "GW.out", np.float32).reshape(n, m), want["GW"])
+
+
+@pytest.mark.gpu
+def test_cxx_fsdp_driver_world1(orc, tmp_path):
+    """INTEGRATION.md §3 as a compiled C++ trainer step over the HQ-FSDP NCCL
+    data plane (halo_fsdp_*): gather -> forward -> regather -> backward ->
+    reduce-scatter, world 1 (NCCL refuses two ranks on one GPU; the protocol
+    at world 2/4 is covered on CPU in test_fsdp_cpu.py).  Outputs bit-exact
+    with the oracle layer; the stale-scale flag trips after a master write."""
+    exe = tmp_path / "fsdp_driver"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-o", str(exe), os.path.join(ROOT, "tests", "cpu", "fsdp_driver.cpp"),
+                    "-I/usr/local/cuda/include", "-L" + PKG, "-lhalo_b200", "-Wl,-rpath," + PKG,
+                    "-L/usr/local/cuda/lib64", "-lcudart"], check=True)
+    b, m, n, block = 256, 512, 256, 256
+    X = orc.bf16_round(orc.randn(b, m, 1))
+    X[:, 3] *= 40
+    W = orc.bf16_round(orc.randn(n, m, 2, 1 / 16))
+    E = orc.bf16_round(orc.randn(b, n, 3, 1e-3))
+    for name, a in (("X", X), ("W", W), ("E", E)):
+        a.astype(np.float32).tofile(tmp_path / f"{name}.f32")
+    r = subprocess.run([str(exe), str(tmp_path), str(b), str(m), str(n), str(block), "1", "0"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "stale-before 0 stale-after 1" in r.stdout, r.stdout
+    want = orc.linear(2, 0, block, X, W, E)
+    assert np.array_equal(np.fromfile(tmp_path / "Y.out", np.float32).reshape(b, n), want["Y"])
+    assert np.array_equal(np.fromfile(tmp_path / "EX.out", np.float32).reshape(b, m), want["EX"])
+    assert np.array_equal(np.fromfile(tmp_path / "GW0.out", np.float32).reshape(n, m), want["GW"])

@@ -4,7 +4,8 @@ trainer.hpp:104-160) on the GPU.
 * halo_adamw_step against a host restatement of AdamWT::step (trainer.hpp:
   126-155) in IEEE double with the device's fp32 state storage: bit-exact
   over several steps, bf16 and fp32 masters, bf16 and fp32 gradients.
-* HqFsdpLlama (world 1: gathered codes installed per layer, prefetch on a
+* HqFsdpLlama (world 1, both data planes -- the library's C++ NCCL plane
+  halo_fsdp_* and torch.distributed: gathered codes installed per layer, prefetch on a
   side stream, activation checkpointing with one regather feeding the
   recompute and the backward, reduce-scatter, per-layer AdamW) against the
   direct composition -- a stack of block.LlamaBlock's with their own HALO
@@ -77,7 +78,8 @@ def test_adamw_matches_reference_formula(T, pdt, gdt):
 SMALL = dict(hidden=256, heads=2, kv_heads=1, inter=512, layers=2, seq=256)
 
 
-def test_fsdp_step_matches_direct_stack(T):
+@pytest.mark.parametrize("plane", ["native", "torch"])
+def test_fsdp_step_matches_direct_stack(T, plane):
     from torch.nn.attention import SDPBackend, sdpa_kernel
 
     from paper_2501_02625_b200 import halo
@@ -85,7 +87,7 @@ def test_fsdp_step_matches_direct_stack(T):
     d = T.LlamaDims(**SMALL)
     scheme = halo.halo2(halo.INT8, 256)
     cfg = T.AdamWConfig(lr=1e-3, warmup_steps=1)
-    model = T.HqFsdpLlama(d, scheme, seed=3, opt=cfg)
+    model = T.HqFsdpLlama(d, scheme, seed=3, opt=cfg, data_plane=plane)
     # the direct composition on copies of the same weights
     blocks = []
     for l in range(d.layers):
@@ -141,8 +143,10 @@ def fsdp_stale(model):
     """regather of layer 0 after its master changed: the device flag trips."""
     from paper_2501_02625_b200 import fsdp
     model.stale.zero_()
-    for name in ("o",):
-        p = model.masters[0][name]
+    p = model.masters[0]["o"]
+    if model.plane is not None:  # the C++ data plane: halo_fsdp_backward_regather's device flag
+        model.plane.regather(p, model.rotate, model.block, model.codes[0]["o"], model.ledger, model.stale)
+    else:
         fsdp.backward_regather(p, model.rotate, model.ledger, True, model.block, model.group,
-                               out=model.codes[0][name], stale_flag=model.stale)
+                               out=model.codes[0]["o"], stale_flag=model.stale)
     model.check()

@@ -34,6 +34,12 @@ for w in $what; do
       echo "rc=$?" >> gpurun_out/bench_cfg5.log ;;
     prof_cfg5)
       timeout 600 python tools/prof_cfg5.py 4 > gpurun_out/prof_cfg5.log 2>&1 ;;
+    glue)
+      timeout 900 python -m pytest tests/test_gpu_glue.py tests/test_gpu_train.py tests/test_gpu_layer.py -x -q > gpurun_out/pytest_glue.log 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_glue.log ;;
+    block)
+      timeout 900 python tools/bench_block.py --steps 10 > gpurun_out/bench_block.log 2>&1
+      echo "rc=$?" >> gpurun_out/bench_block.log ;;
     kern_v2)
       HALO_K1_VERSION=2 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/kern_v2.log 2>&1 ;;
     prof_k1)
