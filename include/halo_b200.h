@@ -351,6 +351,14 @@ HALO_API halo_status halo_rope_qkv(const void* in, void* out, const float* cos_s
                                    int32_t rot_heads, int32_t heads, int32_t head_dim, int32_t backward,
                                    halo_stream_t stream);
 
+/* ------------------------------------------------- FP6 E3M2 wire format */
+/* The packed FP6 payload of the HQ-FSDP gather (hqfsdp.hpp:36-49: four
+ * codes in three bytes, 0.375 x BF16): n device codes (E3M2 in bits 7:2 of a
+ * byte each, n % 4 == 0) <-> 3n/4 bytes; group g = codes 4g..4g+3 packed as
+ * the 24-bit little-endian word c0 | c1 << 6 | c2 << 12 | c3 << 18. */
+HALO_API halo_status halo_fp6_pack(const uint8_t* codes, uint8_t* packed, int64_t n, halo_stream_t stream);
+HALO_API halo_status halo_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, halo_stream_t stream);
+
 /* ------------------------------------------------ optimizer (HQ-FSDP) */
 /* AdamWT::step for one parameter (trainer.hpp:104-160), e.g. this rank's
  * row shard of a master weight in the HQ-FSDP training loop

@@ -169,6 +169,10 @@ def lib():
     L.halo_rope_qkv.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]
     for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv"):
         getattr(L, fn).restype = C.c_int
+    L.halo_fp6_pack.argtypes = [_vp, _vp, _i64, _vp]
+    L.halo_fp6_unpack.argtypes = [_vp, _vp, _i64, _vp]
+    L.halo_fp6_pack.restype = C.c_int
+    L.halo_fp6_unpack.restype = C.c_int
     L.halo_fsdp_get_unique_id.argtypes = [_vp]
     L.halo_fsdp_create.argtypes = [_vp, _i32, _i32, C.POINTER(_vp)]
     L.halo_fsdp_destroy.argtypes = [_vp]
@@ -241,5 +245,5 @@ EXPORTS = (
     "halo_adamw_step", "halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
     "halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
     "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
-    "halo_fsdp_all_reduce_mean",
+    "halo_fsdp_all_reduce_mean", "halo_fp6_pack", "halo_fp6_unpack",
 )

@@ -197,4 +197,41 @@ void run_scale_mul(void* buf, int dtype, int64_t n, float k, cudaStream_t st) {
     else k_scale_mul<float><<<ew_grid(n * 8), 256, 0, st>>>(static_cast<float*>(buf), n, k);
 }
 
+// FP6 E3M2 wire format (the HQ-FSDP gather payload, hqfsdp.hpp:36-49: four
+// codes in three bytes): group g of 4 device codes (E3M2 in bits 7:2 of one
+// byte each) -> 24-bit little-endian word c0 | c1 << 6 | c2 << 12 | c3 << 18.
+// One thread packs / unpacks 8 groups (32 codes <-> 24 bytes).
+__global__ void __launch_bounds__(256) k_fp6_pack(const uint8_t* __restrict__ codes, uint8_t* __restrict__ packed,
+                                                  int64_t groups) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(codes + 4 * g);
+        const uint32_t v = ((w >> 2) & 0x3Fu) | (((w >> 10) & 0x3Fu) << 6) | (((w >> 18) & 0x3Fu) << 12) |
+                           (((w >> 26) & 0x3Fu) << 18);
+        uint8_t* o = packed + 3 * g;
+        o[0] = (uint8_t)v;
+        o[1] = (uint8_t)(v >> 8);
+        o[2] = (uint8_t)(v >> 16);
+    }
+}
+__global__ void __launch_bounds__(256) k_fp6_unpack(const uint8_t* __restrict__ packed, uint8_t* __restrict__ codes,
+                                                    int64_t groups) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        const uint8_t* i = packed + 3 * g;
+        const uint32_t v = (uint32_t)i[0] | ((uint32_t)i[1] << 8) | ((uint32_t)i[2] << 16);
+        const uint32_t w = ((v & 0x3Fu) << 2) | (((v >> 6) & 0x3Fu) << 10) | (((v >> 12) & 0x3Fu) << 18) |
+                           (((v >> 18) & 0x3Fu) << 26);
+        *reinterpret_cast<uint32_t*>(codes + 4 * g) = w;
+    }
+}
+void run_fp6_pack(const uint8_t* codes, uint8_t* packed, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_fp6_pack<<<ew_grid(n * 2), 256, 0, st>>>(codes, packed, n / 4);
+}
+void run_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_fp6_unpack<<<ew_grid(n * 2), 256, 0, st>>>(packed, codes, n / 4);
+}
+
 }  // namespace halo_b200

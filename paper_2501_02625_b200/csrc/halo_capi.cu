@@ -1585,6 +1585,18 @@ extern "C" halo_status halo_rope_qkv(const void* in, void* out, const float* cos
     return cuda_check("rope_qkv");
 }
 
+extern "C" halo_status halo_fp6_pack(const uint8_t* codes, uint8_t* packed, int64_t n, halo_stream_t stream) {
+    if (!codes || !packed || n < 0 || n % 4) return fail(HALO_ERR_INVALID_ARGUMENT, "fp6_pack: n must be a multiple of 4");
+    run_fp6_pack(codes, packed, n, (cudaStream_t)stream);
+    return cuda_check("fp6_pack");
+}
+
+extern "C" halo_status halo_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, halo_stream_t stream) {
+    if (!codes || !packed || n < 0 || n % 4) return fail(HALO_ERR_INVALID_ARGUMENT, "fp6_unpack: n must be a multiple of 4");
+    run_fp6_unpack(packed, codes, n, (cudaStream_t)stream);
+    return cuda_check("fp6_unpack");
+}
+
 extern "C" halo_status halo_adamw_step(void* param, int32_t p_dtype, const void* grad, int32_t g_dtype, float* m,
                                        float* v, int64_t n, double lr, double beta1, double beta2, double eps,
                                        double weight_decay, double bc1, double bc2, halo_stream_t stream) {

@@ -168,6 +168,9 @@ void run_swiglu_bwd(const void* dH, const void* G, const void* U, void* dG, void
 void run_add(const void* a, const void* b, void* out, int dtype, int64_t n, cudaStream_t st);
 // out[i] = T(sum_w double(recv[w*n + i]) / world), n % 4 == 0
 void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype, cudaStream_t st);
+// FP6 E3M2 wire format: 4 codes (bits 7:2 of a byte each) <-> 3 bytes; n % 4 == 0
+void run_fp6_pack(const uint8_t* codes, uint8_t* packed, int64_t n, cudaStream_t st);
+void run_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, cudaStream_t st);
 // Llama block glue (llama_glue.cu)
 bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, float* rstd, int64_t rows, int dim,
                      bool mean, double eps, cudaStream_t st);

@@ -35,6 +35,8 @@ namespace halo_b200 {
 void set_last_error(const char* msg);
 void run_flag_neq(const float* a, const float* b, unsigned* flag, cudaStream_t st);
 void run_scale_mul(void* buf, int dtype, int64_t n, float k, cudaStream_t st);
+void run_fp6_pack(const uint8_t* codes, uint8_t* packed, int64_t n, cudaStream_t st);
+void run_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, cudaStream_t st);
 }
 
 namespace {
@@ -92,6 +94,8 @@ struct halo_fsdp {
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0;
     float* amax = nullptr;  // device: [0] local absmax, [1] reduced max
+    uint8_t* wire = nullptr;  // FP6: packed gather buffer (grow-only)
+    size_t wire_bytes = 0;
 };
 
 extern "C" halo_status halo_fsdp_get_unique_id(void* id) {
@@ -132,6 +136,7 @@ extern "C" halo_status halo_fsdp_destroy(halo_fsdp* f) {
     Nccl* n = nccl();
     if (f->comm && n) n->commDestroy(f->comm);
     if (f->amax) cudaFree(f->amax);
+    if (f->wire) cudaFree(f->wire);
     delete f;
     return HALO_OK;
 }
@@ -143,8 +148,32 @@ extern "C" halo_status halo_fsdp_world(const halo_fsdp* f, int32_t* world, int32
     return HALO_OK;
 }
 
-static halo_status gather_codes(halo_fsdp* f, uint8_t* gathered, int64_t shard_bytes, cudaStream_t st) {
+static halo_status gather_codes(halo_fsdp* f, uint8_t* gathered, int64_t shard_bytes, int32_t format,
+                                cudaStream_t st) {
     if (f->world == 1) return HALO_OK;
+    if (format == HALO_FMT_FP6_E3M2 && shard_bytes % 4 == 0) {
+        // the FP6 wire format: 3 bytes per 4 codes on the wire (hqfsdp.hpp:41-43)
+        const int64_t pk = shard_bytes / 4 * 3;
+        const size_t need = (size_t)pk * (size_t)f->world;
+        if (f->wire_bytes < need) {
+            if (f->wire) cudaFree(f->wire);
+            f->wire = nullptr;
+            f->wire_bytes = 0;
+            if (cudaMalloc(&f->wire, need) != cudaSuccess) {
+                halo_b200::set_last_error("hqfsdp: cudaMalloc failed");
+                return HALO_ERR_CUDA;
+            }
+            f->wire_bytes = need;
+        }
+        halo_b200::run_fp6_pack(gathered + (int64_t)f->rank * shard_bytes, f->wire + (int64_t)f->rank * pk,
+                                shard_bytes, st);
+        const halo_status s = ncheck(nccl()->allGather(f->wire + (int64_t)f->rank * pk, f->wire, (size_t)pk,
+                                                       ncclUint8, f->comm, st),
+                                     "ncclAllGather (fp6 wire)");
+        if (s != HALO_OK) return s;
+        halo_b200::run_fp6_unpack(f->wire, gathered, shard_bytes * f->world, st);
+        return HALO_OK;
+    }
     // in place: this rank's slice already holds its codes
     return ncheck(nccl()->allGather(gathered + (int64_t)f->rank * shard_bytes, gathered, (size_t)shard_bytes,
                                     ncclUint8, f->comm, st),
@@ -175,7 +204,7 @@ extern "C" halo_status halo_fsdp_quantized_all_gather(halo_fsdp* f, const void* 
     s = halo_rotate_quantize_amax(shard, dtype, shard_rows, cols, had_block, format, &f->amax[1],
                                   gathered + (int64_t)f->rank * shard_bytes, scale_out, stream);
     if (s != HALO_OK) return s;
-    return gather_codes(f, gathered, shard_bytes, st);
+    return gather_codes(f, gathered, shard_bytes, format, st);
 }
 
 extern "C" halo_status halo_fsdp_backward_regather(halo_fsdp* f, const void* shard, int32_t dtype,
@@ -195,7 +224,7 @@ extern "C" halo_status halo_fsdp_backward_regather(halo_fsdp* f, const void* sha
     const halo_status s = halo_rotate_quantize(shard, dtype, shard_rows, cols, had_block, format, scale,
                                                gathered + (int64_t)f->rank * shard_bytes, nullptr, stream);
     if (s != HALO_OK) return s;
-    return gather_codes(f, gathered, shard_bytes, st);
+    return gather_codes(f, gathered, shard_bytes, format, st);
 }
 
 extern "C" halo_status halo_fsdp_reduce_scatter(halo_fsdp* f, const void* grad, int32_t dtype, int64_t shard_rows,

@@ -246,6 +246,26 @@ def qmatmul(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: to
     return c
 
 
+# ------------------------------------------------------ FP6 wire format
+
+def fp6_pack(codes: torch.Tensor) -> torch.Tensor:
+    """Device E3M2 codes (bits 7:2 of a byte each) -> the packed FP6 payload
+    (3 bytes per 4 codes, hqfsdp.hpp:36-49), uint8 [numel * 3/4]."""
+    _need_cuda(codes)
+    c = codes.contiguous().view(torch.uint8).reshape(-1)
+    out = torch.empty(c.numel() // 4 * 3, dtype=torch.uint8, device=c.device)
+    check(lib().halo_fp6_pack(_ptr(c), _ptr(out), c.numel(), _stream()))
+    return out
+
+
+def fp6_unpack(packed: torch.Tensor, n: int) -> torch.Tensor:
+    """The packed FP6 payload -> n device codes (uint8, E3M2 in bits 7:2)."""
+    _need_cuda(packed)
+    out = torch.empty(n, dtype=torch.uint8, device=packed.device)
+    check(lib().halo_fp6_unpack(_ptr(packed.contiguous()), _ptr(out), n, _stream()))
+    return out
+
+
 # ------------------------------------------------------ quantized tensor files
 
 def write_quantized_tensor(path: str, codes: torch.Tensor, scales: torch.Tensor, fmt: int = INT8,

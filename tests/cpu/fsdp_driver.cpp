@@ -96,6 +96,20 @@ int main(int argc, char** argv) {
     CK(halo_fsdp_quantized_all_gather(fs, dw, HALO_DTYPE_BF16, rows, m, blk, HALO_FMT_INT8, gathered, scale, amax, st));
     CK(halo_linear_set_qweight(layer, gathered, scale));
     CK(halo_linear_forward(layer, dx, HALO_DTYPE_BF16, b, y, HALO_DTYPE_F32, ctx, st));
+    if (std::getenv("HALO_DRIVER_DUMP")) {
+        const uint8_t *xq, *wq;
+        const float *sx, *sw;
+        int64_t br;
+        CK(halo_ctx_saved(ctx, &xq, &sx, &wq, &sw, &br));
+        cudaStreamSynchronize(st);
+        std::vector<uint8_t> h(b * m);
+        cudaMemcpy(h.data(), xq, b * m, cudaMemcpyDeviceToHost);
+        std::ofstream(dir + "/xq.out", std::ios::binary).write(reinterpret_cast<const char*>(h.data()), b * m);
+        float sxh = 0, swh = 0;
+        cudaMemcpy(&sxh, sx, 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&swh, sw, 4, cudaMemcpyDeviceToHost);
+        std::printf("sx %.9g sw %.9g\n", sxh, swh);
+    }
     // backward: regather under the saved scale (the codes the backward reads)
     CK(halo_fsdp_backward_regather(fs, dw, HALO_DTYPE_BF16, rows, m, blk, HALO_FMT_INT8, scale, amax, stale, gathered, st));
     CK(halo_linear_backward(layer, ctx, de, HALO_DTYPE_BF16, ex, HALO_DTYPE_F32, gw, HALO_DTYPE_F32, st));

@@ -69,3 +69,21 @@ def test_fp6_golden_values(H):
     codes, scale = H.rotate_quantize(a, fmt=2, rotate=False)
     assert scale.item() == np.float32(30.0 / 28.0)
 
+
+
+def test_fp6_wire_format_pack_unpack(H, orc):
+    """The packed FP6 payload of the HQ-FSDP gather (hqfsdp.hpp:36-49: 4 codes
+    in 3 bytes): layout c0 | c1<<6 | c2<<12 | c3<<18 little-endian, restated
+    in numpy; unpack(pack(codes)) == codes; 0.375 of the BF16 bytes."""
+    from paper_2501_02625_b200 import fsdp
+    a = orc.bf16_round(orc.randn(64, 256, 13))
+    codes, _ = H.rotate_quantize(torch.from_numpy(a).cuda().to(torch.bfloat16), 256, fmt=2)
+    packed = H.fp6_pack(codes)
+    c6 = (codes.cpu().numpy().view(np.uint8).reshape(-1, 4).astype(np.uint32) >> 2)
+    word = c6[:, 0] | (c6[:, 1] << 6) | (c6[:, 2] << 12) | (c6[:, 3] << 18)
+    want = np.stack([word & 0xFF, (word >> 8) & 0xFF, (word >> 16) & 0xFF], 1).astype(np.uint8).reshape(-1)
+    assert np.array_equal(packed.cpu().numpy(), want)
+    back = H.fp6_unpack(packed, codes.numel())
+    assert torch.equal(back, codes.view(torch.uint8).reshape(-1))
+    assert packed.numel() == fsdp.code_payload_bytes(fsdp.FP6_E3M2, codes.numel())
+    assert packed.numel() / (2 * codes.numel()) == 0.375

@@ -35,7 +35,7 @@ for w in $what; do
     prof_cfg5)
       timeout 600 python tools/prof_cfg5.py 4 > gpurun_out/prof_cfg5.log 2>&1 ;;
     glue)
-      timeout 900 python -m pytest tests/test_gpu_glue.py tests/test_gpu_train.py tests/test_gpu_layer.py -x -q > gpurun_out/pytest_glue.log 2>&1
+      timeout 900 python -m pytest tests/test_gpu_glue.py tests/test_gpu_train.py tests/test_gpu_layer.py tests/test_cxx_api.py -x -q > gpurun_out/pytest_glue.log 2>&1
       echo "pytest rc=$?" >> gpurun_out/pytest_glue.log ;;
     block)
       timeout 900 python tools/bench_block.py --steps 10 > gpurun_out/bench_block.log 2>&1
