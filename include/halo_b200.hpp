@@ -9,8 +9,14 @@
 //
 // Tensors are device pointers (row-major, caller-owned).  Status codes are
 // rethrown as the reference's exception types: std::invalid_argument,
-// halo_b200::numeric_error (== halo::numeric_error, tensor.hpp:22-24),
-// std::logic_error, and std::runtime_error for CUDA failures.
+// numeric_error, std::logic_error, halo_b200::io_error (HALO_ERR_IO) and
+// std::runtime_error for CUDA / NCCL failures.
+//
+// numeric_error: define HALO_B200_REFERENCE_EXCEPTIONS before including this
+// header (with the reference's include dir on the path) and it IS
+// halo::numeric_error (tensor.hpp:21-23), so a reference caller's divergence
+// handler (halo_cli.cpp:730-732) catches it; otherwise a standalone type of
+// the same shape.
 #pragma once
 
 #include <stdexcept>
@@ -18,9 +24,20 @@
 
 #include "halo_b200.h"
 
+#ifdef HALO_B200_REFERENCE_EXCEPTIONS
+#include <halo/tensor.hpp>
+#endif
+
 namespace halo_b200 {
 
+#ifdef HALO_B200_REFERENCE_EXCEPTIONS
+using numeric_error = ::halo::numeric_error;
+#else
 struct numeric_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+#endif
+struct io_error : std::runtime_error {  // tensor_io.hpp:25-27
     using std::runtime_error::runtime_error;
 };
 
@@ -30,6 +47,7 @@ inline void check(halo_status s) {
     case HALO_ERR_INVALID_ARGUMENT: throw std::invalid_argument(halo_last_error());
     case HALO_ERR_NUMERIC: throw numeric_error(halo_last_error());
     case HALO_ERR_LOGIC: throw std::logic_error(halo_last_error());
+    case HALO_ERR_IO: throw io_error(halo_last_error());
     default: throw std::runtime_error(std::string("halo_b200: ") + halo_last_error());
     }
 }

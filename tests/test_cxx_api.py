@@ -73,3 +73,26 @@ def test_cxx_fsdp_driver_world1(orc, tmp_path):
     assert np.array_equal(np.fromfile(tmp_path / "Y.out", np.float32).reshape(b, n), want["Y"])
     assert np.array_equal(np.fromfile(tmp_path / "EX.out", np.float32).reshape(b, m), want["EX"])
     assert np.array_equal(np.fromfile(tmp_path / "GW0.out", np.float32).reshape(n, m), want["GW"])
+
+
+ADAPTER = os.path.join(ROOT, "oracle", "_ref", "integration_adapter")
+
+
+def test_integration_adapter_host():
+    """INTEGRATION.md §1 compiled against the reference headers: the C++ API
+    throws the reference's own halo::numeric_error (static_assert + catch)."""
+    if not os.path.exists(ADAPTER):
+        pytest.skip("adapter not built (needs /root/reference headers at build time)")
+    r = subprocess.run([ADAPTER], capture_output=True, text=True)
+    assert r.returncode == 0 and "0 failures" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_integration_adapter_matches_reference_layer():
+    """The adapter's HaloLinearLayer (device) vs the unmodified reference
+    HaloLinearLayer in the same process: Y, E_X, grad_W bit-identical."""
+    if not os.path.exists(ADAPTER):
+        pytest.skip("adapter not built")
+    r = subprocess.run([ADAPTER, "gpu"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "Y 0 E_X 0 grad_W 0 differing" in r.stdout
