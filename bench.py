@@ -302,7 +302,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fsdp", action="store_true", help="HQ-FSDP path even at N=1 (always on for N>1)")
-    ap.add_argument("--fsdp-gather", action="store_true", help="HQ-FSDP with NCCL all-gathers instead of peer reads")
+    ap.add_argument("--fsdp-gather", action="store_true",
+                    help="(default for N > 1) HQ-FSDP with INT8 all-gathers through the library's C++ NCCL data plane")
+    ap.add_argument("--fsdp-peer", action="store_true",
+                    help="HQ-FSDP over CUDA-IPC peer memory: GEMMs read peers' shards, G GEMM scatters dW rows")
+    ap.add_argument("--peer-staged", action="store_true",
+                    help="with --fsdp-peer: copy each peer shard once per step into a local buffer (bounded NVLink bytes)")
     ap.add_argument("--graph", action="store_true", help="replay the step as one captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -353,17 +358,18 @@ def main():
     x = x.to(bf)
     dy = (torch.randn(b, HIDDEN, generator=g, device=dev) * 1e-3).to(bf)
     scheme = halo.halo2(fmt, args.block)
-    use_fsdp = (world > 1 or args.fsdp or args.fsdp_gather) and not cfg1
+    use_fsdp = (world > 1 or args.fsdp or args.fsdp_gather or args.fsdp_peer) and not cfg1
+    args.fsdp_gather = use_fsdp and not args.fsdp_peer
     peer_error = None
     mlp = None
-    if use_fsdp and not args.fsdp_gather:
+    if use_fsdp and args.fsdp_peer:
         # HQ-FSDP over peer memory: shards read in place by the GEMMs.  If
         # CUDA IPC / peer access is unavailable on this node, every rank
         # agrees to fall back to the NCCL all-gather protocol (reported).
         from paper_2501_02625_b200.fsdp import PeerFsdpHaloMLP
         ok = 1
         try:
-            mlp = PeerFsdpHaloMLP(wg, wu, wd, scheme)
+            mlp = PeerFsdpHaloMLP(wg, wu, wd, scheme, staged=args.peer_staged)
         except Exception as exc:  # noqa: BLE001
             peer_error, ok = f"{type(exc).__name__}: {exc}"[:200], 0
         if world > 1:
@@ -380,7 +386,7 @@ def main():
         # HQ-FSDP: weights row-sharded over the ranks, INT8 (WH)_Q gathered for
         # the forward, regathered for the backward, dW reduce-scattered
         from paper_2501_02625_b200.fsdp import FsdpHaloMLP
-        mlp = FsdpHaloMLP(wg, wu, wd, scheme)
+        mlp = FsdpHaloMLP(wg, wu, wd, scheme, data_plane="torch" if one_gpu else "native")
     elif not use_fsdp:
         mlp = HaloLinearStep(wg[:HIDDEN], scheme) if cfg1 else HaloMLP(wg, wu, wd, scheme)
     ops_step = mlp.gemm_ops(b)
@@ -590,8 +596,9 @@ def main():
             "vs_baseline": None, "dtype": {halo.INT8: "int8", halo.FP8_E4M3: "fp8_e4m3", halo.FP6_E3M2: "fp6_e3m2"}[fmt], "data": "synthetic",
             "config": {"workload": CFG1_NAME if cfg1 else CONFIG_NAME, "global_batch": b * world, "seq_len": None,
                        "tokens_per_gpu": b, "hadamard_block": args.block,
-                       "parallelism": ((f"hq-fsdp{world} (INT8 weight all-gather + regather, bf16 dW "
-                                        f"reduce-scatter over NCCL)" if args.fsdp_gather else
+                       "parallelism": ((f"hq-fsdp{world} (INT8 weight all-gather + regather and bf16 dW "
+                                        f"reduce-scatter through the library's C++ NCCL data plane, on a side "
+                                        f"stream overlapping the GEMMs)" if args.fsdp_gather else
                                         f"hq-fsdp{world} (INT8 weight shards read in place over NVLink by the "
                                         f"GEMMs, device-mailbox absmax exchange, dW reduce-scatter fused into the G "
                                         f"GEMM: fp32 partial rows TMA-stored to their owners, owner-side "

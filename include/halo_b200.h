@@ -184,6 +184,14 @@ HALO_API halo_status halo_qmatmul_scaled(int32_t format, const uint8_t* a, int32
                                 int32_t a_per_row, const float* scale_b, int32_t b_per_row, void* out,
                                 int32_t out_kind, halo_stream_t stream);
 
+/* Granularity::row / ::column layers (scales on a contracted dim of E / G,
+ * or of F for column) are served by the reference's dequantized double
+ * products restated bit-exactly on the FP64 pipe (deq_gemm) -- a
+ * full-precision matmul, off the tensor-core contract path.  Creating such a
+ * layer returns HALO_ERR_INVALID_ARGUMENT unless this process-wide opt-in is
+ * on (default off). */
+HALO_API halo_status halo_allow_dequantized_products(int32_t on);
+
 /* ----------------------------------------------------------------- layer */
 
 typedef struct halo_linear halo_linear; /* HaloLinearLayerT, halo_linear.hpp:227 */

@@ -169,6 +169,8 @@ def lib():
     L.halo_rope_qkv.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]
     for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv"):
         getattr(L, fn).restype = C.c_int
+    L.halo_allow_dequantized_products.argtypes = [_i32]
+    L.halo_allow_dequantized_products.restype = C.c_int
     L.halo_fp6_pack.argtypes = [_vp, _vp, _i64, _vp]
     L.halo_fp6_unpack.argtypes = [_vp, _vp, _i64, _vp]
     L.halo_fp6_pack.restype = C.c_int
@@ -246,4 +248,5 @@ EXPORTS = (
     "halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
     "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
     "halo_fsdp_all_reduce_mean", "halo_fp6_pack", "halo_fp6_unpack",
+    "halo_allow_dequantized_products",
 )

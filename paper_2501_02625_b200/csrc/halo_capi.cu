@@ -673,11 +673,27 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
     return HALO_OK;
 }
 
+// Granularity::row / ::column backwards (and ::column forwards) are the
+// reference's dequantized double products (quantize.hpp:377-379), restated
+// bit-exactly on the FP64 pipe by deq_gemm -- a full-precision matmul that
+// north_star keeps off the contract path.  Opt-in only.
+static std::atomic<int> g_allow_deq{0};
+extern "C" halo_status halo_allow_dequantized_products(int32_t on) {
+    g_allow_deq.store(on ? 1 : 0);
+    return HALO_OK;
+}
+
 extern "C" halo_status halo_linear_create(const halo_scheme* scheme, const void* w, int32_t w_dtype,
                                           int64_t out_features, int64_t in_features, halo_linear** out) {
     if (!scheme || !out) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     if (!valid_dtype(w_dtype)) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad weight dtype");
     if (validate_scheme(*scheme, in_features, out_features) != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    if (scheme->granularity != HALO_GRAN_TENSOR && !g_allow_deq.load())
+        return fail(HALO_ERR_INVALID_ARGUMENT,
+                    "halo layer: row / column granularity puts scales on a contracted dim, where the reference "
+                    "multiplies dequantized values in double (quantize.hpp:377-379); that full-precision product "
+                    "(deq_gemm, FP64 pipe, ~80x slower than the tensor-core path) is opt-in: "
+                    "halo_allow_dequantized_products(1)");
     auto* l = new halo_linear();
     l->s = *scheme;
     l->m = in_features;

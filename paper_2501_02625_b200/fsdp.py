@@ -381,9 +381,18 @@ class FsdpHaloMLP:
     """Llama MLP block (mlp.HaloMLP) with HQ-FSDP weights: each rank keeps a
     row shard of gate/up/down; every step gathers the INT8 (WH)_Q codes for
     the forward, regathers them for the backward under the saved scale, and
-    reduce-scatters the weight gradients (the loop of hqfsdp.hpp:361-411)."""
+    reduce-scatters the weight gradients (the loop of hqfsdp.hpp:361-411).
 
-    def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16):
+    data_plane="native" runs the collectives through the library's C++ NCCL
+    data plane (NcclDataPlane, halo_fsdp_*), "torch" through the protocol
+    functions above on torch.distributed.  With `overlap` the gathers /
+    regathers of all three weights are issued up front on a side stream and
+    each projection waits only for its own codes; each dW reduce-scatter
+    starts on that stream as soon as its G GEMM is done, behind the next
+    projection's backward."""
+
+    def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16,
+                 data_plane: str | None = "native", overlap: bool = True):
         from .mlp import HaloMLP
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -400,31 +409,92 @@ class FsdpHaloMLP:
         self.buffers = [torch.empty((p.shard_rows * p.world, p.cols), dtype=code_dt, device=p.master.device)
                         for p in self.params]
         self.ledger = CommLedger()
+        self.plane = NcclDataPlane(group) if data_plane == "native" else None
+        dev = self.params[0].master.device
+        self.overlap = overlap
+        self.comm = torch.cuda.Stream(device=dev) if overlap else None
+        self.ready = {n: torch.cuda.Event() for n in ("gate", "up", "down")}
+        self.stale = torch.zeros(1, dtype=torch.int32 if self.plane else torch.float32, device=dev)
+        self._shards = {}
 
     @property
     def layers(self):
         return (self.mlp.gate, self.mlp.up, self.mlp.down)
 
+    _IDX = {"gate": 0, "up": 1, "down": 2}
+
     def _install(self, layer, codes, scale, rows):
         layer.set_qweight(codes[:rows], scale)
 
+    def _fetch_all(self, regather: bool, order):
+        main = torch.cuda.current_stream()
+        side = self.comm if self.overlap else main
+        side.wait_stream(main)  # masters written / buffers last read before this point
+        with torch.cuda.stream(side):
+            for name in order:
+                i = self._IDX[name]
+                p, buf, layer = self.params[i], self.buffers[i], self.layers[i]
+                if regather:
+                    if self.plane is not None:
+                        codes, scale = self.plane.regather(p, self.rotate, self.block, buf, self.ledger,
+                                                           self.stale if self.check_stale else None)
+                    else:
+                        codes, scale = backward_regather(p, self.rotate, self.ledger, self.check_stale, self.block,
+                                                         self.group, out=buf)
+                    self.ledger.backward_consumers += 1
+                elif self.plane is not None:
+                    codes, scale = self.plane.gather(p, self.rotate, self.block, buf, self.ledger)
+                else:
+                    codes, scale = quantized_all_gather(p, self.rotate, self.ledger, self.block, self.group, out=buf)
+                self._install(layer, codes, scale, p.full_rows)
+                self.ready[name].record(side)
+
+    def _wait(self, name, phase):
+        torch.cuda.current_stream().wait_event(self.ready[name])
+
+    def _rs(self, name, grad):
+        i = self._IDX[name]
+        p = self.params[i]
+        if grad is None:
+            return None
+        main = torch.cuda.current_stream()
+        side = self.comm if self.overlap else main
+        side.wait_stream(main)  # the G GEMM wrote grad
+        with torch.cuda.stream(side):
+            if self.plane is not None:
+                out = self.plane.reduce_scatter(grad, p, self.ledger)
+            else:
+                out = reduce_scatter_grads(grad, p, self.ledger, self.group)
+            grad.record_stream(side)
+            out.record_stream(side)
+        return out
+
     def forward(self, x):
-        for layer, p, buf in zip(self.layers, self.params, self.buffers):
-            codes, scale = quantized_all_gather(p, self.rotate, self.ledger, self.block, self.group, out=buf)
-            self._install(layer, codes, scale, p.full_rows)
+        if self.plane is not None and self.check_stale:
+            self.stale.zero_()
+        self._fetch_all(False, ("gate", "up", "down"))
+        self.mlp.pre = self._wait
+        self.mlp.post_grad = None
         return self.mlp.forward(x)
 
     def backward(self, dy):
-        for layer, p, buf in zip(self.layers, self.params, self.buffers):
-            codes, scale = backward_regather(p, self.rotate, self.ledger, self.check_stale, self.block, self.group,
-                                             out=buf)
-            self.ledger.backward_consumers += 1
-        dx, grads = self.mlp.backward(dy)
-        shards = [reduce_scatter_grads(g, p, self.ledger, self.group) for g, p in zip(grads, self.params)]
-        return dx, shards
+        self._fetch_all(True, ("down", "gate", "up"))
+        self.mlp.pre = self._wait
+        self.mlp.post_grad = self._rs
+        dx, shards = self.mlp.backward(dy)
+        if self.overlap:
+            torch.cuda.current_stream().wait_stream(self.comm)
+        if self.plane is not None and self.check_stale:
+            check_stale_flag(self.stale, self.group)
+        return dx, list(shards)
 
     def gemm_ops(self, tokens):
         return self.mlp.gemm_ops(tokens)
+
+    def close(self):
+        torch.cuda.synchronize()
+        if self.plane is not None:
+            self.plane.close()
 
 
 # ------------------------------------------------- peer-memory HQ-FSDP --
@@ -500,10 +570,21 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
     receive slot over NVLink, and after one mailbox barrier the owner takes
     the rank-order double mean -- the reference's arithmetic, bit for bit.
     Needs out_features % (world * 256) == 0 for every projection.
+
+    staged=True bounds the NVLink bytes: right after the "shards written"
+    barrier every rank copies each peer's shard once into a local gathered
+    buffer (copy engine, cudaMemcpyAsync over the IPC mapping) and the GEMMs
+    read that local copy -- (world-1)/world * n*m code bytes per weight and
+    step cross NVLink, independent of the GEMM's tile raster (the in-place
+    reads fetch a B panel once per M-tile unless it hits in L2).  Results are
+    bit-identical either way (the same codes feed the same GEMMs).
     """
 
-    def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16):
-        super().__init__(w_gate, w_up, w_down, scheme, group, check_stale, grad_dtype)
+    def __init__(self, w_gate, w_up, w_down, scheme, group=None, check_stale=False, grad_dtype=torch.bfloat16,
+                 staged: bool = False):
+        super().__init__(w_gate, w_up, w_down, scheme, group, check_stale, grad_dtype, data_plane=None,
+                         overlap=False)
+        self.staged = staged
         from ._lib import HALO_OK  # noqa: F401  (library loaded)
         for p in self.params:
             if p.pad_rows or p.shard_rows % 256:
@@ -552,9 +633,29 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
                     row.append(ptr)
             self.recv_parts.append(row)
         self.epoch = 0
-        for layer, parts, scale, recv in zip(self.layers, self.parts, self.scales, self.recv_parts):
-            layer.set_qweight_sharded(parts, scale, keepalive=self)
+        self.staging = []
+        if staged:
+            self.staging = [torch.empty((p.shard_rows * self.world, p.cols), dtype=code_dt, device=dev)
+                            for p in self.params]
+        for i, (layer, parts, scale, recv) in enumerate(zip(self.layers, self.parts, self.scales, self.recv_parts)):
+            if staged:
+                layer.set_qweight(self.staging[i], scale)
+            else:
+                layer.set_qweight_sharded(parts, scale, keepalive=self)
             layer.set_grad_scatter(recv, self.rank)
+
+    def _stage(self):
+        """Copy every peer's shard into the local gathered buffers (NVLink,
+        copy engine), stream-ordered after the shards-written barrier."""
+        import ctypes as C
+        from . import halo
+        from ._lib import check, lib
+        for i, p in enumerate(self.params):
+            nb = p.shard_rows * p.cols
+            base = self.staging[i].data_ptr()
+            for j in range(self.world):
+                check(lib().halo_device_copy(C.c_void_p(base + j * nb), C.c_void_p(self.parts[i][j]), nb,
+                                             halo._stream()))
 
     def _sync(self, amax_in=None, amax_out=None):
         import ctypes as C
@@ -588,6 +689,8 @@ class PeerFsdpHaloMLP(FsdpHaloMLP):
             self.ledger.record(self.ledger.gather, code_payload_bytes(p.format, elems) + K_SCALE_BYTES, p.world)
             self.ledger.bf16_gather_payload += 2 * elems
         self._sync()  # every rank's shards written before any peer GEMM reads them
+        if self.staged:
+            self._stage()
         return self.mlp.forward(x)
 
     def backward(self, dy):

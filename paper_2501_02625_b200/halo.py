@@ -246,6 +246,14 @@ def qmatmul(a: torch.Tensor, b: torch.Tensor, scale_a: torch.Tensor, scale_b: to
     return c
 
 
+def allow_dequantized_products(on: bool = True):
+    """Opt in to row / column granularity layers, whose contracted-dim scales
+    make the reference multiply dequantized values in double
+    (quantize.hpp:377-379): served bit-exactly on the FP64 pipe (deq_gemm),
+    off the tensor-core path.  Process-wide; off by default."""
+    check(lib().halo_allow_dequantized_products(1 if on else 0))
+
+
 # ------------------------------------------------------ FP6 wire format
 
 def fp6_pack(codes: torch.Tensor) -> torch.Tensor:

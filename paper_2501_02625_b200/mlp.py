@@ -39,10 +39,26 @@ class HaloMLP:
         self.fuse_fwd = os.environ.get("HALO_MLP_FUSE_FWD", "0") == "1"
         # tests: a dict here collects the step's intermediate tensors
         self.trace = None
+        # HQ-FSDP hooks: pre(name, phase) runs before a projection's GEMMs
+        # (waits for its gathered codes), post_grad(name, grad_w) right after
+        # its backward (launches its reduce-scatter)
+        self.pre = None
+        self.post_grad = None
+
+    def _pre(self, name, phase):
+        if self.pre is not None:
+            self.pre(name, phase)
+
+    def _post(self, name, grad):
+        if self.post_grad is not None:
+            return self.post_grad(name, grad)
+        return grad
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self._pre("gate", "fwd")
         g = self.gate.forward(x, self.ctx[0])
         # up_proj sees the same X under the same quantizer: reuse gate's (XH)_Q
+        self._pre("up", "fwd")
         u = self.up.forward_shared(self.ctx[0], self.ctx[1]) if self.share_x else self.up.forward(x, self.ctx[1])
         h = torch.empty_like(g)
         if self.fuse_fwd:
@@ -52,6 +68,7 @@ class HaloMLP:
         else:
             check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
         self._act = (g, u)
+        self._pre("down", "fwd")
         y = self.down.forward(h, self.ctx[2])
         if self.trace is not None:
             self.trace.update(g=g, u=u, h=h, y=y)
@@ -60,7 +77,9 @@ class HaloMLP:
     def backward(self, dy: torch.Tensor, need_grad_w: bool = True):
         """Returns (dx, (dW_gate, dW_up, dW_down))."""
         g, u = self._act
+        self._pre("down", "bwd")
         bd = self.down.backward(self.ctx[2], dy, need_grad_w)
+        gd = self._post("down", bd.grad_w)
         dg = torch.empty_like(g)
         du = torch.empty_like(u)
         if self.fuse_glue:
@@ -70,14 +89,18 @@ class HaloMLP:
         else:
             check(lib().halo_swiglu_backward(halo._ptr(bd.e_x), halo._ptr(g), halo._ptr(u), halo._ptr(dg),
                                              halo._ptr(du), g.numel(), halo._stream()))
+        self._pre("gate", "bwd")
         bg = self.gate.backward(self.ctx[0], dg, need_grad_w)
+        gg = self._post("gate", bg.grad_w)
+        self._pre("up", "bwd")
         bu = self.up.backward(self.ctx[1], du, need_grad_w)
+        gu = self._post("up", bu.grad_w)
         dx = torch.empty_like(bg.e_x)
         check(lib().halo_add(halo._ptr(bg.e_x), halo._ptr(bu.e_x), halo._ptr(dx), DTYPE_BF16, dx.numel(),
                              halo._stream()))
         if self.trace is not None:
             self.trace.update(dh=bd.e_x, dg=dg, du=du, ex_gate=bg.e_x, ex_up=bu.e_x)
-        return dx, (bg.grad_w, bu.grad_w, bd.grad_w)
+        return dx, (gg, gu, gd)
 
     def gemm_ops(self, tokens: int) -> float:
         """Integer ops of the three quantized GEMM triples: 6*b*m*n each."""

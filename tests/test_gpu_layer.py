@@ -21,6 +21,7 @@ def H():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2501_02625_b200 import halo
+    halo.allow_dequantized_products(True)  # row / column granularity layers below
     return halo
 
 

@@ -149,3 +149,29 @@ def test_mlp_fused_forward_glue_bitexact(M, fmt):
     for u, v in zip(a[2], b[2]):
         assert torch.equal(u, v)
 
+
+
+@pytest.mark.parametrize("plane", ["native", "torch"])
+def test_fsdp_mlp_world1_matches_mlp(M, plane):
+    """FsdpHaloMLP at world 1 (gathers / regathers on a side stream, each
+    projection waiting for its own codes, reduce-scatters behind the next
+    backward) -- through the library's C++ NCCL data plane or torch.distributed
+    -- gives the same bits as the plain HaloMLP."""
+    halo, mlp = M
+    from paper_2501_02625_b200.fsdp import FsdpHaloMLP
+    wg, wu, wd, g = _weights(1024, 512)
+    x = torch.randn(512, 512, generator=g, device="cuda").to(torch.bfloat16)
+    dy = (torch.randn(512, 512, generator=g, device="cuda") * 1e-3).to(torch.bfloat16)
+    ref = mlp.HaloMLP(wg, wu, wd, halo.halo2(0, 256))
+    f = FsdpHaloMLP(wg, wu, wd, halo.halo2(0, 256), grad_dtype=torch.float32, data_plane=plane, check_stale=True)
+    for _ in range(2):
+        y0 = ref.forward(x)
+        dx0, g0 = ref.backward(dy)
+        y1 = f.forward(x)
+        dx1, g1 = f.backward(dy)
+        torch.cuda.synchronize()
+        assert torch.equal(y0, y1) and torch.equal(dx0, dx1)
+        for a, b in zip(g0, g1):
+            assert torch.equal(a, b)
+    assert f.ledger.backward_gathers == 6 and f.ledger.gather.count == 12
+    f.close()

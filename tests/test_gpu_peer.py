@@ -139,7 +139,7 @@ def _mlp_data(rank=0, H=512, I=1024, T=512):
     return wg, wu, wd, x, dy
 
 
-def _peer_worker(rank, world, port, out_dir):
+def _peer_worker(rank, world, port, out_dir, staged=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -148,7 +148,7 @@ def _peer_worker(rank, world, port, out_dir):
     from paper_2501_02625_b200 import halo
     from paper_2501_02625_b200.fsdp import PeerFsdpHaloMLP
     wg, wu, wd, x, dy = _mlp_data(rank)
-    mlp = PeerFsdpHaloMLP(wg, wu, wd, halo.halo2(0, 256), grad_dtype=torch.float32)
+    mlp = PeerFsdpHaloMLP(wg, wu, wd, halo.halo2(0, 256), grad_dtype=torch.float32, staged=staged)
     outs = []
     for _ in range(2):  # two steps: the second re-quantizes shards peers read in the first
         y = mlp.forward(x)
@@ -161,13 +161,16 @@ def _peer_worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_peer_fsdp_two_processes(H, tmp_path):
+@pytest.mark.parametrize("staged", [False, True])
+def test_peer_fsdp_two_processes(H, tmp_path, staged):
+    """In-place peer reads and the staged copy (one NVLink copy of each peer
+    shard per step) give the same bits as the single-process MLP."""
     import torch.multiprocessing as mp
     from paper_2501_02625_b200.mlp import HaloMLP
     world = 2
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, str(tmp_path))) for r in range(world)]
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, str(tmp_path), staged)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -29,6 +29,7 @@ for fmt in (halo.INT8, halo.FP8_E4M3):
         layer.backward(ctx, e)
         ctx.check()
 # row granularity: deq_gemm backward
+halo.allow_dequantized_products(True)
 layer = halo.HaloLinearLayer(w, halo.halo2(halo.INT8, 256, halo.GRAN_ROW), out_dtype=torch.float32)
 ctx = halo.SavedContext()
 layer.forward(x, ctx)
