@@ -46,8 +46,8 @@ for w in $what; do
       timeout 600 ncu --set full --clock-control none -k regex:k_rows_v -s 4 -c 2 \
         -f -o gpurun_out/prof_k1 python tools/bench_kernels.py k1 --reps 1 > gpurun_out/prof_k1.log 2>&1 ;;
     prof_k2)
-      timeout 600 ncu --set full --clock-control none -k regex:k_cols_v -s 8 -c 2 \
-        -f -o gpurun_out/prof_k2 python tools/bench_kernels.py k2 --reps 1 > gpurun_out/prof_k2.log 2>&1 ;;
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cols_v -s 0 -c 6 \
+        -f -o gpurun_out/prof_k2 python tools/prof_step.py 1 > gpurun_out/prof_k2.log 2>&1 ;;
     prof_gemm)
       timeout 600 ncu --set full --clock-control none -k regex:k_gemm -s 3 -c 3 \
         -f -o gpurun_out/prof_gemm python tools/bench_kernels.py gemm --reps 1 > gpurun_out/prof_gemm.log 2>&1 ;;
@@ -55,6 +55,8 @@ for w in $what; do
       # one host core, ~9 min: runs in the background while the GPU work proceeds
       (timeout 1500 taskset -c 0 python tools/cpu_ref_cfg1.py > gpurun_out/cpu_ref_cfg1.json 2> gpurun_out/cpu_ref_cfg1.err) &
       CPUREF_PID=$! ;;
+    bench_fsdp)
+      timeout 600 python bench.py --fsdp --no-cpu-baseline > gpurun_out/bench_fsdp.log 2>&1; echo "rc=$?" >> gpurun_out/bench_fsdp.log ;;
     bench_cfg1)
       timeout 600 python bench.py --config cfg1 > gpurun_out/bench_cfg1.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_cfg1.log ;;
     traffic)
