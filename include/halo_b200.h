@@ -53,9 +53,16 @@ typedef enum halo_status {
     HALO_ERR_IO = 6 /* io_error, tensor_io.hpp:25-27 */
 } halo_status;
 
-/* NumericFormat ids, quantize.hpp:22-29 (FP6/MX/BF16/IDENTITY emulation is
- * not part of this path and is rejected). */
-typedef enum halo_format { HALO_FMT_INT8 = 0, HALO_FMT_FP8_E4M3 = 1, HALO_FMT_FP6_E3M2 = 2 } halo_format;
+/* NumericFormat ids, quantize.hpp:22-29.  MXFP6 = E3M2 codes under a
+ * power-of-two scale (compute_scales' MX rule, quantize.hpp:224-232) --
+ * per-tensor here; the 1 x 32 block granularity (Granularity::mx) and the
+ * BF16 / IDENTITY emulations are not on the device path. */
+typedef enum halo_format {
+    HALO_FMT_INT8 = 0,
+    HALO_FMT_FP8_E4M3 = 1,
+    HALO_FMT_FP6_E3M2 = 2,
+    HALO_FMT_MXFP6_E3M2 = 3
+} halo_format;
 
 typedef enum halo_dtype { HALO_DTYPE_F32 = 0, HALO_DTYPE_BF16 = 1 } halo_dtype;
 
@@ -165,6 +172,8 @@ HALO_API halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int32
 #define HALO_GRAN_TENSOR 0
 #define HALO_GRAN_ROW 1
 #define HALO_GRAN_COLUMN 2 /* INT8 / FP8; every product is the dequantized double matmul (deq_gemm) */
+#define HALO_GRAN_MX 4     /* 1 x 32 blocks along rows, with HALO_FMT_MXFP6_E3M2 only (quantize.hpp:247-250);
+                              power-of-two block scales, every product the dequantized double matmul (deq_gemm) */
 
 /* quantize(transform_right(a, block), fmt, Granularity::row()): one scale per
  * row (compute_scales per group, quantize.hpp:202-239); codes bit-exact.
@@ -172,6 +181,16 @@ HALO_API halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int32
 HALO_API halo_status halo_rotate_quantize_rows(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
                                       int64_t had_block, int32_t format, uint8_t* codes, float* scales_out,
                                       halo_stream_t stream);
+
+/* quantize([transform_right](A), mxfp6_e3m2, Granularity::mx()): power-of-two
+ * scales per 1 x 32 block along rows (quantize.hpp:224-232), E3M2 codes in
+ * bits 7:2; scales [rows x ceil(cols/32)].  had_block < 0: no rotation.
+ * transpose_in != 0: A is the (cols x rows) row-major tensor and its
+ * transpose is quantized (the gradient path's quantize(transpose(E_Y)),
+ * halo_linear.hpp:427-431); no rotation then. */
+HALO_API halo_status halo_rotate_quantize_mx(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                             int64_t had_block, int32_t transpose_in, uint8_t* codes, float* scales,
+                                             halo_stream_t stream);
 
 /* qmatmul with row-granularity operands whose scales sit on non-contracted
  * dims: a_per_row != 0 -> scale_a has M entries (rows of C), b_per_row != 0

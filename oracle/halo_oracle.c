@@ -88,6 +88,7 @@ static double format_max(int fmt) {
     case ORC_INT8: return 127.0;
     case ORC_FP8_E4M3: return 448.0;
     case ORC_FP6_E3M2: return 28.0;
+    case ORC_MXFP6_E3M2: return 28.0;
     }
     return 0.0;
 }
@@ -114,9 +115,24 @@ double orc_round_code(double x, int fmt) {
         return q + 0.0;
     }
     case ORC_FP8_E4M3: return round_minifloat(x, 3, -6, 448.0);
-    case ORC_FP6_E3M2: return round_minifloat(x, 2, -2, 28.0);
+    case ORC_FP6_E3M2:
+    case ORC_MXFP6_E3M2: return round_minifloat(x, 2, -2, 28.0);
     }
     return x;
+}
+
+/* quantize.hpp:219-237: the scale of one group from its absmax; MX formats
+ * take the smallest power of two keeping absmax / s <= fmax (:224-232) */
+static float group_scale(double m, int fmt) {
+    if (m == 0.0) return 1.0f;
+    if (fmt == ORC_MXFP6_E3M2) {
+        const double fmax = format_max(fmt);
+        int e = ilogb(m / fmax);
+        if (m / ldexp(1.0, e) > fmax) ++e;
+        if (e < -126) e = -126;
+        return (float)ldexp(1.0, e);
+    }
+    return (float)(m / format_max(fmt));
 }
 
 /* quantize.hpp:202-239, per-tensor group */
@@ -129,29 +145,38 @@ float orc_tensor_scale(const float* a, int64_t n, int fmt, int* nonfinite) {
         if (v > m) m = v;
     }
     if (nonfinite) *nonfinite = bad;
-    if (m == 0.0) return 1.0f;
-    return (float)(m / format_max(fmt));
+    return group_scale(m, fmt);
 }
 
 /* quantize.hpp:244-280 (+ compute_scales :202-239 for row / column groups) */
+/* group_count / group_of (quantize.hpp:110-132): tensor 0, row 1, column 2,
+ * mx 4 (32 consecutive elements along each row) */
+static int64_t mx_blocks(int64_t cols) { return (cols + 31) / 32; }
+static int64_t group_count(int gran, int64_t rows, int64_t cols) {
+    return gran == 0 ? 1 : gran == 1 ? rows : gran == 2 ? cols : rows * mx_blocks(cols);
+}
+static int64_t group_of(int gran, int64_t cols, int64_t i, int64_t j) {
+    return gran == 0 ? 0 : gran == 1 ? i : gran == 2 ? j : i * mx_blocks(cols) + j / 32;
+}
+
 void orc_quantize(const float* a, int64_t rows, int64_t cols, int fmt, int gran,
                   int supplied, float* scales, float* codes) {
     if (!supplied) {
-        const int64_t groups = gran == 0 ? 1 : (gran == 1 ? rows : cols);
+        const int64_t groups = group_count(gran, rows, cols);
         double* absmax = (double*)calloc((size_t)groups, sizeof(double));
         for (int64_t i = 0; i < rows; ++i)
             for (int64_t j = 0; j < cols; ++j) {
-                const int64_t g = gran == 0 ? 0 : (gran == 1 ? i : j);
+                const int64_t g = group_of(gran, cols, i, j);
                 const double v = fabs((double)a[i * cols + j]);
                 if (v > absmax[g]) absmax[g] = v;
             }
         for (int64_t g = 0; g < groups; ++g)
-            scales[g] = absmax[g] == 0.0 ? 1.0f : (float)(absmax[g] / format_max(fmt));
+            scales[g] = group_scale(absmax[g], fmt);
         free(absmax);
     }
     for (int64_t i = 0; i < rows; ++i)
         for (int64_t j = 0; j < cols; ++j) {
-            const int64_t g = gran == 0 ? 0 : (gran == 1 ? i : j);
+            const int64_t g = group_of(gran, cols, i, j);
             const double s = scales[g];
             codes[i * cols + j] = (float)orc_round_code((double)a[i * cols + j] / s, fmt);
         }

@@ -28,7 +28,7 @@ extern "C" {
 #endif
 
 /* format ids follow NumericFormat (quantize.hpp:22-29) */
-enum { ORC_INT8 = 0, ORC_FP8_E4M3 = 1, ORC_FP6_E3M2 = 2 };
+enum { ORC_INT8 = 0, ORC_FP8_E4M3 = 1, ORC_FP6_E3M2 = 2, ORC_MXFP6_E3M2 = 3 };
 
 /* hadamard.hpp:69-93 */
 int orc_is_supported_hadamard_dim(int64_t d);

@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libhalo_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhalo_ref.so")
 
-INT8, FP8_E4M3, FP6_E3M2 = 0, 1, 2
+INT8, FP8_E4M3, FP6_E3M2, MXFP6_E3M2 = 0, 1, 2, 3
 
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
@@ -159,10 +159,15 @@ def fwht_cols(a, block):
     return out
 
 
+def _groups(gran, rows, cols):
+    return 1 if gran == 0 else rows if gran == 1 else cols if gran == 2 else rows * ((cols + 31) // 32)
+
+
 def quantize(a, fmt=INT8, gran=0, scales=None):
+    """gran: 0 tensor, 1 row, 2 column, 4 mx (1 x 32 blocks along rows)."""
     a = f32(a)
     rows, cols = a.shape
-    groups = 1 if gran == 0 else (rows if gran == 1 else cols)
+    groups = _groups(gran, rows, cols)
     s = np.zeros(groups, np.float32) if scales is None else f32(np.atleast_1d(scales)).copy()
     codes = np.zeros_like(a)
     orc().orc_quantize(a, rows, cols, fmt, gran, 0 if scales is None else 1, s, codes)
@@ -186,7 +191,7 @@ def codes_to_bytes(codes, fmt):
     if fmt == INT8:
         out = np.empty(codes.shape, np.int8)
         orc().orc_codes_to_int8(codes, codes.size, out)
-    elif fmt == FP6_E3M2:
+    elif fmt in (FP6_E3M2, MXFP6_E3M2):
         table = e3m2_table()
         lut = {}
         for c in range(63, -1, -1):  # 0.0 -> code 0 (the reference's +0)
@@ -288,7 +293,7 @@ def ref_fwht_cols(a, block):
 def ref_quantize(a, fmt=INT8, gran=0, scales=None):
     a = f32(a)
     rows, cols = a.shape
-    groups = 1 if gran == 0 else (rows if gran == 1 else cols)
+    groups = _groups(gran, rows, cols)
     s = np.zeros(groups, np.float32) if scales is None else f32(np.atleast_1d(scales)).copy()
     codes = np.zeros_like(a)
     L = ref()

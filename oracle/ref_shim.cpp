@@ -66,6 +66,7 @@ Granularity gran_of(int g) {
     switch (g) {
     case 1: return Granularity::row();
     case 2: return Granularity::column();
+    case 4: return Granularity::mx();
     default: return Granularity::tensor();
     }
 }
@@ -168,7 +169,7 @@ int ref_linear_g(int level, int fmt, long long block, int gran, long long b, lon
                  float* xq, float* sx, float* wq, float* sw) {
     return guard([&] {
         const Tensor x = make(X, b, m), w = make(W, n, m), ey = make(EY, b, n);
-        const Granularity g = gran == 2 ? Granularity::column() : gran ? Granularity::row() : Granularity::tensor();
+        const Granularity g = gran_of(gran);
         const HaloScheme scheme = level == 0 ? halo0(fmt_of(fmt), g) : level == 1 ? halo1(fmt_of(fmt), g)
                                                                                  : halo2(fmt_of(fmt), g);
         if (block == 0) {
@@ -205,7 +206,9 @@ int ref_linear_g(int level, int fmt, long long block, int gran, long long b, lon
         if (level >= 1) prod = right_blocked(prod, block, true);
         put(prod, EX);
         // gradient path :418-439
-        Tensor gw = qmatmul(transpose_quantized(qe), qx);
+        // MX blocks do not transpose: quantize the transpose itself (:427-431)
+        Tensor gw = qmatmul(g.kind == GranularityKind::MxBlock ? quantize(transpose(ey), f, g) : transpose_quantized(qe),
+                            qx);
         if (level >= 1) gw = right_blocked(gw, block, true);
         put(gw, GW);
         std::memcpy(xq, qx.codes.data(), sizeof(float) * qx.codes.size());

@@ -23,6 +23,7 @@ HALO_ERR_IO = 6
 FMT_INT8 = 0
 FMT_FP8_E4M3 = 1
 FMT_FP6_E3M2 = 2  # one E3M2 code per byte, in bits 7:2 (the tcgen05 kind::f8f6f4 operand form)
+FMT_MXFP6_E3M2 = 3  # E3M2 codes as FP6, power-of-two scale (quantize.hpp:224-232)
 DTYPE_F32 = 0
 DTYPE_BF16 = 1
 OUT_F32, OUT_BF16, OUT_S32 = 0, 1, 2
@@ -169,6 +170,8 @@ def lib():
     L.halo_rope_qkv.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]
     for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv"):
         getattr(L, fn).restype = C.c_int
+    L.halo_rotate_quantize_mx.argtypes = [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp]
+    L.halo_rotate_quantize_mx.restype = C.c_int
     L.halo_allow_dequantized_products.argtypes = [_i32]
     L.halo_allow_dequantized_products.restype = C.c_int
     L.halo_fp6_pack.argtypes = [_vp, _vp, _i64, _vp]
@@ -248,5 +251,5 @@ EXPORTS = (
     "halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
     "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
     "halo_fsdp_all_reduce_mean", "halo_fp6_pack", "halo_fp6_unpack",
-    "halo_allow_dequantized_products",
+    "halo_allow_dequantized_products", "halo_rotate_quantize_mx",
 )

@@ -36,6 +36,7 @@ constexpr int DG_TM = 8, DG_TN = 4, DG_BM = 16 * DG_TM, DG_BN = 16 * DG_TN, DG_B
 template <int FMT>
 __device__ __forceinline__ float code_value(uint8_t c) {
     if (FMT == FMT_INT8) return (float)(int8_t)c;
+    if (FMT == FMT_E3M2) return e3m2_to_float((uint8_t)(c >> 2));  // bits 7:2 (MXFP6 codes)
     const float mag = e4m3_mag(c & 0x7Fu);
     return (c & 0x80u) ? -mag : mag;
 }
@@ -52,6 +53,7 @@ struct DeqView {
     const float* scale;
     int64_t s0, s1;    // element strides (row index, k) for A; (k, col index) for B
     int64_t ss0, ss1;  // scale strides, same index pair
+    int sh0, sh1;      // the scale index uses (index >> sh): 5 for the 32-wide MX blocks (quantize.hpp:129)
 };
 
 // 128 x 64 output tile per CTA, 8 x 4 per thread (rows tr + 16 r, columns
@@ -82,7 +84,8 @@ __global__ void __launch_bounds__(DG_THREADS, 2) k_deq_gemm(DeqView A, DeqView B
             if (A.s1 == 1) { kk = idx % DG_BK; ii = idx / DG_BK; } else { ii = idx % DG_BM; kk = idx / DG_BM; }
             const int64_t gi = i0 + ii, gk = k0 + kk;
             double v = 0.0;
-            if (gi < M && gk < K) v = deq<FMT>(A.codes[gi * A.s0 + gk * A.s1], A.scale[gi * A.ss0 + gk * A.ss1]);
+            if (gi < M && gk < K)
+                v = deq<FMT>(A.codes[gi * A.s0 + gk * A.s1], A.scale[(gi >> A.sh0) * A.ss0 + (gk >> A.sh1) * A.ss1]);
             As[kk][ii] = v;
         }
 #pragma unroll
@@ -92,7 +95,8 @@ __global__ void __launch_bounds__(DG_THREADS, 2) k_deq_gemm(DeqView A, DeqView B
             if (B.s1 == 1) { jj = idx % DG_BN; kk = idx / DG_BN; } else { kk = idx % DG_BK; jj = idx / DG_BK; }
             const int64_t gj = j0 + jj, gk = k0 + kk;
             double w = 0.0;
-            if (gj < N && gk < K) w = deq<FMT>(B.codes[gk * B.s0 + gj * B.s1], B.scale[gk * B.ss0 + gj * B.ss1]);
+            if (gj < N && gk < K)
+                w = deq<FMT>(B.codes[gk * B.s0 + gj * B.s1], B.scale[(gk >> B.sh0) * B.ss0 + (gj >> B.sh1) * B.ss1]);
             Bs[kk][jj] = w;
         }
         __syncthreads();
@@ -204,15 +208,80 @@ void pad_rows_f32(const void* in, int in_dtype, int64_t b, int64_t b_pad, int64_
 
 bool deq_gemm(int fmt, const uint8_t* a, const float* as, int64_t a_si, int64_t a_sk, int64_t as_si, int64_t as_sk,
               const uint8_t* b, const float* bs, int64_t b_sk, int64_t b_sj, int64_t bs_sk, int64_t bs_sj, float* c,
-              int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
-    if (fmt != FMT_INT8 && fmt != FMT_E4M3) return false;
+              int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st, int a_sh_i, int a_sh_k, int b_sh_k,
+              int b_sh_j) {
+    fmt = code_format(fmt);
+    if (fmt != FMT_INT8 && fmt != FMT_E4M3 && fmt != FMT_E3M2) return false;
     if (M <= 0 || N <= 0) return true;
-    const DeqView A{a, as, a_si, a_sk, as_si, as_sk}, B{b, bs, b_sk, b_sj, bs_sk, bs_sj};
+    const DeqView A{a, as, a_si, a_sk, as_si, as_sk, a_sh_i, a_sh_k}, B{b, bs, b_sk, b_sj, bs_sk, bs_sj, b_sh_k, b_sh_j};
     const dim3 grid((unsigned)((N + DG_BN - 1) / DG_BN), (unsigned)((M + DG_BM - 1) / DG_BM));
     if (fmt == FMT_INT8)
         launch_pdl(k_deq_gemm<FMT_INT8>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
+    else if (fmt == FMT_E3M2)
+        launch_pdl(k_deq_gemm<FMT_E3M2>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
     else
         launch_pdl(k_deq_gemm<FMT_E4M3>, grid, dim3(DG_THREADS), 0, st, A, B, c, M, N, K, ldc);
+    return cudaPeekAtLastError() == cudaSuccess;
+}
+
+// Granularity::mx quantization of NumericFormat::MxFp6E3M2 (quantize.hpp:
+// 202-280): per 1 x 32 block along each row, absmax (exact), power-of-two
+// scale by the MX rule (:224-232: e = ilogb(m/28), +1 if m/2^e > 28, >= -126;
+// 1 for an all-zero block), codes round_code(x / s, Fp6E3M2) by the exact
+// E3M2 quantizer, stored in bits 7:2.  The input is a strided view
+// in[r * rs + c * cs] (cs != 1: quantize(transpose(E_Y)), :427-431); one
+// thread per block, threads of a warp on consecutive blocks.
+template <typename InT>
+__global__ void __launch_bounds__(256) k_mx_quant(const InT* __restrict__ in, int64_t rows, int64_t cols, int64_t rs,
+                                                 int64_t cs, uint8_t* __restrict__ codes, float* __restrict__ scales,
+                                                 unsigned* err) {
+    const int64_t nb = (cols + 31) / 32;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= rows * nb) return;
+    // consecutive threads: consecutive rows of one block column when the
+    // view is transposed (coalesced reads), consecutive blocks of a row
+    // otherwise
+    int64_t r, cb;
+    if (cs != 1) { r = g % rows; cb = g / rows; } else { r = g / nb; cb = g % nb; }
+    const int64_t c0 = cb * 32, cn = cols - c0 < 32 ? cols - c0 : 32;
+    float v[32];
+    float m = 0.f;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+        v[t] = t < cn ? (float)in[r * rs + (c0 + t) * cs] : 0.f;
+        bad |= nonfinite_bits(v[t]);
+        m = fmaxf(m, fabsf(v[t]));
+    }
+    if (bad) atomicOr(err, ERRF_NONFINITE);
+    double sd;
+    if (m == 0.f) {
+        sd = 1.0;
+    } else {
+        const double md = (double)m;
+        int e = ilogb(md / 28.0);
+        if (md / ldexp(1.0, e) > 28.0) ++e;
+        if (e < -126) e = -126;
+        sd = ldexp(1.0, e);
+    }
+    const float s = (float)sd, inv = (float)(1.0 / sd);  // exact: a power of two
+    scales[r * nb + cb] = s;
+    uint8_t* o = codes + r * cols + c0;
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+        if (t < cn) o[t] = (uint8_t)(quant_e3m2(v[t], s, inv) << 2);
+}
+
+bool mx_quantize(int in_dtype, const void* in, int64_t rows, int64_t cols, int64_t rs, int64_t cs, uint8_t* codes,
+                 float* scales, unsigned* err, cudaStream_t st) {
+    if (rows <= 0 || cols <= 0) return true;
+    const int64_t n = rows * ((cols + 31) / 32);
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    if (in_dtype == DT_BF16)
+        k_mx_quant<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(in), rows, cols, rs, cs,
+                                                        codes, scales, err);
+    else
+        k_mx_quant<float><<<grid, 256, 0, st>>>(static_cast<const float*>(in), rows, cols, rs, cs, codes, scales, err);
     return cudaPeekAtLastError() == cudaSuccess;
 }
 

@@ -375,6 +375,7 @@ static void cols_dispatch(int mode, int fmt, const InT* in, int64_t b, int64_t r
 void run_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t B, int mode, int fmt,
               unsigned* amax, const float* sup, uint8_t* codes, void* out, int out_dtype, unsigned* err,
               float* scale_out, cudaStream_t st) {
+    fmt = code_format(fmt);
     // production kernels: fwht3.cu (B <= 256; TMA-staged v4, or v3 with
     // direct loads), then fwht2.cu (8 <= B <= 256); this file keeps the
     // generic paths for the remaining block sizes.  HALO_K1_VERSION=2 / 3
@@ -407,6 +408,7 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
               unsigned* amax_rot, unsigned* amax_plain, const float* sup_rot, const float* sup_plain,
               uint8_t* codes_rot, uint8_t* codes_plain, float* out, int64_t rows_out, unsigned* err,
               float* scale_rot_out, float* scale_plain_out, cudaStream_t st) {
+    fmt = code_format(fmt);
     if (base_dim_of(B)) {
         cols_base(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
                   codes_plain, err, scale_rot_out, scale_plain_out, st, out, rows_out);
@@ -434,6 +436,7 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
 
 void run_plain(const void* in, int in_dtype, int64_t n, int mode, int fmt, unsigned* amax, const float* sup,
                uint8_t* codes, unsigned* err, float* scale_out, cudaStream_t st) {
+    fmt = code_format(fmt);
     if (in_dtype == DT_BF16)
         plain_dispatch<__nv_bfloat16>(mode, fmt, static_cast<const __nv_bfloat16*>(in), n, amax, sup, codes, err, scale_out, st);
     else

@@ -1018,6 +1018,7 @@ bool encode_shard_maps(const uint8_t* const* parts, int n, int64_t inner, int64_
 int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N, int64_t K, int a_kmajor,
                int b_kmajor, const float* sa, const float* sa_vec, const float* sb, const float* sb_vec, void* out,
                int out_kind, int xf_lb, float xf_norm, int out_trans, int64_t n_valid, cudaStream_t st) {
+    fmt = code_format(fmt);
     if ((sa_vec || sb_vec) && (xf_lb > 0 || out_trans || out_kind == 2)) return -1;
     const ShardSpec* sha = t_shard_a;
     const ShardSpec* shb = t_shard_b;

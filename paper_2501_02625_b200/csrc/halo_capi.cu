@@ -64,7 +64,9 @@ halo_status resolve_block(int64_t d, int64_t had_block, int64_t* B, const char* 
 
 // INT8, FP8 E4M3 and FP6 E3M2 (one code per byte, the E3M2 bits in 7:2:
 // the tcgen05 kind::f8f6f4 operand form)
-bool valid_format(int32_t f) { return f == HALO_FMT_INT8 || f == HALO_FMT_FP8_E4M3 || f == HALO_FMT_FP6_E3M2; }
+bool valid_format(int32_t f) {
+    return f == HALO_FMT_INT8 || f == HALO_FMT_FP8_E4M3 || f == HALO_FMT_FP6_E3M2 || f == HALO_FMT_MXFP6_E3M2;
+}
 bool valid_gemm_format(int32_t f) { return valid_format(f); }
 bool valid_dtype(int32_t d) { return d == HALO_DTYPE_F32 || d == HALO_DTYPE_BF16; }
 
@@ -166,6 +168,7 @@ struct halo_ctx {
     // the per-row absmax scratch
     Buffer xs_rows, ws_rows, amax_rows;
     Buffer es_rows, ehs_rows;  // row-granularity backward: per-token E_Y / (H_b E_Y) scales
+    Buffer mx_t, mx_ts;        // Granularity::mx backward: quantize(transpose(E_Y)) codes / block scales
     bool row_gran = false;
     int32_t gran = HALO_GRAN_TENSOR;
     const uint8_t* wq_codes = nullptr;  // ctx.wq (own buffer or the layer's qweight)
@@ -187,6 +190,7 @@ struct halo_ctx {
     ~halo_ctx() {
         xq.release(); wq.release(); ehq.release(); eq.release(); wq2.release(); scratch.release();
         gscratch.release(); dev.release(); xs_rows.release(); ws_rows.release(); amax_rows.release(); es_rows.release(); ehs_rows.release();
+        mx_t.release(); mx_ts.release();
     }
 };
 
@@ -434,6 +438,9 @@ DevScalars* free_scalars(halo_stream_t stream) {
 extern "C" halo_status halo_rotate_quantize(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
                                             int64_t had_block, int32_t format, const float* supplied_scale,
                                             uint8_t* codes, float* scale_out, halo_stream_t stream) {
+    if (format == HALO_FMT_MXFP6_E3M2)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: mxfp6_e3m2 requires mx granularity (quantize.hpp:249-250): "
+                    "halo_rotate_quantize_mx");
     if (!a || !codes) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: null pointer");
     if (!valid_dtype(a_dtype) || !valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: bad dtype/format");
     if (rows < 0 || cols <= 0 || cols % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize: cols must be a positive multiple of 16");
@@ -457,6 +464,9 @@ __global__ void k_word_to_float(const unsigned* w, float* out) { *out = __uint_a
 extern "C" halo_status halo_rotate_quantize_amax(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
                                                  int64_t had_block, int32_t format, const float* amax,
                                                  uint8_t* codes, float* scale_out, halo_stream_t stream) {
+    if (format == HALO_FMT_MXFP6_E3M2)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: mxfp6_e3m2 requires mx granularity (quantize.hpp:249-250): "
+                    "halo_rotate_quantize_mx");
     if (!a || !codes || !amax) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: null pointer");
     if (!valid_dtype(a_dtype) || !valid_format(format))
         return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_amax: bad dtype/format");
@@ -469,12 +479,13 @@ extern "C" halo_status halo_rotate_quantize_amax(const void* a, int32_t a_dtype,
     // the absmax word is the float's bit pattern (non-negative)
     unsigned* word = reinterpret_cast<unsigned*>(const_cast<float*>(amax));
     ProfScope ps(PC_K1, (double)rows * cols * (dt_bytes(a_dtype) + 1), st);
+    const float* sup = nullptr;
     if (had_block >= 0) {
         int64_t B;
         if (resolve_block(cols, had_block, &B, "rotate_quantize_amax") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
-        run_rows(a, a_dtype, rows, cols, B, 1, format, word, nullptr, codes, nullptr, 0, &d->err, scale_out, st);
+        run_rows(a, a_dtype, rows, cols, B, 1, format, word, sup, codes, nullptr, 0, &d->err, scale_out, st);
     } else {
-        run_plain(a, a_dtype, rows * cols, 1, format, word, nullptr, codes, &d->err, scale_out, st);
+        run_plain(a, a_dtype, rows * cols, 1, format, word, sup, codes, &d->err, scale_out, st);
     }
     return cuda_check("rotate_quantize_amax");
 }
@@ -524,6 +535,9 @@ extern "C" halo_status halo_left_rotate_quantize(const void* e, int32_t e_dtype,
                                                  int64_t had_block, int32_t format, uint8_t* codes_rot,
                                                  float* scale_rot, uint8_t* codes_plain, float* scale_plain,
                                                  halo_stream_t stream) {
+    if (format == HALO_FMT_MXFP6_E3M2)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: mxfp6_e3m2 requires mx granularity (quantize.hpp:249-250): "
+                    "halo_rotate_quantize_mx");
     if (!e || !codes_rot) return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: null pointer");
     if (!valid_dtype(e_dtype) || !valid_format(format)) return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: bad dtype/format");
     if (b <= 0 || n <= 0 || n % 16) return fail(HALO_ERR_INVALID_ARGUMENT, "left_rotate_quantize: n must be a positive multiple of 16");
@@ -597,11 +611,46 @@ extern "C" halo_status halo_qmatmul_rotate(int32_t format, const uint8_t* a, int
     return HALO_OK;
 }
 
+extern "C" halo_status halo_rotate_quantize_mx(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
+                                               int64_t had_block, int32_t transpose_in, uint8_t* codes, float* scales,
+                                               halo_stream_t stream) {
+    if (!a || !codes || !scales) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_mx: null pointer");
+    if (!valid_dtype(a_dtype) || rows < 0 || cols <= 0) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_mx: bad arguments");
+    if (transpose_in && had_block >= 0)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_mx: a transposed view is not rotated (halo_linear.hpp:427-431)");
+    if (rows == 0) return HALO_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevScalars* d = free_scalars(stream);
+    if (!d) return HALO_ERR_CUDA;
+    if (transpose_in) {  // quantize(transpose(A)): A is cols x rows row-major
+        if (!mx_quantize(a_dtype, a, rows, cols, 1, rows, codes, scales, &d->err, st))
+            return fail(HALO_ERR_CUDA, "rotate_quantize_mx: launch failed");
+        return cuda_check("rotate_quantize_mx");
+    }
+    if (had_block < 0) {
+        if (!mx_quantize(a_dtype, a, rows, cols, cols, 1, codes, scales, &d->err, st))
+            return fail(HALO_ERR_CUDA, "rotate_quantize_mx: launch failed");
+        return cuda_check("rotate_quantize_mx");
+    }
+    int64_t B;
+    if (resolve_block(cols, had_block, &B, "rotate_quantize_mx") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
+    Buffer& tmp = t_scratch.rows[st];
+    if (tmp.ensure((size_t)(rows * cols) * 2 * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+    float* T0 = tmp.as<float>();
+    float* T1 = T0 + rows * cols;
+    pad_rows_f32(a, a_dtype, rows, rows, cols, T0, st);
+    BaseScope h(false);
+    run_rows(T0, HALO_DTYPE_F32, rows, cols, B, 2, 0, nullptr, nullptr, nullptr, T1, HALO_DTYPE_F32, nullptr, nullptr, st);
+    if (!mx_quantize(HALO_DTYPE_F32, T1, rows, cols, cols, 1, codes, scales, &d->err, st))
+        return fail(HALO_ERR_CUDA, "rotate_quantize_mx: launch failed");
+    return cuda_check("rotate_quantize_mx");
+}
+
 extern "C" halo_status halo_rotate_quantize_rows(const void* a, int32_t a_dtype, int64_t rows, int64_t cols,
                                                  int64_t had_block, int32_t format, uint8_t* codes, float* scales_out,
                                                  halo_stream_t stream) {
     if (!a || !codes || !scales_out) return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: null pointer");
-    if (!valid_dtype(a_dtype) || !valid_format(format) || format == HALO_FMT_FP6_E3M2)
+    if (!valid_dtype(a_dtype) || !valid_format(format) || format == HALO_FMT_FP6_E3M2 || format == HALO_FMT_MXFP6_E3M2)
         return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: bad dtype/format (int8 or fp8_e4m3)");
     if (rows < 0 || cols <= 0 || cols % 256)
         return fail(HALO_ERR_INVALID_ARGUMENT, "rotate_quantize_rows: cols must be a positive multiple of 256");
@@ -645,8 +694,9 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
     if (!s.quantize_f || !s.quantize_e || !s.quantize_g)
         return fail(HALO_ERR_INVALID_ARGUMENT,
                     "halo layer: unquantized matmuls run in working precision in the reference; the device path has no full-precision fallback");
-    if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW && s.granularity != HALO_GRAN_COLUMN)
-        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: tensor, row and column granularity are on the device path");
+    if (s.granularity != HALO_GRAN_TENSOR && s.granularity != HALO_GRAN_ROW && s.granularity != HALO_GRAN_COLUMN &&
+        s.granularity != HALO_GRAN_MX)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: tensor, row, column and mx granularity are on the device path");
     if (s.granularity == HALO_GRAN_ROW && (m % 256 || n % 256 || (s.had_block ? s.had_block : m) > 256 ||
                                            !is_pow2(s.had_block ? s.had_block : m)))
         return fail(HALO_ERR_INVALID_ARGUMENT,
@@ -654,6 +704,11 @@ static halo_status validate_scheme(const halo_scheme& s, int64_t m, int64_t n) {
                     "per-row error quantizer of the backward) and a Hadamard block <= 256");
     if (!valid_format(s.format_x) || s.format_x != s.format_w || s.format_x != s.format_e)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: X/W/E formats must agree and be int8, fp8_e4m3 or fp6_e3m2");
+    // quantize.hpp:247-250: mx granularity <=> the mxfp6_e3m2 format
+    if ((s.format_x == HALO_FMT_MXFP6_E3M2) != (s.granularity == HALO_GRAN_MX))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: mxfp6_e3m2 requires mx granularity and vice versa (quantize.hpp:247-250)");
+    if (s.granularity == HALO_GRAN_MX && (m % 32 || n % 32))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: mx granularity needs in/out features % 32 == 0");
     if (s.format_x == HALO_FMT_FP6_E3M2 && s.granularity != HALO_GRAN_TENSOR)
         return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: fp6_e3m2 on the device path uses tensor granularity");
     if (s.F.left || s.F.right) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: placement_F must be O or M (apply_placement engine is not on the device path)");
@@ -886,6 +941,61 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
     c->gran = s.granularity;
     c->xq_borrow = nullptr;
     c->had_block = s.had_block;
+    if (s.granularity == HALO_GRAN_MX) {
+        // NumericFormat::MxFp6E3M2 under Granularity::mx (quantize.hpp:224-232,
+        // 247-250): 1 x 32 power-of-two block scales along in_features, on
+        // F's contracted dim -- Y is qmatmul's dequantized double product
+        // (:377-379), restated bit-exactly by deq_gemm
+        if (l->qcodes || l->sharded)
+            return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: mx granularity with installed qweight codes");
+        c->wq_sharded = false;
+        const int64_t m = l->m, n = l->n, nb = m / 32, rmax = b > n ? b : n;
+        const int64_t tmp = (rmax * m > b * n ? rmax * m : b * n) * (int64_t)sizeof(float);
+        if (c->xs_rows.ensure((size_t)(b * nb) * sizeof(float)) != HALO_OK ||
+            c->ws_rows.ensure((size_t)(n * nb) * sizeof(float)) != HALO_OK || c->wq.ensure((size_t)(n * m)) != HALO_OK ||
+            c->gscratch.ensure((size_t)tmp) != HALO_OK || c->scratch.ensure((size_t)(rmax * m) * sizeof(float)) != HALO_OK)
+            return HALO_ERR_CUDA;
+        // quantize([A H], mxfp6, mx) (:292-297)
+        auto quant_side = [&](const void* src, int32_t dt, int64_t rows, uint8_t* codes, float* scales) -> bool {
+            if (rot) {
+                float* T0 = c->gscratch.as<float>();
+                float* T1 = c->scratch.as<float>();
+                pad_rows_f32(src, dt, rows, rows, m, T0, st);
+                BaseScope h(false);  // transform_right (H)
+                run_rows(T0, HALO_DTYPE_F32, rows, m, B, 2, 0, nullptr, nullptr, nullptr, T1, HALO_DTYPE_F32, nullptr,
+                         nullptr, st);
+                return mx_quantize(HALO_DTYPE_F32, T1, rows, m, m, 1, codes, scales, &d->err, st);
+            }
+            return mx_quantize(dt, src, rows, m, m, 1, codes, scales, &d->err, st);
+        };
+        {
+            ProfScope ps(PC_K1, (double)b * m * (dt_bytes(x_dtype) + 1), st);
+            if (!quant_side(x, x_dtype, b, c->xq.as<uint8_t>(), c->xs_rows.as<float>()))
+                return fail(HALO_ERR_CUDA, "forward: mx quantization failed");
+        }
+        ++l->cx;
+        {
+            ProfScope ps(PC_K1, (double)n * m * (dt_bytes(l->w_dtype) + 1), st);
+            if (!quant_side(l->w, l->w_dtype, n, c->wq.as<uint8_t>(), c->ws_rows.as<float>()))
+                return fail(HALO_ERR_CUDA, "forward: mx quantization failed");
+        }
+        ++l->cw;
+        c->wq_codes = c->wq.as<uint8_t>();
+        c->wq_scale = c->ws_rows.as<float>();
+        c->xq_scale = c->xs_rows.as<float>();
+        float* P = c->gscratch.as<float>();
+        {
+            // A = xq (i = token, k = in): scale [i][k >> 5]; B = wq^T (k = in,
+            // j = out): scale [j][k >> 5]
+            ProfScope ps(PC_GEMM, 2.0 * (double)b * n * m, st);
+            if (!deq_gemm(s.format_x, c->xq.as<uint8_t>(), c->xs_rows.as<float>(), m, 1, nb, 1, c->wq_codes,
+                          c->wq_scale, 1, m, 1, nb, P, b, n, m, n, st, 0, 5, 5, 0))
+                return fail(HALO_ERR_CUDA, "forward: mx product launch failed");
+        }
+        finish_right(P, y, y_dtype, b, n, 1, false, st);
+        c->valid = true;
+        return cuda_check("forward");
+    }
     if (s.granularity == HALO_GRAN_COLUMN) {
         // Granularity::column: X's and W's scales both sit on F's contracted
         // dim, so Y is qmatmul's dequantized double product
@@ -1211,12 +1321,115 @@ static halo_status backward_grouped(halo_linear* l, halo_ctx* c, const void* e_y
     return cuda_check("backward");
 }
 
+// Granularity::mx backward (halo_linear.hpp:381-439 with MxFp6E3M2): the
+// error path quantizes (H_b pad(E_Y)) or E_Y with 1 x 32 blocks along out
+// features, the gradient path quantizes transpose(E_Y) itself -- MX blocks do
+// not survive a transpose (:427-431) -- with blocks along tokens; both
+// products are dequantized double matmuls (deq_gemm, bit-exact).
+static halo_status backward_mx(halo_linear* l, halo_ctx* c, const void* e_y, int32_t e_dtype, void* e_x,
+                               int32_t ex_dtype, void* grad_w, int32_t gw_dtype, cudaStream_t st) {
+    const halo_scheme& s = l->s;
+    const int64_t b = c->b, m = l->m, n = l->n;
+    const int fmt = s.format_e;
+    if (c->m != m || c->n != n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
+    if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: bad dtype");
+    if (s.peft || l->scatter || c->wq_sharded)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: mx backward: no PEFT / sharded / scattered path");
+    if ((bool)s.E.right != c->wq_rotated || (bool)s.G.right != c->xq_rotated)
+        return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: mx backward needs the saved operand rotations");
+    int64_t Bm = 1;
+    if ((s.E.right || s.G.right) && resolve_block(m, s.had_block, &Bm, "backward") != HALO_OK)
+        return HALO_ERR_INVALID_ARGUMENT;
+    DevScalars* d = c->d();
+    const bool left = s.E.left;
+    const int64_t b_pad = left ? halo_padded_batch(b, s.had_block) : b;
+    int64_t Bb = 1;
+    if (left && resolve_block(b_pad, s.had_block, &Bb, "backward (token dim)") != HALO_OK)
+        return HALO_ERR_INVALID_ARGUMENT;
+    c->b_pad = b_pad;
+    const int64_t nbn = n / 32, nbm = m / 32, nbb = (b + 31) / 32;
+    if (c->eq.ensure((size_t)(b_pad * n)) != HALO_OK || c->es_rows.ensure((size_t)(b_pad * nbn) * sizeof(float)) != HALO_OK ||
+        c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
+        return HALO_ERR_CUDA;
+    float* P = c->scratch.as<float>();
+    // ---- error path (:381-413): A = E codes (i = token, k = out, scale
+    // [i][k >> 5]); B = wq (k = out, j = in, scale [k][j >> 5])
+    if (e_x) {
+        const uint8_t* ecodes;
+        const float* escales;
+        int64_t rows = b;
+        if (left) {
+            if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->ehs_rows.ensure((size_t)(b_pad * nbn) * sizeof(float)) != HALO_OK ||
+                c->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
+                return HALO_ERR_CUDA;
+            float* T = c->gscratch.as<float>();
+            ProfScope ps(PC_K2, (double)b * n * dt_bytes(e_dtype) + (double)b_pad * n * 9, st);
+            pad_rows_f32(e_y, e_dtype, b, b_pad, n, T, st);
+            BaseScope orient(true);  // transform_left_h (:398)
+            run_cols(T, HALO_DTYPE_F32, b_pad, b_pad, n, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     T, b_pad, nullptr, nullptr, nullptr, st);
+            if (!mx_quantize(HALO_DTYPE_F32, T, b_pad, n, n, 1, c->ehq.as<uint8_t>(), c->ehs_rows.as<float>(), &d->err, st))
+                return fail(HALO_ERR_CUDA, "backward: mx quantization failed");
+            ecodes = c->ehq.as<uint8_t>();
+            escales = c->ehs_rows.as<float>();
+            rows = b_pad;
+        } else {
+            ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
+            if (!mx_quantize(e_dtype, e_y, b, n, n, 1, c->eq.as<uint8_t>(), c->es_rows.as<float>(), &d->err, st))
+                return fail(HALO_ERR_CUDA, "backward: mx quantization failed");
+            ecodes = c->eq.as<uint8_t>();
+            escales = c->es_rows.as<float>();
+        }
+        ++l->ce;
+        {
+            ProfScope ps(PC_GEMM, 2.0 * (double)rows * m * n, st);
+            if (!deq_gemm(fmt, ecodes, escales, n, 1, nbn, 1, c->wq_codes, c->wq_scale, m, 1, nbm, 1, P, rows, m, n, m,
+                          st, 0, 5, 0, 5))
+                return fail(HALO_ERR_CUDA, "backward: E product launch failed");
+        }
+        if (left) {  // transform_left, take_rows(b) (:405-409), in place
+            ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
+            BaseScope orient(false);
+            run_cols(P, HALO_DTYPE_F32, b_pad, b_pad, m, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     P, b, nullptr, nullptr, nullptr, st);
+        }
+        finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st);
+    }
+    // ---- gradient path (:418-439): quantize(transpose(E_Y)) [n x b] with
+    // blocks along tokens (A: i = out, k = token, scale [i][k >> 5]); B =
+    // (XH)_Q (k = token, j = in, scale [k][j >> 5])
+    if (grad_w) {
+        if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK || c->mx_t.ensure((size_t)(n * b)) != HALO_OK ||
+            c->mx_ts.ensure((size_t)(n * nbb) * sizeof(float)) != HALO_OK)
+            return HALO_ERR_CUDA;
+        uint8_t* et = c->mx_t.as<uint8_t>();
+        float* ets = c->mx_ts.as<float>();
+        {
+            ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
+            if (!mx_quantize(e_dtype, e_y, n, b, 1, n, et, ets, &d->err, st))
+                return fail(HALO_ERR_CUDA, "backward: mx quantization failed");
+        }
+        ++l->ce;
+        float* G = c->gscratch.as<float>();
+        {
+            ProfScope ps(PC_GEMM, 2.0 * (double)n * m * b, st);
+            if (!deq_gemm(fmt, et, ets, b, 1, nbb, 1, c->xq_codes(), c->xq_scale, m, 1, nbm, 1, G, n, m, b, m, st, 0, 5,
+                          0, 5))
+                return fail(HALO_ERR_CUDA, "backward: G product launch failed");
+        }
+        finish_right(G, grad_w, gw_dtype, n, m, Bm, s.G.right, st);
+    }
+    return cuda_check("backward");
+}
+
 extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, const void* e_y, int32_t e_dtype,
                                             void* e_x, int32_t ex_dtype, void* grad_w, int32_t gw_dtype,
                                             halo_stream_t stream) {
     if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
     if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
+    if (c->gran == HALO_GRAN_MX) return backward_mx(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
     if (c->row_gran || c->gran == HALO_GRAN_COLUMN) return backward_grouped(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
     if (c->m != l->m || c->n != l->n) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: upstream error shape mismatch");
     if (!valid_dtype(e_dtype) || !valid_dtype(ex_dtype) || (grad_w && !valid_dtype(gw_dtype)))

@@ -9,6 +9,12 @@
 namespace halo_b200 {
 
 int num_sms();
+// MXFP6 (NumericFormat::MxFp6E3M2, id 3) has E3M2 codes under power-of-two
+// 1 x 32 block scales (quantize.hpp:224-232, mx_quantize); kernels that only
+// see codes (GEMMs, deq_gemm) treat it as FMT_E3M2
+constexpr int FMT_MXFP6 = 3;
+inline int code_format(int fmt) { return fmt == FMT_MXFP6 ? 2 : fmt; }
+
 float hadamard_norm(int64_t B);
 
 // K1 / K4-right: right transform over the contiguous dim (block B), then
@@ -139,9 +145,16 @@ bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_
 // Granularity::row backward products (deq_gemm.cu): C[i,j] (fp32, ldc) =
 // sum_k deq(A(i,k)) * deq(B(k,j)) in double, k ascending (qmatmul's
 // dequantized path, quantize.hpp:377-379).  Views by element / scale strides.
+// scale index of A(i, k) = (i >> a_sh_i) * as_si + (k >> a_sh_k) * as_sk (B likewise):
+// shift 5 walks the 32-wide MX blocks
 bool deq_gemm(int fmt, const uint8_t* a, const float* as, int64_t a_si, int64_t a_sk, int64_t as_si, int64_t as_sk,
               const uint8_t* b, const float* bs, int64_t b_sk, int64_t b_sj, int64_t bs_sk, int64_t bs_sj, float* c,
-              int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st);
+              int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st, int a_sh_i = 0, int a_sh_k = 0,
+              int b_sh_k = 0, int b_sh_j = 0);
+// Granularity::mx quantization (MxFp6E3M2): view in[r*rs + c*cs] (rows x cols)
+// -> codes [rows x cols] (E3M2 in bits 7:2), scales [rows x ceil(cols/32)]
+bool mx_quantize(int in_dtype, const void* in, int64_t rows, int64_t cols, int64_t rs, int64_t cs, uint8_t* codes,
+                 float* scales, unsigned* err, cudaStream_t st);
 // quantize(A, fmt, Granularity::column()) (deq_gemm.cu): `cols` scales
 bool col_quantize(int fmt, int in_dtype, const void* in, int64_t rows, int64_t cols, unsigned* amax, float* scales,
                   uint8_t* codes, unsigned* err, cudaStream_t st);

@@ -32,17 +32,18 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import (DTYPE_BF16, DTYPE_F32, FMT_FP6_E3M2, FMT_FP8_E4M3, FMT_INT8, OUT_BF16, OUT_F32, OUT_S32,
+from ._lib import (DTYPE_BF16, DTYPE_F32, FMT_FP6_E3M2, FMT_FP8_E4M3, FMT_INT8, FMT_MXFP6_E3M2, OUT_BF16, OUT_F32, OUT_S32,
                    Counters, Scheme, check, lib)
 
 INT8 = FMT_INT8
 FP8_E4M3 = FMT_FP8_E4M3
 FP6_E3M2 = FMT_FP6_E3M2
+MXFP6_E3M2 = FMT_MXFP6_E3M2
 
 _DT = {torch.float32: DTYPE_F32, torch.bfloat16: DTYPE_BF16}
 
 
-GRAN_TENSOR, GRAN_ROW, GRAN_COLUMN = 0, 1, 2  # halo_b200.h HALO_GRAN_*
+GRAN_TENSOR, GRAN_ROW, GRAN_COLUMN, GRAN_MX = 0, 1, 2, 4  # halo_b200.h HALO_GRAN_*
 
 
 def _stream():
@@ -136,6 +137,22 @@ def rotate_quantize(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, scale:
     check(lib().halo_rotate_quantize(_ptr(a), _dt(a), rows, cols, had_block if rotate else -1, fmt,
                                      _ptr(scale), _ptr(codes), _ptr(s_out), _stream()))
     return codes, s_out
+
+
+def rotate_quantize_mx(a: torch.Tensor, had_block: int = 0, rotate: bool = True, transpose: bool = False):
+    """``quantize([transform_right](a), mxfp6_e3m2, Granularity::mx())``:
+    E3M2 codes (bits 7:2) and power-of-two scales per 1 x 32 block along rows
+    (quantize.hpp:224-232), scales shaped [rows, ceil(cols/32)].  transpose:
+    quantize ``a.T`` itself (halo_linear.hpp:427-431; no rotation)."""
+    _need_cuda(a)
+    a = a.contiguous()
+    rows, cols = (a.shape[1], a.shape[0]) if transpose else a.shape
+    codes = torch.empty((rows, cols), dtype=torch.uint8, device=a.device)
+    scales = torch.empty((rows, (cols + 31) // 32), dtype=torch.float32, device=a.device)
+    blk = -1 if (transpose or not rotate) else had_block
+    check(lib().halo_rotate_quantize_mx(_ptr(a), _dt(a), rows, cols, blk, int(transpose), _ptr(codes), _ptr(scales),
+                                        _stream()))
+    return codes, scales
 
 
 def rotate_quantize_rows(a: torch.Tensor, had_block: int = 0, fmt: int = INT8, rotate: bool = True):
@@ -332,8 +349,10 @@ class SavedContext:
         check(lib().halo_ctx_saved(self._h, C.byref(xq), C.byref(sx), C.byref(wq), C.byref(sw), C.byref(b)))
         dt = code_dtype(layer.fmt)
         g = layer.scheme.granularity
-        nsx = b.value if g == GRAN_ROW else layer.in_features if g == GRAN_COLUMN else 1
-        nsw = layer.out_features if g == GRAN_ROW else layer.in_features if g == GRAN_COLUMN else 1
+        nb = (layer.in_features + 31) // 32
+        nsx = b.value if g == GRAN_ROW else layer.in_features if g == GRAN_COLUMN else b.value * nb if g == GRAN_MX else 1
+        nsw = (layer.out_features if g == GRAN_ROW else layer.in_features if g == GRAN_COLUMN
+               else layer.out_features * nb if g == GRAN_MX else 1)
         return (_from_ptr(xq.value, (b.value, layer.in_features), dt),
                 _from_ptr(sx.value, (nsx,), torch.float32),
                 _from_ptr(wq.value, (layer.out_features, layer.in_features), dt),

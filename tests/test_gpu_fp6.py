@@ -87,3 +87,68 @@ def test_fp6_wire_format_pack_unpack(H, orc):
     assert torch.equal(back, codes.view(torch.uint8).reshape(-1))
     assert packed.numel() == fsdp.code_payload_bytes(fsdp.FP6_E3M2, codes.numel())
     assert packed.numel() / (2 * codes.numel()) == 0.375
+
+
+# ------------------------------------------------------------------ MXFP6
+# NumericFormat::MxFp6E3M2 with Granularity::mx (the only pairing the
+# reference accepts, quantize.hpp:247-250): power-of-two scales per 1 x 32
+# block, E3M2 codes; every layer product is the reference's dequantized
+# double matmul (deq_gemm, opt-in), bit-exact.
+
+@pytest.mark.parametrize("block", [-1, 32, 256])
+def test_mx_quantizer_matches_oracle(H, orc, block):
+    a = orc.bf16_round(orc.randn(48, 512, 3))
+    a[:, 5] *= 300
+    a[7, :64] = 0.0
+    codes, scales = H.rotate_quantize_mx(torch.from_numpy(a).cuda().to(torch.bfloat16), block, rotate=block >= 0)
+    x = orc.fwht_rows(a, block) if block >= 0 else a
+    want_c, want_s = orc.quantize(x, 3, 4)
+    assert np.array_equal(scales.cpu().numpy().reshape(-1), want_s)
+    assert np.array_equal(codes.cpu().numpy(), orc.codes_to_bytes(want_c, 3))
+    # quantize(transpose(E)) -- the gradient path's operand
+    e = orc.bf16_round(orc.randn(96, 64, 5, 1e-3))
+    tc, ts = H.rotate_quantize_mx(torch.from_numpy(e).cuda().to(torch.bfloat16), transpose=True)
+    wc, ws = orc.quantize(np.ascontiguousarray(e.T), 3, 4)
+    assert np.array_equal(ts.cpu().numpy().reshape(-1), ws)
+    assert np.array_equal(tc.cpu().numpy(), orc.codes_to_bytes(wc, 3))
+
+
+@pytest.mark.parametrize("level", [0, 1, 2])
+@pytest.mark.parametrize("block", [0, 64])
+def test_mxfp6_layer_matches_reference(H, orc, level, block):
+    """The unmodified reference HaloLinearLayer with halo{level}(MxFp6E3M2,
+    Granularity::mx()): Y, E_X, grad_W bit-exact; counters as the reference
+    (the gradient path quantizes transpose(E_Y) itself: e += 1)."""
+    H.allow_dequantized_products(True)
+    b, m, n = 96, 256, 128
+    X = orc.bf16_round(orc.randn(b, m, 1))
+    X[:, 3] *= 40
+    X = orc.bf16_round(X)
+    W = orc.bf16_round(orc.randn(n, m, 2, 1 / 16))
+    E = orc.bf16_round(orc.randn(b, n, 3, 1e-3))
+    want = orc.ref_linear(level, 3, block, X, W, E, gran=4)
+    layer = H.HaloLinearLayer(torch.from_numpy(W).cuda().to(torch.bfloat16),
+                              getattr(H, f"halo{level}")(H.MXFP6_E3M2, block, H.GRAN_MX), out_dtype=torch.float32)
+    ctx = H.SavedContext()
+    y = layer.forward(torch.from_numpy(X).cuda().to(torch.bfloat16), ctx)
+    back = layer.backward(ctx, torch.from_numpy(E).cuda().to(torch.bfloat16))
+    ctx.check()
+    xq, sx, wq, sw = ctx.saved(layer)
+    assert np.array_equal(xq.cpu().numpy(), orc.codes_to_bytes(want["xq"], 3))
+    assert sx[0].item() == want["sx"] and sw[0].item() == want["sw"]
+    assert np.array_equal(y.cpu().numpy(), want["Y"])
+    assert np.array_equal(back.e_x.cpu().numpy(), want["EX"])
+    assert np.array_equal(back.grad_w.cpu().numpy(), want["GW"])
+    c = layer.counters()
+    assert (c.x, c.w, c.e) == (1, 1, 2)
+
+
+def test_mxfp6_rules(H):
+    W = torch.zeros(128, 256, dtype=torch.bfloat16, device="cuda")
+    H.allow_dequantized_products(True)
+    with pytest.raises(ValueError):  # mxfp6 needs mx granularity
+        H.HaloLinearLayer(W, H.halo2(H.MXFP6_E3M2, 256))
+    with pytest.raises(ValueError):  # mx granularity needs mxfp6
+        H.HaloLinearLayer(W, H.halo2(H.FP6_E3M2, 256, H.GRAN_MX))
+    with pytest.raises(ValueError):  # per-tensor quantizers refuse mxfp6
+        H.rotate_quantize(W, 256, fmt=H.MXFP6_E3M2)

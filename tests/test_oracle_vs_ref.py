@@ -13,7 +13,7 @@ def O(orc):
 
 
 @pytest.mark.parametrize("level", [0, 1, 2])
-@pytest.mark.parametrize("fmt", [0, 1])
+@pytest.mark.parametrize("fmt", [0, 1, 2])
 @pytest.mark.parametrize("block,b,m,n", [(0, 64, 128, 32), (32, 96, 64, 48), (16, 30, 32, 16), (0, 60, 64, 16)])
 def test_layer_bitexact(O, level, fmt, block, b, m, n):
     seed = 1000 + 7 * level + 3 * fmt + b
@@ -108,3 +108,22 @@ def test_fsdp_gather_matches_single_process(O):
             P[:rows] = W
             want, s = O.quantize(O.fwht_rows(P, cols) if rep % 4 != 3 else P, fmt)
             assert np.array_equal(codes, want) and scale == s[0]
+
+
+def test_mxfp6_quantizer(O):
+    """NumericFormat::MxFp6E3M2 under Granularity::mx (the only pairing the
+    reference accepts, quantize.hpp:247-250): power-of-two scale per 1 x 32
+    block (:224-232), E3M2 codes -- the restatement against the reference,
+    incl. an absmax exactly at 28 * 2^k, all-zero blocks and ragged cols."""
+    for cols in (64, 80):
+        a = O.bf16_round(O.randn(40, cols, 31))
+        a[3, :] = 28.0 * 4      # m / 2^e == 28 exactly: no bump
+        a[5, :32] = 0.0         # all-zero block -> scale 1
+        a[:, 7] *= 1e-20
+        got = O.quantize(a, 3, 4)
+        want = O.ref_quantize(a, 3, 4)
+        assert np.array_equal(got[1], want[1]) and np.array_equal(got[0], want[0])
+        s = want[1][want[1] != 1.0]
+        assert np.all(np.frexp(s)[0] == 0.5)  # powers of two
+    with pytest.raises(ValueError):
+        O.ref_quantize(a, 3, 0)  # mxfp6 needs mx granularity
