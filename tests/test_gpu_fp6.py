@@ -97,9 +97,10 @@ def test_fp6_wire_format_pack_unpack(H, orc):
 
 @pytest.mark.parametrize("block", [-1, 32, 256])
 def test_mx_quantizer_matches_oracle(H, orc, block):
-    a = orc.bf16_round(orc.randn(48, 512, 3))
+    a = orc.randn(48, 512, 3)
     a[:, 5] *= 300
     a[7, :64] = 0.0
+    a = orc.bf16_round(a)  # the device input is bf16: keep the oracle's identical
     codes, scales = H.rotate_quantize_mx(torch.from_numpy(a).cuda().to(torch.bfloat16), block, rotate=block >= 0)
     x = orc.fwht_rows(a, block) if block >= 0 else a
     want_c, want_s = orc.quantize(x, 3, 4)
