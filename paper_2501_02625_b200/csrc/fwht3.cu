@@ -576,6 +576,141 @@ __global__ void __launch_bounds__(128) k_rows_v4(const __grid_constant__ CUtenso
     core.reduce(absmax, err);
 }
 
+// ------------------------------- large blocks: 512 <= B <= 8192 (LB 9..13)
+// A 256-thread CTA owns a tile of 8192 contiguous elements (8192 / B whole
+// blocks), fp32 in 32 KB of shared memory.  Stage bits are processed in
+// increasing order, the reference's (hadamard.hpp:140-176):
+//   * bits 0..4 in registers exactly as RowsCore's phase 1 (thread t holds
+//     elements 32t .. 32t+31);
+//   * then rounds of up to 3 bits: a thread takes 8 float4 slots -- 4
+//     consecutive elements (bits 0-1, four independent columns, so every
+//     butterfly is an FADD2) x the 2^k values of the round's bits -- with
+//     consecutive lanes on consecutive slots (conflict-free LDS.128 /
+//     STS.128; the phase-1 write goes through an XOR swizzle of the slot's low
+//     3 bits with bits 3-5), runs the k stages, writes back;
+//   * the last round does not write back: it quantizes (4 codes -> one 32-bit
+//     store, lanes on consecutive words), reduces the absmax (skipping the
+//     last stage: max(|u+v|,|u-v|) = |u|+|v| exactly) or stores the
+//     transformed values.
+// One barrier per round.  Replaces the radix-16 scalar kernel of
+// fwht_big.cu for these block sizes.
+namespace {
+constexpr int BG2_TILE = 8192;
+__device__ __forceinline__ int bg2_phys(int q) { return q ^ ((q >> 3) & 7); }
+
+template <int LB, int LO>
+struct Bg2Round {
+    static constexpr int K = (LB - LO) < 3 ? (LB - LO) : 3;
+    static constexpr bool LAST = LO + K >= LB;
+    // slot of (thread t, s = 0..7): round bits v = s & (2^K - 1), group g = s >> K
+    __device__ __forceinline__ static int slot(int t, int s) {
+        const int v = s & ((1 << K) - 1), g = s >> K;
+        const int rest = t + 256 * g;                 // 11 - K bits: slot bits [0, LO-2) then [LO-2+K, 11)
+        const int low = rest & ((1 << (LO - 2)) - 1);
+        const int high = rest >> (LO - 2);
+        return low | (v << (LO - 2)) | (high << (LO - 2 + K));
+    }
+};
+}  // namespace
+
+
+// rounds LO, LO+3, ... (compile-time recursion); the last one emits
+template <int LB, int LO, int FMT, int MODE, bool SUP, typename OutT>
+__device__ __forceinline__ void bg2_rounds(float4* S, int t, int64_t base, int64_t n,
+                                           RowsCore<LB, FMT, MODE, SUP, OutT>& core, uint8_t* __restrict__ codes,
+                                           OutT* __restrict__ out) {
+    using R = Bg2Round<LB, LO>;
+    float2 a[8], c[8];  // slot s: elements 0,1 in a[s], 2,3 in c[s]
+    int q[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        q[s] = R::slot(t, s);
+        const float4 f = S[bg2_phys(q[s])];
+        a[s] = make_float2(f.x, f.y);
+        c[s] = make_float2(f.z, f.w);
+    }
+#pragma unroll
+    for (int b = 0; b < R::K; ++b) {
+        const int h = 1 << b;
+        const bool last_stage = v3_abs<MODE>() && R::LAST && b == R::K - 1;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            if ((s & h) == 0) {
+                if (last_stage) {
+                    core.amax = max3nan(core.amax, fabsf(a[s].x) + fabsf(a[s + h].x), fabsf(a[s].y) + fabsf(a[s + h].y));
+                    core.amax = max3nan(core.amax, fabsf(c[s].x) + fabsf(c[s + h].x), fabsf(c[s].y) + fabsf(c[s + h].y));
+                } else {
+                    bfly2(a[s], a[s + h]);
+                    bfly2(c[s], c[s + h]);
+                }
+            }
+        }
+    }
+    if constexpr (!R::LAST) {
+#pragma unroll
+        for (int s = 0; s < 8; ++s) S[bg2_phys(q[s])] = make_float4(a[s].x, a[s].y, c[s].x, c[s].y);
+        __syncthreads();
+        bg2_rounds<LB, LO + 3>(S, t, base, n, core, codes, out);
+    } else {
+        if constexpr (v3_q<MODE>()) {
+            float dmax = 0.f;
+            uint32_t wd[8];
+#pragma unroll
+            for (int s = 0; s < 8; ++s) wd[s] = core.quant4(a[s], c[s], dmax);
+            if (__any_sync(0xffffffffu, !(dmax < core.thr))) {
+                if (!(dmax < core.thr)) {
+#pragma unroll
+                    for (int s = 0; s < 8; ++s)
+                        if (group_slow<FMT, SUP>(a[s], c[s], core.s, core.inv, core.thr))
+                            wd[s] = exact4<FMT>(a[s], c[s], core.s, core.inv);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < 8; ++s) *reinterpret_cast<uint32_t*>(codes + base + 4 * q[s]) = wd[s];
+        } else if constexpr (MODE == V3_XFORM) {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const float2 x = mul2(a[s], core.norm2), y = mul2(c[s], core.norm2);
+                if constexpr (sizeof(OutT) == 4)
+                    *reinterpret_cast<float4*>(out + base + 4 * q[s]) = make_float4(x.x, x.y, y.x, y.y);
+                else
+                    *reinterpret_cast<uint2*>(out + base + 4 * q[s]) = make_uint2(pack_bf16x2(x.x, x.y), pack_bf16x2(y.x, y.y));
+            }
+        }
+    }
+}
+
+template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
+__global__ void __launch_bounds__(256) k_rows_lb(const InT* __restrict__ in, int64_t n, float norm, unsigned* absmax,
+                                                 const float* supplied, uint8_t* __restrict__ codes,
+                                                 OutT* __restrict__ out, unsigned* err, float* scale_out) {
+    __shared__ __align__(16) float4 S[BG2_TILE / 4];
+    const int t = threadIdx.x;
+    RowsCore<LB, FMT, MODE, SUP, OutT> core;
+    core.init(absmax, supplied, norm, err, scale_out);
+    const int64_t ntiles = n / BG2_TILE;
+    // the next tile's global loads are issued before this tile's rounds so
+    // their latency hides behind the shared-memory work
+    Load32<InT> cur, nxt;
+    if (blockIdx.x < ntiles) cur.load(in + (int64_t)blockIdx.x * BG2_TILE + 32 * t, true, true);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * BG2_TILE;
+        // ---- bits 0..4 in registers
+        float2 v[16];
+        cur.get(v);
+        if (tile + gridDim.x < ntiles) nxt.load(in + (tile + gridDim.x) * BG2_TILE + 32 * t, true, true);
+        core.phase1(v);
+        __syncthreads();  // the previous tile's last round has read its slots
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            S[bg2_phys(8 * t + j)] = make_float4(v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y);
+        __syncthreads();
+        bg2_rounds<LB, 5>(S, t, base, n, core, codes, out);
+        cur = nxt;
+    }
+    core.reduce(absmax, err);
+}
+
 // ------------------------------------------ SwiGLU forward + K1 phase A
 // h = silu(g) * u (swiglu_fwd1, the glue kernel's exact formula), rounded to
 // bf16 and written out for K1's quantize pass, and in the same pass the
@@ -806,6 +941,78 @@ bool rows_v3_per_row(int fmt, int in_dtype, const void* in, int64_t rows, int64_
         case 7: dispatch_rows_v3<7>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
         default: dispatch_rows_v3<8>(mode, fmt, in_dtype, in, n, cols, amax_rows, row_scales, codes, err, st); break;
         }
+    }
+    return true;
+}
+
+
+// ------------------------------------------------------- large-block launcher
+namespace {
+template <int LB, typename InT, int FMT, int MODE, bool SUP, typename OutT>
+void launch_lb(const InT* in, int64_t n, unsigned* amax, const float* sup, uint8_t* codes, OutT* out, unsigned* err,
+               float* sout, cudaStream_t st) {
+    auto kern = k_rows_lb<LB, InT, FMT, MODE, SUP, OutT>;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int64_t grid = n / BG2_TILE;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    if (grid > cap) grid = cap;
+    kern<<<(unsigned)(grid < 1 ? 1 : grid), 256, 0, st>>>(in, n, hadamard_norm(int64_t(1) << LB), amax, sup, codes, out,
+                                                          err, sout);
+}
+
+template <int LB>
+void dispatch_lb(int mode, int fmt, int in_dtype, const void* in, int64_t n, unsigned* amax, const float* sup,
+                 uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
+    using bf = __nv_bfloat16;
+    if (mode == V3_XFORM) {
+        const float* p = static_cast<const float*>(in);
+        if (out_dtype == DT_BF16) launch_lb<LB, float, 0, V3_XFORM, false, bf>(p, n, amax, sup, codes, static_cast<bf*>(out), err, sout, st);
+        else launch_lb<LB, float, 0, V3_XFORM, false, float>(p, n, amax, sup, codes, static_cast<float*>(out), err, sout, st);
+        return;
+    }
+#define HALO_LB(T)                                                                                                        \
+    {                                                                                                                     \
+        auto p = static_cast<const T*>(in);                                                                               \
+        if (mode == V3_ABSMAX) launch_lb<LB, T, 0, V3_ABSMAX, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st); \
+        else if (fmt == FMT_INT8) {                                                                                       \
+            if (sup) launch_lb<LB, T, FMT_INT8, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);   \
+            else launch_lb<LB, T, FMT_INT8, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);      \
+        } else if (fmt == FMT_E3M2) {                                                                                     \
+            if (sup) launch_lb<LB, T, FMT_E3M2, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);   \
+            else launch_lb<LB, T, FMT_E3M2, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);      \
+        } else {                                                                                                          \
+            if (sup) launch_lb<LB, T, FMT_E4M3, V3_QUANT, true, float>(p, n, amax, sup, codes, nullptr, err, sout, st);   \
+            else launch_lb<LB, T, FMT_E4M3, V3_QUANT, false, float>(p, n, amax, sup, codes, nullptr, err, sout, st);      \
+        }                                                                                                                 \
+    }
+    if (in_dtype == DT_BF16) HALO_LB(bf) else HALO_LB(float)
+#undef HALO_LB
+}
+}  // namespace
+
+// B = 2^lb, 9 <= lb <= 13, n a multiple of 8192, 32 B aligned operands.
+// HALO_K1_LB=0 keeps the older radix-16 kernel (fwht_big.cu) for A/B runs.
+bool rows_lb(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
+             uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
+    static const bool on = [] {
+        const char* e = getenv("HALO_K1_LB");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || B < 512 || B > 8192 || (B & (B - 1)) || n % BG2_TILE) return false;
+    if (mode == V3_XFORM && in_dtype != DT_F32) return false;
+    if ((uintptr_t)in % 32 || (uintptr_t)codes % 16 || (uintptr_t)out % 16) return false;
+    int lb = 0;
+    while ((int64_t(1) << lb) < B) ++lb;
+    switch (lb) {
+    case 9: dispatch_lb<9>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 10: dispatch_lb<10>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 11: dispatch_lb<11>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 12: dispatch_lb<12>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    default: dispatch_lb<13>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
     }
     return true;
 }

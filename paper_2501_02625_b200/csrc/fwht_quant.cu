@@ -389,6 +389,8 @@ void run_rows(const void* in, int in_dtype, int64_t rows, int64_t cols, int64_t 
     if (ver >= 3 && aligned &&
         rows_v3(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))
         return;
+    if (rows_lb(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))
+        return;
     if (rows_big(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))
         return;
     if (rows_v2(mode, fmt, in_dtype, in, rows * cols, B, amax, sup, codes, out, out_dtype, err, scale_out, st))

@@ -109,6 +109,9 @@ bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
              uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
 
 // K1 / K4 for large blocks (fwht_big.cu): 512 <= B <= 16384, B = 2^k
+// K1 / K4 for 512 <= B <= 8192 (fwht3.cu, radix-8 float4 rounds); false = not applicable
+bool rows_lb(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
+             uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
 bool rows_big(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
               uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
 

@@ -40,6 +40,11 @@ for w in $what; do
     block)
       timeout 900 python tools/bench_block.py --steps 10 > gpurun_out/bench_block.log 2>&1
       echo "rc=$?" >> gpurun_out/bench_block.log ;;
+    sweep_right)
+      timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_new.jsonl 2>&1
+      HALO_K1_LB=0 timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_old.jsonl 2>&1 ;;
+    sweep)
+      timeout 900 python tools/sweep_fwht.py > gpurun_out/sweep.jsonl 2>&1 ;;
     kern_v2)
       HALO_K1_VERSION=2 timeout 600 python tools/bench_kernels.py k1 > gpurun_out/kern_v2.log 2>&1 ;;
     prof_k1)
