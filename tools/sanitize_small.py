@@ -62,3 +62,40 @@ torch.cuda.synchronize()
 assert am_out.item() == 1.5
 check(lib().halo_peer_free(mb))
 print("sanitize workload done")
+
+# ---- round-2 kernels: large-block K1/K4, MX quantizer + MXFP6 layer, RMSNorm,
+# RoPE, AdamW, FP6 wire format, the NCCL data plane at world 1
+for blk in (512, 4096):
+    xl = torch.randn(8, 8192, device=dev).to(bf)
+    halo.rotate_quantize(xl, blk)
+    halo.transform_right(torch.randn(8, 8192, device=dev), blk)
+halo.rotate_quantize_mx(x, 256)
+halo.rotate_quantize_mx(e, transpose=True)
+mxl = halo.HaloLinearLayer(w, halo.halo2(halo.MXFP6_E3M2, 256, halo.GRAN_MX), out_dtype=torch.float32)
+ctx = halo.SavedContext()
+mxl.forward(x, ctx)
+mxl.backward(ctx, e)
+ctx.check()
+from paper_2501_02625_b200 import block  # noqa: E402
+xn = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
+wn = torch.ones(512, device=dev, requires_grad=True)
+yn = block._rmsnorm(xn, wn)
+yn.backward(torch.randn_like(yn))
+qkv = torch.randn(256, 4 * 128, device=dev).to(bf).requires_grad_(True)
+ro = block._RopeQKVFn.apply(qkv, block.rope_table(128, 128, dev), 128, 3, 4, 128)
+ro.backward(torch.randn_like(ro))
+from paper_2501_02625_b200.train import DeviceAdamW  # noqa: E402
+pw = torch.randn(4096, device=dev).to(bf)
+opt = DeviceAdamW([pw])
+opt.step([torch.randn(4096, device=dev)])
+c6, _ = halo.rotate_quantize(x, 256, fmt=halo.FP6_E3M2)
+halo.fp6_unpack(halo.fp6_pack(c6), c6.numel())
+from paper_2501_02625_b200.fsdp import FsdpHaloMLP  # noqa: E402
+wg_ = (torch.randn(512, 256, device=dev) / 16).to(bf)
+wd_ = (torch.randn(256, 512, device=dev) / 16).to(bf)
+f = FsdpHaloMLP(wg_, wg_.clone(), wd_, halo.halo2(halo.INT8, 256), check_stale=True)
+f.forward(torch.randn(256, 256, device=dev).to(bf))
+f.backward(torch.randn(256, 256, device=dev).to(bf) * 1e-3)
+f.close()
+torch.cuda.synchronize()
+print("sanitize workload (round-2 kernels) done")
