@@ -257,6 +257,7 @@ bool cols_base(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64
     const int64_t n = rows_pad * cols;
     // stream-ordered scratch (transposed copies), freed after use
     void *t_in = nullptr, *t_out = nullptr;
+    retain_async_pool();
     if (cudaMallocAsync(&t_in, (size_t)n * (mode == 2 ? 4 : esz), st) != cudaSuccess) return false;
     if (cudaMallocAsync(&t_out, (size_t)n * (mode == 2 ? 4 : 1), st) != cudaSuccess) {
         cudaFreeAsync(t_in, st);

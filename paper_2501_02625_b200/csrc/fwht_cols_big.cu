@@ -255,6 +255,7 @@ bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_
     // stream-ordered scratch for the partial transform: no sharing between
     // streams or calls, returned to the pool after the last reader
     float* buf = nullptr;
+    retain_async_pool();
     if (cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)rows_pad * (size_t)cols * sizeof(float), st) !=
         cudaSuccess)
         return false;

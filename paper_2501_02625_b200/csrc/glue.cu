@@ -234,4 +234,16 @@ void run_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, cudaStream
     k_fp6_unpack<<<ew_grid(n * 2), 256, 0, st>>>(packed, codes, n / 4);
 }
 
+void retain_async_pool() {
+    static thread_local int done_dev = -1;
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = d;
+}
+
 }  // namespace halo_b200

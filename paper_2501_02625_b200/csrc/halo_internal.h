@@ -9,6 +9,11 @@
 namespace halo_b200 {
 
 int num_sms();
+// stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; with the default release threshold (0) every synchronisation hands
+// the pages back and the next allocation re-maps them (tens of ms for the
+// large-block K2 scratch).  Called before such allocations: keep the pool.
+void retain_async_pool();
 // MXFP6 (NumericFormat::MxFp6E3M2, id 3) has E3M2 codes under power-of-two
 // 1 x 32 block scales (quantize.hpp:224-232, mx_quantize); kernels that only
 // see codes (GEMMs, deq_gemm) treat it as FMT_E3M2
