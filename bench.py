@@ -178,8 +178,7 @@ def run_reference(args, rank, world):
 
 
 CFG5_NAME = ("HQ-FSDP Llama-3-8B ({layers} layers) HALO-2 {fmt} fine-tuning step, {tokens} tokens/GPU (seq 2048), "
-             "INT8 weight all-gather + regather, dW reduce-scatter, AdamW on sharded bf16 masters, "
-             "activation checkpointing")
+             "INT8 weight all-gather + regather, dW reduce-scatter, AdamW on sharded bf16 masters, {ac}")
 
 
 def run_cfg5(args, world, rank, local, dev, fmt):
@@ -192,7 +191,7 @@ def run_cfg5(args, world, rank, local, dev, fmt):
     from paper_2501_02625_b200.train import HqFsdpLlama, LlamaDims
     d = LlamaDims(layers=args.layers)
     b = args.tokens or 4 * d.seq
-    model = HqFsdpLlama(d, halo.halo2(fmt, args.block), seed=1234)
+    model = HqFsdpLlama(d, halo.halo2(fmt, args.block), seed=1234, activation_checkpoint=args.ac)
     g = torch.Generator(device=dev).manual_seed(4321 + rank)
     bf = torch.bfloat16
     x = torch.randn(b, d.hidden, generator=g, device=dev)
@@ -257,7 +256,9 @@ def run_cfg5(args, world, rank, local, dev, fmt):
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": {halo.INT8: "int8", halo.FP8_E4M3: "fp8_e4m3", halo.FP6_E3M2: "fp6_e3m2"}[fmt],
                "data": "synthetic",
-               "config": {"workload": CFG5_NAME.format(layers=d.layers, fmt=args.fmt.upper(), tokens=b),
+               "config": {"workload": CFG5_NAME.format(layers=d.layers, fmt=args.fmt.upper(), tokens=b,
+                                                       ac="activation checkpointing" if args.ac else
+                                                       "activations kept (no checkpointing)"),
                           "global_batch": b * world, "seq_len": d.seq, "tokens_per_gpu": b, "layers": d.layers,
                           "hadamard_block": args.block,
                           "parallelism": f"hq-fsdp{world} (NCCL INT8 all-gather one layer ahead on a side stream)"
@@ -293,6 +294,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32, help="cfg5: decoder layers (Llama-3-8B: 32)")
+    ap.add_argument("--ac", action="store_true",
+                    help="cfg5: activation checkpointing (one regather feeds recompute + backward); default off, "
+                         "the reference's FsdpSimConfig default")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg1", "cfg5"],
                     help="cfg2 (default): the Llama-3-8B MLP at 8192 tokens; cfg1: BASELINE configs[0], one HALO-2 "
                          "linear 4096 -> 4096 at 2048 tokens")

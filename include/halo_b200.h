@@ -273,6 +273,13 @@ HALO_API halo_status halo_ctx_saved(const halo_ctx* ctx, const uint8_t** xq, con
 /* backward scratch views of the last backward: E quantizations and scales */
 HALO_API halo_status halo_ctx_error_operands(const halo_ctx* ctx, const uint8_t** ehq, const float** seh,
                                     const uint8_t** eq, const float** se, int64_t* b_pad);
+/* the backward scratch of `ctx` (error-operand codes and scales, the E / G
+ * products' fp32 buffers) lives in `owner` from now on (NULL: its own again):
+ * contexts whose backwards run one after another on one stream -- e.g. the
+ * layers of a stack without activation checkpointing -- share one set
+ * instead of holding one each.  `owner` must outlive `ctx`'s backward calls;
+ * halo_ctx_error_operands then reports the shared buffers. */
+HALO_API halo_status halo_ctx_share_scratch(halo_ctx* ctx, halo_ctx* owner);
 /* synchronises `stream` and reports device-side numeric errors (NaN/Inf in
  * an input: tensor.hpp:86-91, quantize.hpp:292/373) as HALO_ERR_NUMERIC,
  * then clears the flag. */

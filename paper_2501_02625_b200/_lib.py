@@ -172,6 +172,8 @@ def lib():
         getattr(L, fn).restype = C.c_int
     L.halo_rotate_quantize_mx.argtypes = [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp]
     L.halo_rotate_quantize_mx.restype = C.c_int
+    L.halo_ctx_share_scratch.argtypes = [_vp, _vp]
+    L.halo_ctx_share_scratch.restype = C.c_int
     L.halo_allow_dequantized_products.argtypes = [_i32]
     L.halo_allow_dequantized_products.restype = C.c_int
     L.halo_fp6_pack.argtypes = [_vp, _vp, _i64, _vp]
@@ -251,5 +253,5 @@ EXPORTS = (
     "halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
     "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
     "halo_fsdp_all_reduce_mean", "halo_fp6_pack", "halo_fp6_unpack",
-    "halo_allow_dequantized_products", "halo_rotate_quantize_mx",
+    "halo_allow_dequantized_products", "halo_rotate_quantize_mx", "halo_ctx_share_scratch",
 )

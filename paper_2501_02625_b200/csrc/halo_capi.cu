@@ -185,6 +185,11 @@ struct halo_ctx {
     // with this X buffer (h) by the fused pass
     const void* x_amax_src = nullptr;
     int64_t x_amax_b = 0;
+    // backward scratch (eq, ehq, scratch, gscratch, per-row / MX scale
+    // scratch) may live in another context: contexts whose backwards run
+    // one after another on one stream share one set (halo_ctx_share_scratch)
+    halo_ctx* sowner = nullptr;
+    halo_ctx* S() { return sowner ? sowner : this; }
     const uint8_t* xq_codes() const { return xq_borrow ? xq_borrow : xq.as<uint8_t>(); }
     DevScalars* d() const { return dev.as<DevScalars>(); }
     ~halo_ctx() {
@@ -953,13 +958,13 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         const int64_t tmp = (rmax * m > b * n ? rmax * m : b * n) * (int64_t)sizeof(float);
         if (c->xs_rows.ensure((size_t)(b * nb) * sizeof(float)) != HALO_OK ||
             c->ws_rows.ensure((size_t)(n * nb) * sizeof(float)) != HALO_OK || c->wq.ensure((size_t)(n * m)) != HALO_OK ||
-            c->gscratch.ensure((size_t)tmp) != HALO_OK || c->scratch.ensure((size_t)(rmax * m) * sizeof(float)) != HALO_OK)
+            c->S()->gscratch.ensure((size_t)tmp) != HALO_OK || c->S()->scratch.ensure((size_t)(rmax * m) * sizeof(float)) != HALO_OK)
             return HALO_ERR_CUDA;
         // quantize([A H], mxfp6, mx) (:292-297)
         auto quant_side = [&](const void* src, int32_t dt, int64_t rows, uint8_t* codes, float* scales) -> bool {
             if (rot) {
-                float* T0 = c->gscratch.as<float>();
-                float* T1 = c->scratch.as<float>();
+                float* T0 = c->S()->gscratch.as<float>();
+                float* T1 = c->S()->scratch.as<float>();
                 pad_rows_f32(src, dt, rows, rows, m, T0, st);
                 BaseScope h(false);  // transform_right (H)
                 run_rows(T0, HALO_DTYPE_F32, rows, m, B, 2, 0, nullptr, nullptr, nullptr, T1, HALO_DTYPE_F32, nullptr,
@@ -983,7 +988,7 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         c->wq_codes = c->wq.as<uint8_t>();
         c->wq_scale = c->ws_rows.as<float>();
         c->xq_scale = c->xs_rows.as<float>();
-        float* P = c->gscratch.as<float>();
+        float* P = c->S()->gscratch.as<float>();
         {
             // A = xq (i = token, k = in): scale [i][k >> 5]; B = wq^T (k = in,
             // j = out): scale [j][k >> 5]
@@ -1007,15 +1012,15 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         const int64_t tmp = (rmax * m > b * n ? rmax * m : b * n) * (int64_t)sizeof(float);
         if (c->xs_rows.ensure((size_t)m * sizeof(float)) != HALO_OK || c->ws_rows.ensure((size_t)m * sizeof(float)) != HALO_OK ||
             c->amax_rows.ensure((size_t)m * sizeof(unsigned)) != HALO_OK || c->wq.ensure((size_t)(n * m)) != HALO_OK ||
-            c->gscratch.ensure((size_t)tmp) != HALO_OK || c->scratch.ensure((size_t)(rmax * m) * sizeof(float)) != HALO_OK)
+            c->S()->gscratch.ensure((size_t)tmp) != HALO_OK || c->S()->scratch.ensure((size_t)(rmax * m) * sizeof(float)) != HALO_OK)
             return HALO_ERR_CUDA;
         // quantize([A H], fmt, column) (:292-297)
         auto quant_side = [&](const void* src, int32_t dt, int64_t rows, uint8_t* codes, float* scales) -> bool {
             const void* q = src;
             int32_t qdt = dt;
             if (rot) {
-                float* T0 = c->gscratch.as<float>();
-                float* T1 = c->scratch.as<float>();
+                float* T0 = c->S()->gscratch.as<float>();
+                float* T1 = c->S()->scratch.as<float>();
                 pad_rows_f32(src, dt, rows, rows, m, T0, st);
                 BaseScope h(false);  // transform_right (H)
                 run_rows(T0, HALO_DTYPE_F32, rows, m, B, 2, 0, nullptr, nullptr, nullptr, T1, HALO_DTYPE_F32, nullptr,
@@ -1040,7 +1045,7 @@ extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_
         c->wq_codes = c->wq.as<uint8_t>();
         c->wq_scale = c->ws_rows.as<float>();
         c->xq_scale = c->xs_rows.as<float>();
-        float* P = c->gscratch.as<float>();
+        float* P = c->S()->gscratch.as<float>();
         {
             ProfScope ps(PC_GEMM, 2.0 * (double)b * n * m, st);
             if (!deq_gemm(s.format_x, c->xq.as<uint8_t>(), c->xs_rows.as<float>(), m, 1, 0, 1, c->wq_codes,
@@ -1254,40 +1259,40 @@ static halo_status backward_grouped(halo_linear* l, halo_ctx* c, const void* e_y
         return HALO_ERR_INVALID_ARGUMENT;
     c->b_pad = b_pad;
     const int64_t mx = b_pad > n ? b_pad : n;
-    if (c->eq.ensure((size_t)(b * n)) != HALO_OK || c->es_rows.ensure((size_t)mx * sizeof(float)) != HALO_OK ||
+    if (c->S()->eq.ensure((size_t)(b * n)) != HALO_OK || c->S()->es_rows.ensure((size_t)mx * sizeof(float)) != HALO_OK ||
         c->amax_rows.ensure((size_t)mx * sizeof(unsigned)) != HALO_OK ||
-        c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
+        c->S()->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
         return HALO_ERR_CUDA;
     // (E_Y)_Q per token (:371); feeds E (no left rotation) and G
     const bool plain = grad_w || !left;
     if (plain) {
         ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
-        if (!gquant(e_dtype, e_y, b, c->es_rows.as<float>(), c->eq.as<uint8_t>()))
+        if (!gquant(e_dtype, e_y, b, c->S()->es_rows.as<float>(), c->S()->eq.as<uint8_t>()))
             return fail(HALO_ERR_INVALID_ARGUMENT, "backward: row-granularity operands must be 32 B aligned");
         ++l->ce;
     }
-    float* P = c->scratch.as<float>();
+    float* P = c->S()->scratch.as<float>();
     // ---- error path (:381-413)
     if (left) {
         // (H_b pad(E_Y))_Q per padded token (:393-399)
-        if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->ehs_rows.ensure((size_t)mx * sizeof(float)) != HALO_OK ||
-            c->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
+        if (c->S()->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->S()->ehs_rows.ensure((size_t)mx * sizeof(float)) != HALO_OK ||
+            c->S()->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
             return HALO_ERR_CUDA;
-        float* T = c->gscratch.as<float>();
+        float* T = c->S()->gscratch.as<float>();
         {
             ProfScope ps(PC_K2, (double)b * n * dt_bytes(e_dtype) + (double)b_pad * n * 9, st);
             pad_rows_f32(e_y, e_dtype, b, b_pad, n, T, st);
             BaseScope orient(true);  // transform_left_h (:398)
             run_cols(T, HALO_DTYPE_F32, b_pad, b_pad, n, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                      T, b_pad, nullptr, nullptr, nullptr, st);
-            if (!gquant(HALO_DTYPE_F32, T, b_pad, c->ehs_rows.as<float>(), c->ehq.as<uint8_t>()))
+            if (!gquant(HALO_DTYPE_F32, T, b_pad, c->S()->ehs_rows.as<float>(), c->S()->ehq.as<uint8_t>()))
                 return fail(HALO_ERR_INVALID_ARGUMENT, "backward: row-granularity operands must be 32 B aligned");
         }
         ++l->ce;
         if (e_x) {
             {
                 ProfScope ps(PC_GEMM, 2.0 * (double)b_pad * m * n, st);
-                if (!deq_gemm(fmt, c->ehq.as<uint8_t>(), c->ehs_rows.as<float>(), n, 1, e_si, e_sk, c->wq_codes,
+                if (!deq_gemm(fmt, c->S()->ehq.as<uint8_t>(), c->S()->ehs_rows.as<float>(), n, 1, e_si, e_sk, c->wq_codes,
                               c->wq_scale, m, 1, w_sk, w_sj, P, b_pad, m, n, m, st))
                     return fail(HALO_ERR_CUDA, "backward: E product launch failed");
             }
@@ -1299,7 +1304,7 @@ static halo_status backward_grouped(halo_linear* l, halo_ctx* c, const void* e_y
         }
     } else if (e_x) {
         ProfScope ps(PC_GEMM, 2.0 * (double)b * m * n, st);
-        if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), n, 1, e_si, e_sk, c->wq_codes, c->wq_scale, m,
+        if (!deq_gemm(fmt, c->S()->eq.as<uint8_t>(), c->S()->es_rows.as<float>(), n, 1, e_si, e_sk, c->wq_codes, c->wq_scale, m,
                       1, w_sk, w_sj, P, b, m, n, m, st))
             return fail(HALO_ERR_CUDA, "backward: E product launch failed");
     }
@@ -1308,11 +1313,11 @@ static halo_status backward_grouped(halo_linear* l, halo_ctx* c, const void* e_y
     // ---- gradient path (:418-439): G = transpose_quantized(eq) (XH)_Q [H^T];
     // E_Y^T's scales become per-column (:312-316)
     if (grad_w) {
-        if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
-        float* G = c->gscratch.as<float>();
+        if (c->S()->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+        float* G = c->S()->gscratch.as<float>();
         {
             ProfScope ps(PC_GEMM, 2.0 * (double)n * m * b, st);
-            if (!deq_gemm(fmt, c->eq.as<uint8_t>(), c->es_rows.as<float>(), 1, n, g_si, g_sk, c->xq_codes(), c->xq_scale,
+            if (!deq_gemm(fmt, c->S()->eq.as<uint8_t>(), c->S()->es_rows.as<float>(), 1, n, g_si, g_sk, c->xq_codes(), c->xq_scale,
                           m, 1, x_sk, x_sj, G, n, m, b, m, st))
                 return fail(HALO_ERR_CUDA, "backward: G product launch failed");
         }
@@ -1349,10 +1354,10 @@ static halo_status backward_mx(halo_linear* l, halo_ctx* c, const void* e_y, int
         return HALO_ERR_INVALID_ARGUMENT;
     c->b_pad = b_pad;
     const int64_t nbn = n / 32, nbm = m / 32, nbb = (b + 31) / 32;
-    if (c->eq.ensure((size_t)(b_pad * n)) != HALO_OK || c->es_rows.ensure((size_t)(b_pad * nbn) * sizeof(float)) != HALO_OK ||
-        c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
+    if (c->S()->eq.ensure((size_t)(b_pad * n)) != HALO_OK || c->S()->es_rows.ensure((size_t)(b_pad * nbn) * sizeof(float)) != HALO_OK ||
+        c->S()->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK)
         return HALO_ERR_CUDA;
-    float* P = c->scratch.as<float>();
+    float* P = c->S()->scratch.as<float>();
     // ---- error path (:381-413): A = E codes (i = token, k = out, scale
     // [i][k >> 5]); B = wq (k = out, j = in, scale [k][j >> 5])
     if (e_x) {
@@ -1360,26 +1365,26 @@ static halo_status backward_mx(halo_linear* l, halo_ctx* c, const void* e_y, int
         const float* escales;
         int64_t rows = b;
         if (left) {
-            if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->ehs_rows.ensure((size_t)(b_pad * nbn) * sizeof(float)) != HALO_OK ||
-                c->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
+            if (c->S()->ehq.ensure((size_t)(b_pad * n)) != HALO_OK || c->S()->ehs_rows.ensure((size_t)(b_pad * nbn) * sizeof(float)) != HALO_OK ||
+                c->S()->gscratch.ensure((size_t)(b_pad * n) * sizeof(float)) != HALO_OK)
                 return HALO_ERR_CUDA;
-            float* T = c->gscratch.as<float>();
+            float* T = c->S()->gscratch.as<float>();
             ProfScope ps(PC_K2, (double)b * n * dt_bytes(e_dtype) + (double)b_pad * n * 9, st);
             pad_rows_f32(e_y, e_dtype, b, b_pad, n, T, st);
             BaseScope orient(true);  // transform_left_h (:398)
             run_cols(T, HALO_DTYPE_F32, b_pad, b_pad, n, Bb, 2, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                      T, b_pad, nullptr, nullptr, nullptr, st);
-            if (!mx_quantize(HALO_DTYPE_F32, T, b_pad, n, n, 1, c->ehq.as<uint8_t>(), c->ehs_rows.as<float>(), &d->err, st))
+            if (!mx_quantize(HALO_DTYPE_F32, T, b_pad, n, n, 1, c->S()->ehq.as<uint8_t>(), c->S()->ehs_rows.as<float>(), &d->err, st))
                 return fail(HALO_ERR_CUDA, "backward: mx quantization failed");
-            ecodes = c->ehq.as<uint8_t>();
-            escales = c->ehs_rows.as<float>();
+            ecodes = c->S()->ehq.as<uint8_t>();
+            escales = c->S()->ehs_rows.as<float>();
             rows = b_pad;
         } else {
             ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
-            if (!mx_quantize(e_dtype, e_y, b, n, n, 1, c->eq.as<uint8_t>(), c->es_rows.as<float>(), &d->err, st))
+            if (!mx_quantize(e_dtype, e_y, b, n, n, 1, c->S()->eq.as<uint8_t>(), c->S()->es_rows.as<float>(), &d->err, st))
                 return fail(HALO_ERR_CUDA, "backward: mx quantization failed");
-            ecodes = c->eq.as<uint8_t>();
-            escales = c->es_rows.as<float>();
+            ecodes = c->S()->eq.as<uint8_t>();
+            escales = c->S()->es_rows.as<float>();
         }
         ++l->ce;
         {
@@ -1400,18 +1405,18 @@ static halo_status backward_mx(halo_linear* l, halo_ctx* c, const void* e_y, int
     // blocks along tokens (A: i = out, k = token, scale [i][k >> 5]); B =
     // (XH)_Q (k = token, j = in, scale [k][j >> 5])
     if (grad_w) {
-        if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK || c->mx_t.ensure((size_t)(n * b)) != HALO_OK ||
-            c->mx_ts.ensure((size_t)(n * nbb) * sizeof(float)) != HALO_OK)
+        if (c->S()->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK || c->S()->mx_t.ensure((size_t)(n * b)) != HALO_OK ||
+            c->S()->mx_ts.ensure((size_t)(n * nbb) * sizeof(float)) != HALO_OK)
             return HALO_ERR_CUDA;
-        uint8_t* et = c->mx_t.as<uint8_t>();
-        float* ets = c->mx_ts.as<float>();
+        uint8_t* et = c->S()->mx_t.as<uint8_t>();
+        float* ets = c->S()->mx_ts.as<float>();
         {
             ProfScope ps(PC_K2, (double)b * n * (dt_bytes(e_dtype) + 1), st);
             if (!mx_quantize(e_dtype, e_y, n, b, 1, n, et, ets, &d->err, st))
                 return fail(HALO_ERR_CUDA, "backward: mx quantization failed");
         }
         ++l->ce;
-        float* G = c->gscratch.as<float>();
+        float* G = c->S()->gscratch.as<float>();
         {
             ProfScope ps(PC_GEMM, 2.0 * (double)n * m * b, st);
             if (!deq_gemm(fmt, et, ets, b, 1, nbb, 1, c->xq_codes(), c->xq_scale, m, 1, nbm, 1, G, n, m, b, m, st, 0, 5,
@@ -1442,7 +1447,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
     int64_t Bm = 1;
     if ((s.E.right || s.G.right) && resolve_block(m, s.had_block, &Bm, "backward") != HALO_OK)
         return HALO_ERR_INVALID_ARGUMENT;
-    if (c->eq.ensure((size_t)(b * n)) != HALO_OK) return HALO_ERR_CUDA;
+    if (c->S()->eq.ensure((size_t)(b * n)) != HALO_OK) return HALO_ERR_CUDA;
 
     // weight operand for E with E's right rotation (:390)
     const uint8_t* wq = c->wq_codes;
@@ -1467,8 +1472,8 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         int64_t Bb;
         if (resolve_block(b_pad, s.had_block, &Bb, "backward (token dim)") != HALO_OK) return HALO_ERR_INVALID_ARGUMENT;
         c->b_pad = b_pad;
-        if (c->ehq.ensure((size_t)(b_pad * n)) != HALO_OK) return HALO_ERR_CUDA;
-        if (c->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+        if (c->S()->ehq.ensure((size_t)(b_pad * n)) != HALO_OK) return HALO_ERR_CUDA;
+        if (c->S()->scratch.ensure((size_t)(b_pad * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
         // (H_b E_Y)_Q and (E_Y)_Q in one pass (:399 and :371); the plain
         // codes only feed G, so PEFT / no-grad_w backwards skip them (:446-448)
         const bool plain = (grad_w || l->scatter) && !s.peft;
@@ -1476,25 +1481,25 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         // this E_Y: skip K2's phase A
         const bool have_amax = c->e_amax_src == e_y && c->e_amax_b == b && e_dtype == HALO_DTYPE_BF16;
         c->e_amax_src = nullptr;
-        halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->ehq.as<uint8_t>(),
-                                        plain ? c->eq.as<uint8_t>() : nullptr, &d->amax[SEH], &d->amax[SE],
+        halo_status r = left_quant_impl(e_y, e_dtype, b, n, Bb, b_pad, fmt, c->S()->ehq.as<uint8_t>(),
+                                        plain ? c->S()->eq.as<uint8_t>() : nullptr, &d->amax[SEH], &d->amax[SE],
                                         &d->scale[SEH], &d->scale[SE], &d->err, st, have_amax, !s.peft);
         if (r != HALO_OK) return r;
         l->ce += plain ? 2 : 1;
-        float* P = c->scratch.as<float>();
+        float* P = c->S()->scratch.as<float>();
         if (fuse_k4() && fusable_block(Bb)) {
             // prod^T = wq^T ehq^T (:401, transposed: M = in-features,
             // N = padded tokens); the epilogue applies transform_left over
             // the token axis (:405-408) and stores take_rows(b) of prod
             // (:409) row-major.  ss = sw * s_ehq: same exact double product.
             ShardScope shards(wsh, nullptr);  // A = (WH)_Q, MN-major, K = out_features
-            int gr = prof_gemm_x(fmt, wq, c->ehq.as<uint8_t>(), m, b_pad, n, 0, 1, sw, &d->scale[SEH], P, 0, Bb, 1, b,
+            int gr = prof_gemm_x(fmt, wq, c->S()->ehq.as<uint8_t>(), m, b_pad, n, 0, 1, sw, &d->scale[SEH], P, 0, Bb, 1, b,
                                  st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
         } else {
             // prod = qmatmul(eq, wq)  (:401): B operand (n x m) is MN-major
             ShardScope shards(nullptr, wsh);
-            int gr = prof_gemm(fmt, c->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
+            int gr = prof_gemm(fmt, c->S()->ehq.as<uint8_t>(), wq, b_pad, m, n, 1, 0, &d->scale[SEH], sw, P, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
             // prod = transform_left(prod); take_rows(b)  (:405-409), in place
             ProfScope ps(PC_K4, (double)b_pad * m * 4 + (double)b * m * 4, st);
@@ -1506,7 +1511,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st);
     } else {
         c->b_pad = b;
-        const halo_status r = rotate_quantize_impl(e_y, e_dtype, b, n, 1, false, fmt, nullptr, c->eq.as<uint8_t>(),
+        const halo_status r = rotate_quantize_impl(e_y, e_dtype, b, n, 1, false, fmt, nullptr, c->S()->eq.as<uint8_t>(),
                                                    &d->amax[SE], &d->scale[SE], &d->err, st);
         if (r != HALO_OK) return r;
         l->ce += 1;
@@ -1514,17 +1519,17 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         if (s.E.right && fuse_k4() && fusable_block(Bm)) {
             // E_X = (E_Y)_Q (WH)_Q H^T (:410-411) with the right transform in
             // the GEMM epilogue
-            int gr = prof_gemm_x(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
+            int gr = prof_gemm_x(fmt, c->S()->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
                                  ex_dtype == HALO_DTYPE_F32 ? 0 : 1, Bm, 0, m, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
         } else if (s.E.right) {
-            if (c->scratch.ensure((size_t)(b * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
-            float* P = c->scratch.as<float>();
-            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
+            if (c->S()->scratch.ensure((size_t)(b * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+            float* P = c->S()->scratch.as<float>();
+            int gr = prof_gemm(fmt, c->S()->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
             finish_right(P, e_x, ex_dtype, b, m, Bm, true, st);
         } else {
-            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
+            int gr = prof_gemm(fmt, c->S()->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
                               ex_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
         }
@@ -1543,9 +1548,9 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
             if (s.G.right && !(fuse_k4() && fusable_block(Bm)))
                 return fail(HALO_ERR_INVALID_ARGUMENT, "backward: scattered G needs the fused right transform");
             ShardScope scat(nullptr, nullptr, &l->scatter_c);
-            const int gr = s.G.right ? prof_gemm_x(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp,
+            const int gr = s.G.right ? prof_gemm_x(fmt, c->S()->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp,
                                                    nullptr, 0, Bm, 0, m, st)
-                                     : prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp,
+                                     : prof_gemm(fmt, c->S()->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp,
                                                  nullptr, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: scattered G GEMM launch failed");
             return cuda_check("backward");
@@ -1553,17 +1558,17 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         if (s.G.right && fuse_k4() && fusable_block(Bm)) {
             // grad_w = (E_Y^T)_Q (XH)_Q H^T (:433-437), the right transform in
             // the GEMM epilogue
-            int gr = prof_gemm_x(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, grad_w,
+            int gr = prof_gemm_x(fmt, c->S()->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, grad_w,
                                  gw_dtype == HALO_DTYPE_F32 ? 0 : 1, Bm, 0, m, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
         } else if (s.G.right) {
-            if (c->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
-            float* G = c->gscratch.as<float>();
-            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, G, 0, st);
+            if (c->S()->gscratch.ensure((size_t)(n * m) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+            float* G = c->S()->gscratch.as<float>();
+            int gr = prof_gemm(fmt, c->S()->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, G, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
             finish_right(G, grad_w, gw_dtype, n, m, Bm, true, st);
         } else {
-            int gr = prof_gemm(fmt, c->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, grad_w,
+            int gr = prof_gemm(fmt, c->S()->eq.as<uint8_t>(), xq, n, m, b, 0, 0, &d->scale[SE], sxp, grad_w,
                               gw_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: G GEMM launch failed");
         }
@@ -1628,11 +1633,20 @@ extern "C" halo_status halo_ctx_error_operands(const halo_ctx* c, const uint8_t*
     // row / column granularity: the scale vectors of the last backward
     // (per token for ROW: b_pad / b floats; per column for COLUMN: out_features)
     const bool grouped = c->gran != HALO_GRAN_TENSOR;
-    if (ehq) *ehq = c->ehq.as<uint8_t>();
-    if (seh) *seh = grouped ? c->ehs_rows.as<float>() : &c->d()->scale[SEH];
-    if (eq) *eq = c->eq.as<uint8_t>();
-    if (se) *se = grouped ? c->es_rows.as<float>() : &c->d()->scale[SE];
+    const halo_ctx* sc = c->sowner ? c->sowner : c;
+    if (ehq) *ehq = sc->ehq.as<uint8_t>();
+    if (seh) *seh = grouped ? sc->ehs_rows.as<float>() : &c->d()->scale[SEH];
+    if (eq) *eq = sc->eq.as<uint8_t>();
+    if (se) *se = grouped ? sc->es_rows.as<float>() : &c->d()->scale[SE];
     if (b_pad) *b_pad = c->b_pad;
+    return HALO_OK;
+}
+
+extern "C" halo_status halo_ctx_share_scratch(halo_ctx* ctx, halo_ctx* owner) {
+    if (!ctx) return fail(HALO_ERR_INVALID_ARGUMENT, "ctx: null");
+    if (owner == ctx) owner = nullptr;
+    if (owner && owner->sowner) owner = owner->sowner;
+    ctx->sowner = owner;
     return HALO_OK;
 }
 

@@ -376,6 +376,12 @@ class SavedContext:
             out["seh"] = _from_ptr(seh.value, (n_seh,), torch.float32)
         return out
 
+    def share_scratch(self, owner: "SavedContext | None"):
+        """Use `owner`'s backward scratch (halo_ctx_share_scratch): contexts
+        whose backwards run one after another share one set of buffers."""
+        check(lib().halo_ctx_share_scratch(self._h, owner._h if owner is not None else None))
+        self._scratch_owner = owner  # keep it alive
+
     def check(self):
         """Synchronise and raise HaloNumericError for non-finite inputs."""
         check(lib().halo_ctx_check(self._h, _stream()))

@@ -127,7 +127,7 @@ class HqFsdpLlama:
 
     def __init__(self, dims: LlamaDims, scheme, group=None, seed: int = 0, device="cuda",
                  check_stale: bool = True, prefetch: bool = True, opt: AdamWConfig | None = None,
-                 data_plane: str = "native"):
+                 data_plane: str = "native", activation_checkpoint: bool = False):
         self.d = dims
         self.scheme = scheme
         self.group = group
@@ -136,10 +136,12 @@ class HqFsdpLlama:
         self.fmt = scheme.format_w
         self.block = scheme.had_block
         self.rotate = bool(scheme.F.middle)
-        # activation checkpointing is how the stack runs: one set of HALO
-        # projections (and their saved contexts) serves every layer, so a
-        # layer's context only lives from its recompute to its backward
-        self.ac = True
+        # FsdpSimConfig::activation_checkpoint (hqfsdp.hpp:300-310, default
+        # off): on, only layer inputs are kept and the backward recomputes
+        # each layer on its one regather (two consumers); off, every layer
+        # keeps its activations and its own HALO contexts, and the regather
+        # feeds the backward alone
+        self.ac = activation_checkpoint
         self.check_stale = check_stale
         self.prefetch = prefetch
         self.device = torch.device(device)
@@ -164,24 +166,29 @@ class HqFsdpLlama:
         for lay, (n1, n2) in zip(self.masters, self.norms):
             params += [lay[name].master for name in WEIGHTS] + [n1, n2]
         self.opt = DeviceAdamW(params, opt)
-        # one set of HALO projections serves every layer: the layer's gathered
-        # codes are installed before it runs (set_qweight); the placeholder
-        # weights are never read once codes are installed
+        # HALO projections run on installed gathered codes (set_qweight); the
+        # placeholder weights are never read.  With checkpointing one executor
+        # (projections + contexts) and two code slots serve every layer;
+        # without, each layer has its own executor and code buffer, since its
+        # contexts must live from its forward to its backward
         self._dummy = {name: torch.zeros(shapes[name], dtype=bf, device=self.device) for name in WEIGHTS}
-        self.lin = {name: HaloLinear(self._dummy[name], scheme) for name in ("qkv", "o")}
-        from .mlp import HaloMLP
-        self.mlp = HaloMLP(self._dummy["gate"], self._dummy["up"], self._dummy["down"], scheme)
-        self.mlp_owners = [_GradSink(), _GradSink(), _GradSink()]
-        self.mlp.owners = self.mlp_owners
-        self.layers_of = {"qkv": self.lin["qkv"].layer, "o": self.lin["o"].layer, "gate": self.mlp.gate,
-                          "up": self.mlp.up, "down": self.mlp.down}
+        nexec = 1 if self.ac else dims.layers
+        self.execs = [_Executor(self._dummy, scheme) for _ in range(nexec)]
+        # without checkpointing every layer keeps its contexts to its
+        # backward, but the backwards run one at a time: one backward
+        # scratch serves all (≈1.7 GB per layer at 8192 tokens otherwise)
+        self._scratch = halo.SavedContext()
+        for ex in self.execs:
+            for ctx in ex.contexts():
+                ctx.share_scratch(self._scratch)
         code_dt = halo.code_dtype(self.fmt)
         p0 = self.masters[0]
+        nslots = 2 if self.ac else dims.layers
         self.codes = [{name: torch.empty((p0[name].shard_rows * self.world, p0[name].cols), dtype=code_dt,
-                                         device=self.device) for name in WEIGHTS} for _ in range(2)]
-        self.scales = [dict() for _ in range(2)]
+                                         device=self.device) for name in WEIGHTS} for _ in range(nslots)]
+        self.scales = [dict() for _ in range(nslots)]
         self.comm = torch.cuda.Stream(device=self.device)
-        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.ready = [torch.cuda.Event() for _ in range(nslots)]
         self.ledger = fsdp.CommLedger()
         # the collectives: the library's C++ NCCL data plane (halo_fsdp_*) or
         # torch.distributed (the protocol functions of fsdp.py)
@@ -192,10 +199,16 @@ class HqFsdpLlama:
         self.cs = rope_table(dims.seq, dims.head_dim, self.device)
 
     # ------------------------------------------------------------ weights
+    def _slot(self, l: int) -> int:
+        return l % 2 if self.ac else l
+
+    def _exec(self, l: int) -> "_Executor":
+        return self.execs[0] if self.ac else self.execs[l]
+
     def _fetch(self, l: int, regather: bool):
-        """Gather (or regather) layer l's five code tensors into slot l % 2 on
+        """Gather (or regather) layer l's five code tensors into its slot on
         the side stream; `ready[slot]` fires when they are complete."""
-        slot = l % 2
+        slot = self._slot(l)
         main = torch.cuda.current_stream(self.device)
         side = self.comm if self.prefetch else main
         # the slot was last read by layer l -/+ 2, enqueued before this point
@@ -211,8 +224,9 @@ class HqFsdpLlama:
                     else:
                         codes, scale = fsdp.backward_regather(p, self.rotate, self.ledger, self.check_stale,
                                                               self.block, self.group, out=out, stale_flag=self.stale)
-                    # one regather, two consumers: recompute forward + backward
-                    self.ledger.backward_consumers += 2
+                    # with checkpointing one regather feeds two consumers:
+                    # the recompute forward and the backward (:308-310, 384)
+                    self.ledger.backward_consumers += 2 if self.ac else 1
                 elif self.plane is not None:
                     codes, scale = self.plane.gather(p, self.rotate, self.block, out, self.ledger)
                 else:
@@ -221,30 +235,23 @@ class HqFsdpLlama:
                 self.scales[slot][name] = scale
             self.ready[slot].record(side)
 
-    def _install(self, l: int):
-        slot = l % 2
-        torch.cuda.current_stream(self.device).wait_event(self.ready[slot])
+    def _install(self, l: int, wait: bool = True):
+        slot = self._slot(l)
+        if wait:
+            torch.cuda.current_stream(self.device).wait_event(self.ready[slot])
+        ex = self._exec(l)
         for name in WEIGHTS:
             p = self.masters[l][name]
-            self.layers_of[name].set_qweight(self.codes[slot][name][: p.full_rows], self.scales[slot][name])
+            ex.layers_of[name].set_qweight(self.codes[slot][name][: p.full_rows], self.scales[slot][name])
 
     # -------------------------------------------------------------- block
     def _block(self, x: torch.Tensor, l: int) -> torch.Tensor:
         """Llama block (block.attention_block) on the installed codes."""
         d = self.d
         n1, n2 = self.norms[l]
-        return attention_block(x, self.lin["qkv"], self.lin["o"], lambda m: _HaloMLPFn.apply(m, self.mlp), n1, n2,
+        ex = self._exec(l)
+        return attention_block(x, ex.lin["qkv"], ex.lin["o"], lambda m: _HaloMLPFn.apply(m, ex.mlp), n1, n2,
                                self.cs, d.seq, d.heads, d.kv_heads)
-
-    def _zero_grads(self):
-        for lin in self.lin.values():
-            lin.grad = None
-        for s in self.mlp_owners:
-            s.grad = None
-
-    def _grads(self):
-        return {"qkv": self.lin["qkv"].grad, "o": self.lin["o"].grad, "gate": self.mlp_owners[0].grad,
-                "up": self.mlp_owners[1].grad, "down": self.mlp_owners[2].grad}
 
     # --------------------------------------------------------------- step
     def step(self, x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
@@ -253,38 +260,56 @@ class HqFsdpLlama:
         Returns dL/dx of the stack input."""
         L = self.d.layers
         self.opt.begin_step()
-        # ---------------- forward (weights gathered one layer ahead); only
-        # the layer inputs are kept
+        # ---------------- forward (weights gathered one layer ahead)
         saved = []
         h = x
         self._fetch(0, regather=False)
-        with torch.no_grad():
-            for l in range(L):
-                self._install(l)
-                if l + 1 < L:
-                    self._fetch(l + 1, regather=False)
-                saved.append(h)
-                h = self._block(h, l)
+        for l in range(L):
+            self._install(l)
+            if l + 1 < L:
+                self._fetch(l + 1, regather=False)
+            if self.ac:  # only the layer input is kept
+                with torch.no_grad():
+                    saved.append(h)
+                    h = self._block(h, l)
+            else:  # the layer's graph (and its HALO contexts) live until its backward
+                n1, n2 = self.norms[l]
+                n1.requires_grad_(True)
+                n2.requires_grad_(True)
+                xin = h.detach().requires_grad_(True)
+                with torch.enable_grad():
+                    y = self._block(xin, l)
+                saved.append((xin, y))
+                h = y.detach()
         # ---------------- backward (regathered one layer ahead)
         g = dy
         self.stale.zero_()
         self._fetch(L - 1, regather=True)
         for l in reversed(range(L)):
-            self._install(l)
+            if self.ac:
+                self._install(l)  # the recompute forward and the backward read the regathered codes
+            else:
+                # the contexts saved at the forward point at this layer's
+                # buffer, which the regather rewrote in place
+                torch.cuda.current_stream(self.device).wait_event(self.ready[self._slot(l)])
             if l > 0:
                 self._fetch(l - 1, regather=True)
-            self._zero_grads()
+            ex = self._exec(l)
+            ex.zero_grads()
             n1, n2 = self.norms[l]
-            n1.grad = n2.grad = None
-            n1.requires_grad_(True)
-            n2.requires_grad_(True)
-            xin = saved[l].detach().requires_grad_(True)
-            with torch.enable_grad():
-                y = self._block(xin, l)  # recompute on the same regathered codes
+            if self.ac:
+                n1.grad = n2.grad = None
+                n1.requires_grad_(True)
+                n2.requires_grad_(True)
+                xin = saved[l].detach().requires_grad_(True)
+                with torch.enable_grad():
+                    y = self._block(xin, l)  # recompute on the same regathered codes
+            else:
+                xin, y = saved[l]
             y.backward(g)
             g = xin.grad
             saved[l] = None
-            grads = self._grads()
+            grads = ex.grads()
             base = l * (len(WEIGHTS) + 2)
             for j, name in enumerate(WEIGHTS):
                 p = self.masters[l][name]
@@ -304,7 +329,7 @@ class HqFsdpLlama:
                 n.requires_grad_(False)
                 self.opt.update(base + len(WEIGHTS) + j, ng)
                 n.grad = None
-            self._zero_grads()
+            ex.zero_grads()
         if self.check_stale:
             torch.cuda.current_stream(self.device).wait_stream(self.comm)
             fsdp.check_stale_flag(self.stale, self.group)
@@ -318,7 +343,7 @@ class HqFsdpLlama:
         """6*b*m*n of the five projections per layer (the quantized GEMM work),
         plus the recompute forward's 2*b*m*n under activation checkpointing."""
         per = sum(o * i for o, i in self.d.shapes().values())
-        return 8.0 * tokens * per * self.d.layers
+        return (8.0 if self.ac else 6.0) * tokens * per * self.d.layers
 
     def close(self):
         torch.cuda.synchronize(self.device)
@@ -331,3 +356,31 @@ class _GradSink:
 
     def __init__(self):
         self.grad = None
+
+
+class _Executor:
+    """The five HALO projections of one Llama layer (qkv and o as
+    block.HaloLinear, gate / up / down as one HaloMLP) on placeholder weights;
+    gathered codes are installed per layer."""
+
+    def __init__(self, dummy, scheme):
+        from .mlp import HaloMLP
+        self.lin = {name: HaloLinear(dummy[name], scheme) for name in ("qkv", "o")}
+        self.mlp = HaloMLP(dummy["gate"], dummy["up"], dummy["down"], scheme)
+        self.owners = [_GradSink(), _GradSink(), _GradSink()]
+        self.mlp.owners = self.owners
+        self.layers_of = {"qkv": self.lin["qkv"].layer, "o": self.lin["o"].layer, "gate": self.mlp.gate,
+                          "up": self.mlp.up, "down": self.mlp.down}
+
+    def contexts(self):
+        return [self.lin["qkv"].sctx, self.lin["o"].sctx] + list(self.mlp.ctx)
+
+    def zero_grads(self):
+        for lin in self.lin.values():
+            lin.grad = None
+        for s in self.owners:
+            s.grad = None
+
+    def grads(self):
+        return {"qkv": self.lin["qkv"].grad, "o": self.lin["o"].grad, "gate": self.owners[0].grad,
+                "up": self.owners[1].grad, "down": self.owners[2].grad}

@@ -5,7 +5,8 @@ trainer.hpp:104-160) on the GPU.
   126-155) in IEEE double with the device's fp32 state storage: bit-exact
   over several steps, bf16 and fp32 masters, bf16 and fp32 gradients.
 * HqFsdpLlama (world 1, both data planes -- the library's C++ NCCL plane
-  halo_fsdp_* and torch.distributed: gathered codes installed per layer, prefetch on a
+  halo_fsdp_* and torch.distributed -- with and without activation
+  checkpointing: gathered codes installed per layer, prefetch on a
   side stream, activation checkpointing with one regather feeding the
   recompute and the backward, reduce-scatter, per-layer AdamW) against the
   direct composition -- a stack of block.LlamaBlock's with their own HALO
@@ -78,8 +79,8 @@ def test_adamw_matches_reference_formula(T, pdt, gdt):
 SMALL = dict(hidden=256, heads=2, kv_heads=1, inter=512, layers=2, seq=256)
 
 
-@pytest.mark.parametrize("plane", ["native", "torch"])
-def test_fsdp_step_matches_direct_stack(T, plane):
+@pytest.mark.parametrize("plane,ac", [("native", True), ("torch", True), ("native", False)])
+def test_fsdp_step_matches_direct_stack(T, plane, ac):
     from torch.nn.attention import SDPBackend, sdpa_kernel
 
     from paper_2501_02625_b200 import halo
@@ -87,7 +88,7 @@ def test_fsdp_step_matches_direct_stack(T, plane):
     d = T.LlamaDims(**SMALL)
     scheme = halo.halo2(halo.INT8, 256)
     cfg = T.AdamWConfig(lr=1e-3, warmup_steps=1)
-    model = T.HqFsdpLlama(d, scheme, seed=3, opt=cfg, data_plane=plane)
+    model = T.HqFsdpLlama(d, scheme, seed=3, opt=cfg, data_plane=plane, activation_checkpoint=ac)
     # the direct composition on copies of the same weights
     blocks = []
     for l in range(d.layers):
@@ -130,7 +131,7 @@ def test_fsdp_step_matches_direct_stack(T, plane):
     nw = len(T.WEIGHTS) * d.layers
     assert led.gather.count == 2 * nw * 2          # forward gathers + backward regathers, 2 steps
     assert led.backward_gathers == 2 * nw
-    assert led.backward_consumers == 2 * 2 * nw    # one regather, two consumers (AC)
+    assert led.backward_consumers == 2 * nw * (2 if ac else 1)  # with AC one regather feeds two consumers
     # a master changed after its forward gather (here: by the step's own
     # AdamW update) makes the regather's stale check trip
     model.masters[0]["o"].master.add_(1.0)

@@ -31,7 +31,9 @@ for w in $what; do
       echo "rc=$?" >> gpurun_out/bench_cfg5_l4.log ;;
     cfg5)
       timeout 1200 python bench.py --config cfg5 --steps 5 --warmup 3 > gpurun_out/bench_cfg5.log 2>&1
-      echo "rc=$?" >> gpurun_out/bench_cfg5.log ;;
+      echo "rc=$?" >> gpurun_out/bench_cfg5.log
+      timeout 1200 python bench.py --config cfg5 --ac --steps 5 --warmup 3 > gpurun_out/bench_cfg5_ac.log 2>&1
+      echo "rc=$?" >> gpurun_out/bench_cfg5_ac.log ;;
     prof_cfg5)
       timeout 600 python tools/prof_cfg5.py 4 > gpurun_out/prof_cfg5.log 2>&1 ;;
     glue)
