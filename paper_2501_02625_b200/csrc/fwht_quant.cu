@@ -420,6 +420,9 @@ void run_cols(const void* in, int in_dtype, int64_t b, int64_t rows_pad, int64_t
         cols_v3(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
                 codes_plain, err, scale_rot_out, scale_plain_out, st))
         return;
+    if (cols_lb(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
+                codes_plain, err, scale_rot_out, scale_plain_out, st, out, rows_out))
+        return;
     if (cols_big(mode, fmt, in_dtype, in, b, rows_pad, cols, B, amax_rot, amax_plain, sup_rot, sup_plain, codes_rot,
                  codes_plain, err, scale_rot_out, scale_plain_out, st, out, rows_out))
         return;

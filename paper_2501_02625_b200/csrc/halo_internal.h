@@ -120,6 +120,11 @@ bool rows_lb(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
 bool rows_big(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
               uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st);
 
+// K2 for 512 <= B <= 4096 along the token axis, one kernel per phase
+// (fwht_cols_lb.cu); false = shape not covered (the caller falls back)
+bool cols_lb(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
+             unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,
+             float* sro, float* spo, cudaStream_t st, float* xout, int64_t rows_out);
 // K2 for large blocks along the token axis (fwht_cols_big.cu): 512 <= B <= 16384
 bool cols_big(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t rows_pad, int64_t cols, int64_t B,
               unsigned* ar, unsigned* ap, const float* sr, const float* sp, uint8_t* cr, uint8_t* cp, unsigned* err,

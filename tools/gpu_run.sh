@@ -45,6 +45,17 @@ for w in $what; do
     sweep_right)
       timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_new.jsonl 2>&1
       HALO_K1_LB=0 timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_old.jsonl 2>&1 ;;
+    lb)
+      timeout 900 python -m pytest tests/test_gpu_cols_lb.py tests/test_gpu_kernels.py -k "left or large or transform" -x -q > gpurun_out/pytest_lb.log 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_lb.log
+      timeout 600 python tools/sweep_fwht.py left > gpurun_out/sweep_left_new.jsonl 2>&1
+      HALO_K2_LB=0 timeout 600 python tools/sweep_fwht.py left > gpurun_out/sweep_left_old.jsonl 2>&1 ;;
+    prof_lb)
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cols_lb -s 2 -c 2 \
+        -f -o gpurun_out/prof_lb python tools/bench_lb.py 8192 1024 1 > gpurun_out/prof_lb.log 2>&1
+      ncu -i gpurun_out/prof_lb.ncu-rep --page raw --csv > gpurun_out/prof_lb.raw.csv 2>/dev/null ;;
+    lbt)
+      for bl in 512 1024 2048 4096; do timeout 300 python tools/bench_lb.py 8192 $bl; done > gpurun_out/lbt.log 2>&1 ;;
     sweep)
       timeout 900 python tools/sweep_fwht.py > gpurun_out/sweep.jsonl 2>&1 ;;
     kern_v2)
