@@ -58,7 +58,9 @@ class HaloLinear:
     """One projection: weight [out, in] (bf16), a reusable SavedContext."""
 
     def __init__(self, w: torch.Tensor, scheme, bf16: bool = False):
-        self.w = w
+        # the bf16 reference arm trains the weight too (autograd's dW GEMM),
+        # so both arms do the same three GEMMs per projection
+        self.w = w.requires_grad_(True) if bf16 else w
         self.bf16 = bf16
         self.grad = None
         if not bf16:

@@ -241,6 +241,10 @@ def test_llama_block_runs_and_tracks_bf16(H, sch):
     assert rel(outs[0][0] - x.float(), outs[1][0] - x.float()) < 0.1  # block update (y - x)
     assert rel(outs[0][1], outs[1][1]) < 0.25
     assert all(l.grad is not None and torch.isfinite(l.grad).all() for l in qb.linears())
+    # weight gradients: the bf16 arm trains its weights too (same GEMM work)
+    for lq, lr in zip(qb.linears(), rb.linears()):
+        assert lr.w.grad is not None
+        assert rel(lq.grad.float(), lr.w.grad.float()) < 0.5
 
 
 @pytest.mark.parametrize("fmt", [0, 1])

@@ -35,6 +35,7 @@ def run(name, scheme, bf16, args):
         y.backward(dy)
         for l in blk.linears():
             l.grad = None
+            l.w.grad = None  # bf16 arm: autograd's dW
         return xi.grad
 
     for _ in range(3):

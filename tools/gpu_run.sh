@@ -56,6 +56,9 @@ for w in $what; do
       ncu -i gpurun_out/prof_lb.ncu-rep --page raw --csv > gpurun_out/prof_lb.raw.csv 2>/dev/null ;;
     lbt)
       for bl in 512 1024 2048 4096; do timeout 300 python tools/bench_lb.py 8192 $bl; done > gpurun_out/lbt.log 2>&1 ;;
+    prof_block)
+      timeout 600 python tools/prof_block.py int8 > gpurun_out/prof_block_int8.log 2>&1
+      timeout 600 python tools/prof_block.py bf16 > gpurun_out/prof_block_bf16.log 2>&1 ;;
     sweep)
       timeout 900 python tools/sweep_fwht.py > gpurun_out/sweep.jsonl 2>&1 ;;
     kern_v2)

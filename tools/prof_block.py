@@ -24,6 +24,7 @@ def step():
     y.backward(dy)
     for l in blk.linears():
         l.grad = None
+        l.w.grad = None  # bf16 arm: autograd's dW
 
 
 for _ in range(3):
