@@ -103,6 +103,37 @@ if "gemm_sweep" in what:
         timeit(lambda: halo.qmatmul(a, b, one, one, a_kmajor=bool(ak), b_kmajor=bool(bk), out=out), ops=2 * M * N * K,
                name=f"gemm[{M}x{N}x{K} a{'K' if ak else 'MN'} b{'K' if bk else 'MN'} {out}]")
         del a, b
+if "gemm_k" in what:  # per-tile overhead: fixed M x N, growing K
+    one = torch.ones(1, device=dev)
+    def cod(r, c):
+        return torch.randint(-127, 128, (r, c), dtype=torch.int8, device=dev, generator=g)
+    for K in (1024, 2048, 4096, 8192, 16384):
+        for (M, N, out) in [(8192, 14336, "bf16"), (8192, 14336, "f32")]:
+            a, b = cod(M, K), cod(N, K)
+            timeit(lambda: halo.qmatmul(a, b, one, one, out=out), ops=2 * M * N * K, name=f"gemm_k[{M}x{N}x{K} {out}]",
+                   tiles=(M // 256) * (N // 256))
+            del a, b
+if "gemm_edown" in what:  # the E GEMM of down_proj (prod^T: M = 14336, N = 8192 tokens, K = 4096)
+    one = torch.ones(1, device=dev)
+    def cod(r, c):
+        return torch.randint(-127, 128, (r, c), dtype=torch.int8, device=dev, generator=g)
+    M, N, K = 14336, 8192, 4096
+    a, b = cod(K, M), cod(N, K)
+    for hb, tr in ((None, False), (256, False), (None, True), (256, True)):
+        kw = {} if hb is None else {"had_block": hb}
+        timeit(lambda: halo.qmatmul(a, b, one, one, a_kmajor=False, b_kmajor=True, out="f32", transposed=tr, **kw),
+               ops=2 * M * N * K, name=f"gemm_edown[aMN bK f32 xf={hb} trans={tr}]")
+    a2 = cod(M, K)
+    timeit(lambda: halo.qmatmul(a2, b, one, one, out="f32", had_block=256, transposed=True), ops=2 * M * N * K,
+           name="gemm_edown[aK bK f32 xf=256 trans=True]")
+    del a, b, a2
+    for (M, N) in ((14336, 4096), (4096, 14336)):  # the G GEMMs (dW, right transform along N)
+        a, b = cod(8192, M), cod(8192, N)
+        for hb in (None, 256):
+            kw = {} if hb is None else {"had_block": hb}
+            timeit(lambda: halo.qmatmul(a, b, one, one, a_kmajor=False, b_kmajor=False, out="f32", **kw),
+                   ops=2 * M * N * 8192, name=f"gemm_G[{M}x{N}x8192 aMN bMN f32 xf={hb}]")
+        del a, b
 if "gemm_epi" in what:
     one = torch.ones(1, device=dev)
     def cod(r, c):
