@@ -377,6 +377,20 @@ HALO_API halo_status halo_rmsnorm_forward(const void* x, const float* gain, void
 HALO_API halo_status halo_rmsnorm_backward(const void* x, const void* dy, int32_t dy_dtype, const float* gain,
                                            const float* rstd, void* dx, float* dgain, int64_t rows, int64_t dim,
                                            int32_t mean, halo_stream_t stream);
+/* The pre-norm residual pattern of the Llama block (model.hpp:159-209:
+ * h = x + r; y = rmsnorm(h)) in one pass: h = RN_bf16(x + r) (bf16, as a
+ * bf16 tensor add rounds) is written to h and normalised into y (bf16);
+ * mean = 1 (the Llama form) only. */
+HALO_API halo_status halo_add_rmsnorm_forward(const void* x, const void* r, const float* gain, void* h, void* y,
+                                              float* rstd, int64_t rows, int64_t dim, double eps,
+                                              halo_stream_t stream);
+/* Its backward: dx = RN_bf16(RN_bf16(rmsnorm_backward(h, dy)) + dres) --
+ * the residual-stream gradient dres (bf16) accumulated the way autograd
+ * sums two bf16 gradients -- and dgain as halo_rmsnorm_backward; the result
+ * is the gradient of both x and r.  mean = 1 only. */
+HALO_API halo_status halo_rmsnorm_backward_res(const void* h, const void* dy, int32_t dy_dtype, const float* gain,
+                                               const float* rstd, const void* dres, void* dx, float* dgain,
+                                               int64_t rows, int64_t dim, halo_stream_t stream);
 /* Rotary embedding over fused qkv rows [rows x heads*head_dim] (bf16): the
  * first rot_heads heads (q and k) rotated by (cos, sin) pairs of
  * cos_sin[(row % seq) * head_dim/2 + i] (fp32 interleaved), the rest (v)

@@ -167,8 +167,11 @@ def lib():
     L.halo_adamw_step.restype = C.c_int
     L.halo_rmsnorm_forward.argtypes = [_vp, _vp, _vp, _i32, _vp, _i64, _i64, _i32, C.c_double, _vp]
     L.halo_rmsnorm_backward.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _vp]
+    L.halo_add_rmsnorm_forward.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, C.c_double, _vp]
+    L.halo_rmsnorm_backward_res.argtypes = [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]
     L.halo_rope_qkv.argtypes = [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]
-    for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv"):
+    for fn in ("halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv", "halo_add_rmsnorm_forward",
+               "halo_rmsnorm_backward_res"):
         getattr(L, fn).restype = C.c_int
     L.halo_rotate_quantize_mx.argtypes = [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp]
     L.halo_rotate_quantize_mx.restype = C.c_int
@@ -249,7 +252,8 @@ EXPORTS = (
     "halo_profile_read", "halo_linear_set_qweight_sharded", "halo_peer_alloc", "halo_peer_free",
     "halo_ipc_handle", "halo_ipc_open", "halo_ipc_close", "halo_peer_sync", "halo_linear_set_grad_scatter",
     "halo_reduce_scatter_shard", "halo_rotate_quantize_amax", "halo_swiglu_forward_absmax",
-    "halo_adamw_step", "halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
+    "halo_adamw_step", "halo_rmsnorm_forward", "halo_rmsnorm_backward", "halo_rope_qkv",
+    "halo_add_rmsnorm_forward", "halo_rmsnorm_backward_res", "halo_quantized_tensor_write", "halo_quantized_tensor_info", "halo_quantized_tensor_read",
     "halo_fsdp_get_unique_id", "halo_fsdp_create", "halo_fsdp_destroy", "halo_fsdp_world",
     "halo_fsdp_quantized_all_gather", "halo_fsdp_backward_regather", "halo_fsdp_reduce_scatter",
     "halo_fsdp_all_reduce_mean", "halo_fp6_pack", "halo_fp6_unpack",

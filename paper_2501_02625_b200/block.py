@@ -111,6 +111,47 @@ def _rmsnorm(x, w, eps=1e-5):
     return _RMSNormFn.apply(x, w, eps)
 
 
+class _AddRMSNormFn(torch.autograd.Function):
+    """h = x + r; m = rmsnorm(h) in one kernel (halo_add_rmsnorm_forward),
+    and the backward's residual-gradient sum dh + rmsnorm'(dm) fused into the
+    norm backward's store (halo_rmsnorm_backward_res).  Bit-identical with
+    the unfused torch add + _RMSNormFn: the same bf16 roundings."""
+
+    @staticmethod
+    def forward(ctx, x, r, w, eps):
+        from ._lib import check, lib
+        x, r = x.contiguous(), r.contiguous()
+        rows, dim = x.shape
+        h = torch.empty_like(x)
+        m = torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        check(lib().halo_add_rmsnorm_forward(halo._ptr(x), halo._ptr(r), halo._ptr(w), halo._ptr(h), halo._ptr(m),
+                                             halo._ptr(rstd), rows, dim, eps, halo._stream()))
+        ctx.save_for_backward(h, w, rstd)
+        return h, m
+
+    @staticmethod
+    def backward(ctx, dh, dm):
+        from ._lib import check, lib
+        h, w, rstd = ctx.saved_tensors
+        rows, dim = h.shape
+        if dm is None:
+            return dh, dh, None, None
+        dm = dm.contiguous()
+        dx = torch.empty_like(h)
+        dw = torch.empty(dim, dtype=torch.float32, device=h.device)
+        if dh is None:
+            check(lib().halo_rmsnorm_backward(halo._ptr(h), halo._ptr(dm), halo._dt(dm), halo._ptr(w),
+                                              halo._ptr(rstd), halo._ptr(dx), halo._ptr(dw), rows, dim, 1,
+                                              halo._stream()))
+        else:
+            dh = dh.contiguous()
+            check(lib().halo_rmsnorm_backward_res(halo._ptr(h), halo._ptr(dm), halo._dt(dm), halo._ptr(w),
+                                                  halo._ptr(rstd), halo._ptr(dh), halo._ptr(dx), halo._ptr(dw),
+                                                  rows, dim, halo._stream()))
+        return dx, dx, dw, None
+
+
 class _RopeQKVFn(torch.autograd.Function):
     """RoPE on the q and k heads of the fused qkv output (halo_rope_qkv), one
     pass forward and backward."""
@@ -154,13 +195,15 @@ def attention_block(x, qkv_fn, o_fn, mlp_fn, n1, n2, cs, seq, heads, kv_heads):
     a = _rmsnorm(x, n1)
     qkv = _RopeQKVFn.apply(qkv_fn(a), cs, seq, heads + kv_heads, heads + 2 * kv_heads, hd)
     nq, nk = heads * hd, kv_heads * hd
-    q = qkv[:, :nq].view(B, seq, heads, hd).transpose(1, 2)
-    k = qkv[:, nq:nq + nk].view(B, seq, kv_heads, hd).transpose(1, 2)
-    v = qkv[:, nq + nk:].view(B, seq, kv_heads, hd).transpose(1, 2)
+    # one split (its backward is a single cat into dqkv; three slices would
+    # each zero-fill a full-size gradient and then sum them)
+    qs, ks, vs = qkv.split([nq, nk, nk], dim=1)
+    q = qs.view(B, seq, heads, hd).transpose(1, 2)
+    k = ks.view(B, seq, kv_heads, hd).transpose(1, 2)
+    v = vs.view(B, seq, kv_heads, hd).transpose(1, 2)
     att = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
     att = att.transpose(1, 2).reshape(T, H)
-    h = x + o_fn(att)
-    m = _rmsnorm(h, n2)
+    h, m = _AddRMSNormFn.apply(x, o_fn(att), n2, 1e-5)  # h = x + O(att); m = rmsnorm(h)
     return h + mlp_fn(m)
 
 

@@ -1817,6 +1817,34 @@ extern "C" halo_status halo_rmsnorm_backward(const void* x, const void* dy, int3
     return cuda_check("rmsnorm_backward");
 }
 
+extern "C" halo_status halo_add_rmsnorm_forward(const void* x, const void* r, const float* gain, void* h, void* y,
+                                                float* rstd, int64_t rows, int64_t dim, double eps,
+                                                halo_stream_t stream) {
+    if (!x || !r || !gain || !h || !y) return fail(HALO_ERR_INVALID_ARGUMENT, "add_rmsnorm: bad arguments");
+    if (rows < 0 || dim <= 0 || dim % 8 || !(eps >= 0.0))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "add_rmsnorm: dim must be a positive multiple of 8, eps >= 0");
+    if (rows == 0) return HALO_OK;
+    ProfScope ps(PC_GLUE, (double)rows * dim * 8, (cudaStream_t)stream);
+    if (!run_rmsnorm_fwd(x, gain, y, HALO_DTYPE_BF16, rstd, rows, (int)dim, true, eps, (cudaStream_t)stream, r, h))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "add_rmsnorm: unsupported arguments");
+    return cuda_check("add_rmsnorm_forward");
+}
+
+extern "C" halo_status halo_rmsnorm_backward_res(const void* h, const void* dy, int32_t dy_dtype, const float* gain,
+                                                 const float* rstd, const void* dres, void* dx, float* dgain,
+                                                 int64_t rows, int64_t dim, halo_stream_t stream) {
+    if (!h || !dy || !gain || !rstd || !dres || !dx || !dgain || !valid_dtype(dy_dtype))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "rmsnorm_backward_res: bad arguments");
+    if (rows < 0 || dim <= 0 || dim % 8) return fail(HALO_ERR_INVALID_ARGUMENT, "rmsnorm_backward_res: dim must be a positive multiple of 8");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (rows == 0) return cudaMemsetAsync(dgain, 0, sizeof(float) * dim, st) == cudaSuccess ? HALO_OK : cuda_check("rmsnorm_backward_res");
+    Buffer& sc = t_norm_scratch[st];
+    if (sc.ensure((size_t)rmsnorm_bwd_scratch(rows, (int)dim) * sizeof(float)) != HALO_OK) return HALO_ERR_CUDA;
+    ProfScope ps(PC_GLUE, (double)rows * dim * (2 + dt_bytes(dy_dtype) + 4), st);
+    run_rmsnorm_bwd(h, dy, dy_dtype, gain, rstd, dx, dgain, sc.as<float>(), rows, (int)dim, true, st, dres);
+    return cuda_check("rmsnorm_backward_res");
+}
+
 extern "C" halo_status halo_rope_qkv(const void* in, void* out, const float* cos_sin, int64_t rows, int32_t seq,
                                      int32_t rot_heads, int32_t heads, int32_t head_dim, int32_t backward,
                                      halo_stream_t stream) {

@@ -198,10 +198,13 @@ void run_rank_mean(const float* recv, int world, int64_t n, void* out, int dtype
 void run_fp6_pack(const uint8_t* codes, uint8_t* packed, int64_t n, cudaStream_t st);
 void run_fp6_unpack(const uint8_t* packed, uint8_t* codes, int64_t n, cudaStream_t st);
 // Llama block glue (llama_glue.cu)
+// res / hout: h = RN_bf16(x + res) is written to hout and normalised (Llama form)
 bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, float* rstd, int64_t rows, int dim,
-                     bool mean, double eps, cudaStream_t st);
+                     bool mean, double eps, cudaStream_t st, const void* res = nullptr, void* hout = nullptr);
+// dres: dx = RN_bf16(RN_bf16(dx_norm) + dres) (Llama form)
 bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* gain, const float* rstd, void* dx,
-                     float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st);
+                     float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st,
+                     const void* dres = nullptr);
 int64_t rmsnorm_bwd_scratch(int64_t rows, int dim);
 bool run_rope(const void* in, void* out, const float* cs, int64_t rows, int seq, int nrot, int nall, int hd,
               bool backward, cudaStream_t st);

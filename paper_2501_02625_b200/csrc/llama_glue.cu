@@ -36,19 +36,32 @@ constexpr int NORM_WARPS = 8;
 // one warp per row; a lane owns 8-element groups g = lane, lane + 32, ...
 // EXACT (the reference form): y = float(double(x) * r * double(g)) as
 // rmsnorm.hpp:38-42; otherwise (Llama) the fp32 product (x * r) * g.
-template <typename OutT, bool EXACT>
+// ADD: the input row is h = RN_bf16(x + res) (torch's bf16 add), written to
+// hout and normalised -- the residual add fused into the norm's first pass.
+template <typename OutT, bool EXACT, bool ADD = false>
 __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bfloat16* __restrict__ x,
                                                                   const float* __restrict__ gain, OutT* __restrict__ y,
                                                                   float* __restrict__ rstd, int64_t rows, int dim,
-                                                                  double div, double eps) {
+                                                                  double div, double eps,
+                                                                  const __nv_bfloat16* __restrict__ res = nullptr,
+                                                                  __nv_bfloat16* __restrict__ hout = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * NORM_WARPS + (threadIdx.x >> 5);
     if (row >= rows) return;
-    const __nv_bfloat16* xr = x + row * dim;
+    const __nv_bfloat16* xr = (ADD ? hout : x) + row * dim;  // pass 2 reads h back (this thread wrote it)
     double s = 0.0;
     for (int c = lane * 8; c < dim; c += 256) {
         float v[8];
-        load8(xr + c, v);
+        if constexpr (ADD) {
+            float a[8], b[8];
+            load8(x + row * dim + c, a);
+            load8(res + row * dim + c, b);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(a[j] + b[j]));
+            store8(hout + row * dim + c, v);
+        } else {
+            load8(xr + c, v);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) s += (double)v[j] * (double)v[j];
     }
@@ -79,16 +92,22 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bflo
 // (double) and r -> shared memory.  Phase 2 (column-parallel, coalesced 16 B
 // per thread and row): dx for every (row, column) and the gain-gradient
 // partial sum over the CTA's rows in a fixed order (deterministic), written
-// to part[blockIdx.x].  The second read of x / dy hits L2.
-constexpr int BWD_ROWS = 32;
-template <typename DyT, bool EXACT>
+// to part[blockIdx.x].  The second read of x / dy hits L2.  Phase 2 walks
+// its rows UNROLL at a time with every load issued before the math, so a
+// thread keeps 2 * UNROLL 16-byte requests in flight.
+constexpr int BWD_ROWS = 16;
+constexpr int BWD_UNROLL = 4;
+// RES: dx = RN_bf16(RN_bf16(dx_norm) + dres) -- the autograd engine's bf16
+// accumulation of the residual-stream gradient, fused into the store.
+template <typename DyT, bool EXACT, bool RES = false>
 __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bfloat16* __restrict__ x,
                                                                   const DyT* __restrict__ dy,
                                                                   const float* __restrict__ gain,
                                                                   const float* __restrict__ rstd,
                                                                   __nv_bfloat16* __restrict__ dx,
                                                                   float* __restrict__ part, int64_t rows, int dim,
-                                                                  double div) {
+                                                                  double div,
+                                                                  const __nv_bfloat16* __restrict__ dres = nullptr) {
     __shared__ double kr[BWD_ROWS];
     __shared__ double rr[BWD_ROWS];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -127,11 +146,10 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bflo
 #pragma unroll
             for (int j = 0; j < 8; ++j) accd[j] = 0.0;
         }
-        for (int i = 0; i < nr; ++i) {
+        // rows in order (the gain-gradient partial sums stay deterministic)
+        auto one_row = [&](int i, const float (&v)[8], const float (&d)[8], const float (&e)[8]) {
             const int64_t row = row0 + i;
-            float v[8], d[8], o[8];
-            load8(x + row * dim + c, v);
-            load8(dy + row * dim + c, d);
+            float o[8];
             const double r = rr[i], k = kr[i];
             const float rf = (float)r, kf = (float)k;
 #pragma unroll
@@ -143,8 +161,34 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bflo
                     o[j] = rf * g[j] * d[j] - kf * v[j];
                     acc[j] += d[j] * v[j] * rf;
                 }
+                if constexpr (RES) o[j] = __bfloat162float(__float2bfloat16_rn(o[j])) + e[j];
             }
             store8(dx + row * dim + c, o);
+        };
+        int i = 0;
+        for (; i + BWD_UNROLL <= nr; i += BWD_UNROLL) {
+            float v[BWD_UNROLL][8], d[BWD_UNROLL][8], e[BWD_UNROLL][RES ? 8 : 1];
+#pragma unroll
+            for (int u = 0; u < BWD_UNROLL; ++u) {
+                load8(x + (row0 + i + u) * dim + c, v[u]);
+                load8(dy + (row0 + i + u) * dim + c, d[u]);
+                if constexpr (RES) load8(dres + (row0 + i + u) * dim + c, e[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < BWD_UNROLL; ++u) {
+                float e8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if constexpr (RES)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) e8[j] = e[u][j];
+                one_row(i + u, v[u], d[u], e8);
+            }
+        }
+        for (; i < nr; ++i) {
+            float v[8], d[8], e8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            load8(x + (row0 + i) * dim + c, v);
+            load8(dy + (row0 + i) * dim + c, d);
+            if constexpr (RES) load8(dres + (row0 + i) * dim + c, e8);
+            one_row(i, v, d, e8);
         }
         if constexpr (EXACT) {
 #pragma unroll
@@ -205,18 +249,23 @@ __global__ void __launch_bounds__(256) k_rope(const __nv_bfloat16* __restrict__ 
 }  // namespace
 
 bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, float* rstd, int64_t rows, int dim,
-                     bool mean, double eps, cudaStream_t st) {
-    if (dim % 8 || dim <= 0) return false;
+                     bool mean, double eps, cudaStream_t st, const void* res, void* hout) {
+    if (dim % 8 || dim <= 0 || (!res) != (!hout)) return false;
     const unsigned grid = (unsigned)((rows + NORM_WARPS - 1) / NORM_WARPS);
     const double div = mean ? (double)dim : 1.0;
     auto xp = static_cast<const __nv_bfloat16*>(x);
+    auto rp = static_cast<const __nv_bfloat16*>(res);
+    auto hp = static_cast<__nv_bfloat16*>(hout);
     // the reference form (x/||x||, eps 0) evaluates y in double like rmsnorm.hpp
     const bool exact = !mean;
-#define HALO_NF(T, E) k_rmsnorm_fwd<T, E><<<grid, 32 * NORM_WARPS, 0, st>>>(xp, gain, static_cast<T*>(y), rstd, rows, dim, div, eps)
-    if (y_dtype == DT_BF16) {
-        if (exact) HALO_NF(__nv_bfloat16, true); else HALO_NF(__nv_bfloat16, false);
+#define HALO_NF(T, E, A) k_rmsnorm_fwd<T, E, A><<<grid, 32 * NORM_WARPS, 0, st>>>(xp, gain, static_cast<T*>(y), rstd, rows, dim, div, eps, rp, hp)
+    if (res) {
+        if (y_dtype != DT_BF16 || exact) return false;  // the Llama block form only
+        HALO_NF(__nv_bfloat16, false, true);
+    } else if (y_dtype == DT_BF16) {
+        if (exact) HALO_NF(__nv_bfloat16, true, false); else HALO_NF(__nv_bfloat16, false, false);
     } else {
-        if (exact) HALO_NF(float, true); else HALO_NF(float, false);
+        if (exact) HALO_NF(float, true, false); else HALO_NF(float, false, false);
     }
 #undef HALO_NF
     return true;
@@ -225,18 +274,22 @@ bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, flo
 int64_t rmsnorm_bwd_scratch(int64_t rows, int dim) { return (rows + BWD_ROWS - 1) / BWD_ROWS * (int64_t)dim; }
 
 bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* gain, const float* rstd, void* dx,
-                     float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st) {
+                     float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st, const void* dres) {
     if (dim % 8 || dim <= 0) return false;
     const unsigned grid = (unsigned)((rows + BWD_ROWS - 1) / BWD_ROWS);
     const double div = mean ? (double)dim : 1.0;
     auto xp = static_cast<const __nv_bfloat16*>(x);
     auto dxp = static_cast<__nv_bfloat16*>(dx);
+    auto rp = static_cast<const __nv_bfloat16*>(dres);
     const bool exact = !mean;
-#define HALO_NB(T, E) k_rmsnorm_bwd<T, E><<<grid, 32 * NORM_WARPS, 0, st>>>(xp, static_cast<const T*>(dy), gain, rstd, dxp, scratch, rows, dim, div)
-    if (dy_dtype == DT_BF16) {
-        if (exact) HALO_NB(__nv_bfloat16, true); else HALO_NB(__nv_bfloat16, false);
+#define HALO_NB(T, E, R) k_rmsnorm_bwd<T, E, R><<<grid, 32 * NORM_WARPS, 0, st>>>(xp, static_cast<const T*>(dy), gain, rstd, dxp, scratch, rows, dim, div, rp)
+    if (dres) {
+        if (exact) return false;  // the Llama block form only
+        if (dy_dtype == DT_BF16) HALO_NB(__nv_bfloat16, false, true); else HALO_NB(float, false, true);
+    } else if (dy_dtype == DT_BF16) {
+        if (exact) HALO_NB(__nv_bfloat16, true, false); else HALO_NB(__nv_bfloat16, false, false);
     } else {
-        if (exact) HALO_NB(float, true); else HALO_NB(float, false);
+        if (exact) HALO_NB(float, true, false); else HALO_NB(float, false, false);
     }
 #undef HALO_NB
     k_sum_rows<<<(dim + 255) / 256, 256, 0, st>>>(scratch, (int)grid, dim, dgain);

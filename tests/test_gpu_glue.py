@@ -123,3 +123,33 @@ def test_block_on_fused_glue(L):
     y.backward(torch.randn_like(y) * 1e-2)
     assert bool(torch.isfinite(y.float()).all()) and bool(torch.isfinite(x.grad.float()).all())
     assert blk.n1.grad is not None and bool(torch.isfinite(blk.n1.grad).all())
+
+
+@pytest.mark.parametrize("rows,dim", [(300, 512), (1024, 4096)])
+def test_add_rmsnorm_matches_unfused(rows, dim):
+    """halo_add_rmsnorm_forward / halo_rmsnorm_backward_res (block.py
+    _AddRMSNormFn) == torch's bf16 residual add + _RMSNormFn, bit for bit:
+    h, the normed output, both input gradients and the gain gradient."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_02625_b200.block import _AddRMSNormFn, _RMSNormFn
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    bf = torch.bfloat16
+    x = torch.randn(rows, dim, generator=g, device="cuda").to(bf)
+    r = (torch.randn(rows, dim, generator=g, device="cuda") * 0.3).to(bf)
+    w = torch.rand(dim, generator=g, device="cuda") + 0.5
+    ch = (torch.randn(rows, dim, generator=g, device="cuda") * 1e-2).to(bf)
+    cm = (torch.randn(rows, dim, generator=g, device="cuda") * 1e-2).to(bf)
+    outs = []
+    for fused in (True, False):
+        xi, ri = x.clone().requires_grad_(True), r.clone().requires_grad_(True)
+        wi = w.clone().requires_grad_(True)
+        if fused:
+            h, m = _AddRMSNormFn.apply(xi, ri, wi, 1e-5)
+        else:
+            h = xi + ri
+            m = _RMSNormFn.apply(h, wi, 1e-5)
+        ((h * ch).sum() + (m * cm).sum()).backward()
+        outs.append((h.detach(), m.detach(), xi.grad, ri.grad, wi.grad))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
