@@ -15,6 +15,8 @@ same block on torch.nn.functional.linear (cuBLAS) for the speed-up baseline.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.nn.functional as F
 
@@ -185,6 +187,11 @@ def rope_table(seq, hd, device, theta=500000.0):
     return torch.stack((ang.cos(), ang.sin()), -1).float().contiguous()
 
 
+# HALO_BLOCK_UNFUSED_GLUE=1: the unfused residual add / RMSNorm and q/k/v
+# slices (A/B measurements; numerically identical)
+_UNFUSED_GLUE = os.environ.get("HALO_BLOCK_UNFUSED_GLUE", "0") == "1"
+
+
 def attention_block(x, qkv_fn, o_fn, mlp_fn, n1, n2, cs, seq, heads, kv_heads):
     """The Llama block on given projections (shared by LlamaBlock and the
     HQ-FSDP stack, train.HqFsdpLlama):
@@ -197,13 +204,20 @@ def attention_block(x, qkv_fn, o_fn, mlp_fn, n1, n2, cs, seq, heads, kv_heads):
     nq, nk = heads * hd, kv_heads * hd
     # one split (its backward is a single cat into dqkv; three slices would
     # each zero-fill a full-size gradient and then sum them)
-    qs, ks, vs = qkv.split([nq, nk, nk], dim=1)
+    if _UNFUSED_GLUE:  # A/B reference: the former slices
+        qs, ks, vs = qkv[:, :nq], qkv[:, nq:nq + nk], qkv[:, nq + nk:]
+    else:
+        qs, ks, vs = qkv.split([nq, nk, nk], dim=1)
     q = qs.view(B, seq, heads, hd).transpose(1, 2)
     k = ks.view(B, seq, kv_heads, hd).transpose(1, 2)
     v = vs.view(B, seq, kv_heads, hd).transpose(1, 2)
     att = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
     att = att.transpose(1, 2).reshape(T, H)
-    h, m = _AddRMSNormFn.apply(x, o_fn(att), n2, 1e-5)  # h = x + O(att); m = rmsnorm(h)
+    if _UNFUSED_GLUE:
+        h = x + o_fn(att)
+        m = _rmsnorm(h, n2)
+    else:
+        h, m = _AddRMSNormFn.apply(x, o_fn(att), n2, 1e-5)  # h = x + O(att); m = rmsnorm(h)
     return h + mlp_fn(m)
 
 
