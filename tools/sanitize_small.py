@@ -97,5 +97,16 @@ f = FsdpHaloMLP(wg_, wg_.clone(), wd_, halo.halo2(halo.INT8, 256), check_stale=T
 f.forward(torch.randn(256, 256, device=dev).to(bf))
 f.backward(torch.randn(256, 256, device=dev).to(bf) * 1e-3)
 f.close()
+# large-block left transform (fwht_cols_lb.cu): bf16 / fp32, padded token block, transform-only
+for B in (512, 4096):
+    el = (torch.randn(B - 37, 16384 // B * 2 if B < 4096 else 16, device=dev) * 1e-3)
+    halo.left_rotate_quantize(el.to(bf), B)
+    halo.left_rotate_quantize(el, B)
+    halo.transform_left(torch.randn(B, max(8, 16384 // B), device=dev), B)
+# fused residual add + RMSNorm (block.py _AddRMSNormFn)
+xa = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
+ra = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
+ha, ma = block._AddRMSNormFn.apply(xa, ra, torch.ones(512, device=dev, requires_grad=True), 1e-5)
+((ha * 0.5).sum() + ma.sum()).backward()
 torch.cuda.synchronize()
 print("sanitize workload (round-2 kernels) done")
