@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhalo_b200.so")
+# HALO_B200_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("HALO_B200_LIB") or os.path.join(HERE, "libhalo_b200.so")
 
 HALO_OK = 0
 HALO_ERR_INVALID_ARGUMENT = 1
