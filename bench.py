@@ -13,11 +13,15 @@ quantized GEMMs per step / step time (TOPS).
 
 N > 1 (torchrun, one rank per GPU): HQ-FSDP (hqfsdp.hpp) — every rank owns a
 row shard of each weight and runs the block on its own 8192 tokens (weak
-scaling).  Default (peer): each rank quantizes its rows of (WH)_Q under the
-shared scale into a CUDA-IPC buffer and the GEMMs read the peers' rows in
-place over NVLink (no all-gather; absmax exchange + barriers by a device
-mailbox kernel); dW is reduce-scattered over NCCL.  --fsdp-gather: the
-NCCL all-gather / regather variant.  All inside the timed step.
+scaling).  Default: the C++ NCCL data plane (csrc/hqfsdp_nccl.cpp) -- absmax
+all-reduce, each rank quantizes its rows of (WH)_Q under the shared scale,
+INT8 all-gather (prefetched on a side stream), regather in backward under
+the saved scale with a device stale check, dW reduce-scatter.
+--fsdp-peer: the CUDA-IPC variant whose GEMMs read the peers' rows in place
+(or from a staged local copy, --peer-staged) and whose G GEMM scatters dW
+rows to their owners.  All inside the timed step.
+`--config cfg5`: the 32-layer HQ-FSDP Llama-3-8B fine-tuning step (tokens/s);
+`--config cfg1`: one HALO-2 layer 2048 x 4096 -> 4096.
 `--impl reference` times the reference's own CPU implementation (the
 unmodified headers compiled into oracle/_ref) on a bounded sample.
 """
