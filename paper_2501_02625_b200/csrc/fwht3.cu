@@ -288,10 +288,120 @@ struct RowsCore {
         }
     }
 
+    // B = 512 / 1024 (LB 9, 10): a segment is NP = 16 / 32 lanes (two / one
+    // per warp chunk); one exchange through the warp's 4 KB gives lane pp
+    // the CW = 2 / 1 elements at offset CW*pp of every 32-block of its
+    // segment (slot pp*NP + (q ^ pp): conflict-free both ways), then the
+    // block-index bits run as FADD2 pairs -- one exchange where the generic
+    // large-block kernel needs a round per 3 bits.
+    __device__ __forceinline__ void finish_wide(float2 (&v)[16], int64_t base, int64_t n, float4* S,
+                                                uint8_t* __restrict__ codes, OutT* __restrict__ out) {
+        constexpr int NP = 1 << (LB - 5);
+        const int l = threadIdx.x & 31;
+        const int kk = l / NP, pp = l % NP;
+        const int64_t sb = base + (int64_t)kk * (NP * 32);  // segment base
+        float2 U[16];  // LB 9: U[b] = elements 32b + 2pp + {0,1}; LB 10: U[j] = (32j + pp, 32(j+16) + pp)
+        if constexpr (LB == 9) {
+            float2* T = reinterpret_cast<float2*>(S) + kk * 256;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) T[pp * 16 + (q ^ pp)] = v[q];
+            __syncwarp();
+#pragma unroll
+            for (int b = 0; b < 16; ++b) U[b] = T[b * 16 + (pp ^ b)];
+            __syncwarp();
+        } else {
+            float* T = reinterpret_cast<float*>(S);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                T[pp * 32 + ((2 * q) ^ pp)] = v[q].x;
+                T[pp * 32 + ((2 * q + 1) ^ pp)] = v[q].y;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) U[j] = make_float2(T[j * 32 + (pp ^ j)], T[(j + 16) * 32 + (pp ^ (j + 16))]);
+            __syncwarp();
+        }
+        // phase 2: block-index bit t <-> stage len = 32 << t
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int h = 1 << t;
+            const bool last = v3_abs<MODE>() && LB == 9 && t == 3;
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+                if ((b & h) == 0) {
+                    if (last) amax = max3nan(amax, fabsf(U[b].x) + fabsf(U[b + h].x), fabsf(U[b].y) + fabsf(U[b + h].y));
+                    else bfly2(U[b], U[b + h]);
+                }
+        }
+        if constexpr (LB == 10) {  // len = 512: the two halves of each U
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if constexpr (v3_abs<MODE>()) {
+                    amax = max3nan(amax, fabsf(U[j].x) + fabsf(U[j].y), 0.f);
+                } else {
+                    const float a = U[j].x, c = U[j].y;
+                    U[j] = make_float2(a + c, a - c);
+                }
+            }
+        }
+        // element offset (within the segment) of value w (0/1) of U[i]
+        auto off = [&](int i, int w) -> int64_t { return LB == 9 ? 32 * i + 2 * pp + w : 32 * (i + 16 * w) + pp; };
+        if constexpr (v3_q<MODE>()) {
+            float dmax = 0.f;
+            uint32_t wd[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) wd[g] = quant4(U[2 * g], U[2 * g + 1], dmax);
+            if (__any_sync(0xffffffffu, !(dmax < thr))) {
+                if (!(dmax < thr)) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        if (group_slow<FMT, SUP>(U[2 * g], U[2 * g + 1], s, inv, thr))
+                            wd[g] = exact4<FMT>(U[2 * g], U[2 * g + 1], s, inv);
+                }
+            }
+            if (sb < n) {
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const uint32_t w = wd[g];
+                    if constexpr (LB == 9) {  // bytes 0,1 -> block 2g; 2,3 -> block 2g+1
+                        *reinterpret_cast<uint16_t*>(codes + sb + off(2 * g, 0)) = (uint16_t)(w & 0xFFFFu);
+                        *reinterpret_cast<uint16_t*>(codes + sb + off(2 * g + 1, 0)) = (uint16_t)(w >> 16);
+                    } else {  // bytes: U[2g].x, U[2g].y, U[2g+1].x, U[2g+1].y
+                        codes[sb + off(2 * g, 0)] = (uint8_t)(w & 0xFFu);
+                        codes[sb + off(2 * g, 1)] = (uint8_t)((w >> 8) & 0xFFu);
+                        codes[sb + off(2 * g + 1, 0)] = (uint8_t)((w >> 16) & 0xFFu);
+                        codes[sb + off(2 * g + 1, 1)] = (uint8_t)(w >> 24);
+                    }
+                }
+            }
+        } else if constexpr (MODE == V3_XFORM) {
+            if (sb < n) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float2 a = mul2(U[i], norm2);
+                    if constexpr (LB == 9) {
+                        if constexpr (sizeof(OutT) == 4) *reinterpret_cast<float2*>(out + sb + off(i, 0)) = a;
+                        else *reinterpret_cast<uint32_t*>(out + sb + off(i, 0)) = pack_bf16x2(a.x, a.y);
+                    } else {
+                        if constexpr (sizeof(OutT) == 4) {
+                            out[sb + off(i, 0)] = a.x;
+                            out[sb + off(i, 1)] = a.y;
+                        } else {
+                            out[sb + off(i, 0)] = __float2bfloat16_rn(a.x);
+                            out[sb + off(i, 1)] = __float2bfloat16_rn(a.y);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
     // everything after phase 1 (all 32 lanes of the warp call this together)
     __device__ __forceinline__ void finish(float2 (&v)[16], int64_t base, int64_t n, int k, int p, float4* S,
                                            uint8_t* __restrict__ codes, OutT* __restrict__ out) {
-        if constexpr (!X2) {
+        if constexpr (LB == 9 || LB == 10) {
+            finish_wide(v, base, n, S, codes, out);
+        } else if constexpr (!X2) {
             const int64_t e0 = base + k * 256 + p * 32;
             if constexpr (v3_q<MODE>()) {
                 float dmax = 0.f;
@@ -823,6 +933,15 @@ unsigned v3_grid(K kern, int64_t n) {
 
 }  // namespace
 
+// HALO_K1_WIDE=0: B = 512 / 1024 through the generic large-block kernel (A/B)
+bool wide_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("HALO_K1_WIDE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int k1_version() {
     static const int ver = [] {
         const char* e = getenv("HALO_K1_VERSION");
@@ -1017,10 +1136,12 @@ bool rows_lb(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
     return true;
 }
 
-// B = 2^lb with lb in [0, 8]; n a multiple of 16 (and of B).
+// B = 2^lb with lb in [0, 10]; n a multiple of 16 (and of B).  B = 512 / 1024
+// (RowsCore::finish_wide) only for whole 1024-element chunks.
 bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
              uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
-    if (n % 16 || B < 1 || B > 256 || (B & (B - 1))) return false;
+    if (n % 16 || B < 1 || B > 1024 || (B & (B - 1))) return false;
+    if (B > 256 && (n % 1024 || !wide_enabled())) return false;
     if (mode == V3_XFORM && in_dtype != DT_F32) return false;
     int lb = 0;
     while ((int64_t(1) << lb) < B) ++lb;
@@ -1033,7 +1154,9 @@ bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
     case 5: dispatch_v3<5>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
     case 6: dispatch_v3<6>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
     case 7: dispatch_v3<7>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
-    default: dispatch_v3<8>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 8: dispatch_v3<8>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    case 9: dispatch_v3<9>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
+    default: dispatch_v3<10>(mode, fmt, in_dtype, in, n, amax, sup, codes, out, out_dtype, err, sout, st); break;
     }
     return true;
 }

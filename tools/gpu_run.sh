@@ -59,6 +59,11 @@ for w in $what; do
     prof_block)
       timeout 600 python tools/prof_block.py int8 > gpurun_out/prof_block_int8.log 2>&1
       timeout 600 python tools/prof_block.py bf16 > gpurun_out/prof_block_bf16.log 2>&1 ;;
+    wide)
+      timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_layer.py tests/test_gpu_base_dims.py tests/test_gpu_fuzz.py -x -q > gpurun_out/pytest_wide.log 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_wide.log
+      timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_wide.jsonl 2>&1
+      HALO_K1_WIDE=0 timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_nowide.jsonl 2>&1 ;;
     sweep)
       timeout 900 python tools/sweep_fwht.py > gpurun_out/sweep.jsonl 2>&1 ;;
     kern_v2)
