@@ -64,6 +64,9 @@ for w in $what; do
       echo "pytest rc=$?" >> gpurun_out/pytest_wide.log
       timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_wide.jsonl 2>&1
       HALO_K1_WIDE=0 timeout 600 python tools/sweep_fwht.py right > gpurun_out/sweep_right_nowide.jsonl 2>&1 ;;
+    prof_wide)
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_rows_v4|k_cols_lb' -s 4 -c 4 \
+        -f -o gpurun_out/prof_wide python tools/prof_lb_kernels.py > gpurun_out/prof_wide.log 2>&1 ;;
     sweep)
       timeout 900 python tools/sweep_fwht.py > gpurun_out/sweep.jsonl 2>&1 ;;
     kern_v2)
