@@ -126,9 +126,11 @@ template <int LB, typename InT>
 struct LbCfg {
     static constexpr int B = 1 << LB;
     static constexpr int ES = (int)sizeof(InT);
-    // elements per strip: 16384 (two CTAs per SM for bf16) unless the
-    // 16-byte staged rows need a wider strip (bf16 at B = 4096)
-    static constexpr int E = (ES == 2 && LB == 12) ? 32768 : 16384;
+    // elements per strip: wide rows pay (32-column bf16 strips run the
+    // B = 1024 op 1.3-1.5x faster than 16-column ones, 16 vs 8 columns at
+    // B = 2048 1.3x: profiles/r02k_ab_left_strip_width.txt), so bf16 takes
+    // 32 K-element strips (one CTA per SM) from B = 1024 on
+    static constexpr int E = (ES == 2 && LB >= 10) ? 32768 : 16384;
     static constexpr int W = E / B;                    // columns per strip
     static constexpr int NCP = W / 2;                  // column pairs
     static constexpr int NT = E / 128;                 // 64 float2 per thread
@@ -486,7 +488,7 @@ bool cols_lb(int mode, int fmt, int in_dtype, const void* in, int64_t b, int64_t
     if (!lb_enabled() || mode > 2 || B < 512 || B > 4096 || (B & (B - 1)) || rows_pad % B || b <= 0) return false;
     if (mode == LB_XFORM && (in_dtype != DT_F32 || !xout)) return false;
     const int es = in_dtype == DT_BF16 ? 2 : 4;
-    const int64_t W = (es == 2 ? 32768 : 16384) / B;
+    const int64_t W = ((es == 2 && B >= 1024) ? 32768 : 16384) / B;  // LbCfg::W
     if (cols % W || (uintptr_t)in % 16 || (cols * es) % 16) return false;
     if (mode == LB_QUANT && ((uintptr_t)cr % 16 || (cp && (uintptr_t)cp % 4))) return false;
     if (mode == LB_XFORM && (uintptr_t)xout % 16) return false;

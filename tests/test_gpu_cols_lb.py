@@ -35,7 +35,7 @@ def _codes(t):
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("fmt", [0, 1, 2])
 def test_left_large_block_codes_bitexact(H, orc, block, dtype, fmt):
-    E = 32768 if (dtype == "bf16" and block == 4096) else 16384  # strip elements
+    E = 32768 if (dtype == "bf16" and block >= 1024) else 16384  # strip elements
     W = E // block
     b, n = 2 * block - 37, 4 * W           # two token blocks (the second padded), four column strips
     rng = np.random.default_rng(block + 7 * fmt)

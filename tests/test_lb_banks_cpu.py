@@ -19,7 +19,7 @@ def _mod():
 
 def test_lb_layouts_bank_optimal():
     m = _mod()
-    for es, LB, E in ((2, 9, 16384), (2, 10, 16384), (2, 11, 16384), (2, 12, 32768),
+    for es, LB, E in ((2, 9, 16384), (2, 10, 32768), (2, 11, 32768), (2, 12, 32768),
                       (4, 9, 16384), (4, 10, 16384), (4, 11, 16384), (4, 12, 16384)):
         bad, _ = m.run(LB, E, es)
         assert max(bad.values()) == 0, (es, LB, bad)

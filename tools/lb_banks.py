@@ -52,7 +52,7 @@ def run(LB,E,es):
 
 if __name__ == "__main__":
     worst = 0
-    for es, LB, E in ((2, 9, 16384), (2, 10, 16384), (2, 11, 16384), (2, 12, 32768),
+    for es, LB, E in ((2, 9, 16384), (2, 10, 32768), (2, 11, 32768), (2, 12, 32768),
                       (4, 9, 16384), (4, 10, 16384), (4, 11, 16384), (4, 12, 16384)):
         bad, geo = run(LB, E, es)
         worst = max(worst, max(bad.values()))
