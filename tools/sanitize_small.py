@@ -98,7 +98,7 @@ f.forward(torch.randn(256, 256, device=dev).to(bf))
 f.backward(torch.randn(256, 256, device=dev).to(bf) * 1e-3)
 f.close()
 # large-block left transform (fwht_cols_lb.cu): bf16 / fp32, padded token block, transform-only
-for B in (512, 4096):
+for B in (512, 1024, 2048, 4096):
     el = (torch.randn(B - 37, 16384 // B * 2 if B < 4096 else 16, device=dev) * 1e-3)
     halo.left_rotate_quantize(el.to(bf), B)
     halo.left_rotate_quantize(el, B)
