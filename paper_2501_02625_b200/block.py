@@ -113,6 +113,46 @@ def _rmsnorm(x, w, eps=1e-5):
     return _RMSNormFn.apply(x, w, eps)
 
 
+class _RMSNormTeeFn(torch.autograd.Function):
+    """a = rmsnorm(x) for a block input x that also feeds the residual: the
+    Function returns (x, a) so that the residual gradient reaches its backward,
+    which folds the autograd engine's bf16 sum dx = RN(dres + rmsnorm'(da))
+    into the norm backward's store (halo_rmsnorm_backward_res) instead of a
+    separate add.  Bit-identical with `a = _rmsnorm(x)` used next to `x`."""
+
+    @staticmethod
+    def forward(ctx, x, w, eps):
+        from ._lib import DTYPE_BF16, check, lib
+        x = x.contiguous()
+        rows, dim = x.shape
+        a = torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        check(lib().halo_rmsnorm_forward(halo._ptr(x), halo._ptr(w), halo._ptr(a), DTYPE_BF16, halo._ptr(rstd), rows,
+                                         dim, 1, eps, halo._stream()))
+        ctx.save_for_backward(x, w, rstd)
+        return x.view_as(x), a
+
+    @staticmethod
+    def backward(ctx, dres, da):
+        from ._lib import check, lib
+        x, w, rstd = ctx.saved_tensors
+        rows, dim = x.shape
+        if da is None:
+            return dres, None, None
+        da = da.contiguous()
+        dx = torch.empty_like(x)
+        dw = torch.empty(dim, dtype=torch.float32, device=x.device)
+        if dres is None:
+            check(lib().halo_rmsnorm_backward(halo._ptr(x), halo._ptr(da), halo._dt(da), halo._ptr(w), halo._ptr(rstd),
+                                              halo._ptr(dx), halo._ptr(dw), rows, dim, 1, halo._stream()))
+        else:
+            dres = dres.contiguous()
+            check(lib().halo_rmsnorm_backward_res(halo._ptr(x), halo._ptr(da), halo._dt(da), halo._ptr(w),
+                                                  halo._ptr(rstd), halo._ptr(dres), halo._ptr(dx), halo._ptr(dw),
+                                                  rows, dim, halo._stream()))
+        return dx, dw, None
+
+
 class _AddRMSNormFn(torch.autograd.Function):
     """h = x + r; m = rmsnorm(h) in one kernel (halo_add_rmsnorm_forward),
     and the backward's residual-gradient sum dh + rmsnorm'(dm) fused into the
@@ -199,7 +239,10 @@ def attention_block(x, qkv_fn, o_fn, mlp_fn, n1, n2, cs, seq, heads, kv_heads):
     T, H = x.shape
     B = T // seq
     hd = H // heads
-    a = _rmsnorm(x, n1)
+    if _UNFUSED_GLUE:
+        a = _rmsnorm(x, n1)
+    else:
+        x, a = _RMSNormTeeFn.apply(x, n1, 1e-5)  # x also feeds the residual: its gradient sum is fused
     qkv = _RopeQKVFn.apply(qkv_fn(a), cs, seq, heads + kv_heads, heads + 2 * kv_heads, hd)
     nq, nk = heads * hd, kv_heads * hd
     # one split (its backward is a single cat into dqkv; three slices would

@@ -153,3 +153,30 @@ def test_add_rmsnorm_matches_unfused(rows, dim):
         outs.append((h.detach(), m.detach(), xi.grad, ri.grad, wi.grad))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_rmsnorm_tee_matches_unfused():
+    """block.py _RMSNormTeeFn (the first norm of a block, whose input also
+    feeds the residual) == _RMSNormFn next to the tensor itself: outputs,
+    the input gradient (residual + norm paths) and the gain gradient."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2501_02625_b200.block import _RMSNormFn, _RMSNormTeeFn
+    g = torch.Generator(device="cuda").manual_seed(7)
+    bf = torch.bfloat16
+    rows, dim = 512, 1024
+    x = torch.randn(rows, dim, generator=g, device="cuda").to(bf)
+    w = torch.rand(dim, generator=g, device="cuda") + 0.5
+    cx = (torch.randn(rows, dim, generator=g, device="cuda") * 1e-2).to(bf)
+    ca = (torch.randn(rows, dim, generator=g, device="cuda") * 1e-2).to(bf)
+    outs = []
+    for fused in (True, False):
+        xi, wi = x.clone().requires_grad_(True), w.clone().requires_grad_(True)
+        if fused:
+            xr, a = _RMSNormTeeFn.apply(xi, wi, 1e-5)
+        else:
+            xr, a = xi, _RMSNormFn.apply(xi, wi, 1e-5)
+        ((xr * cx).sum() + (a * ca).sum()).backward()
+        outs.append((a.detach(), xi.grad, wi.grad))
+    for p, q in zip(*outs):
+        assert torch.equal(p, q)
