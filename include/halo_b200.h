@@ -252,6 +252,17 @@ HALO_API halo_status halo_linear_forward(halo_linear* layer, const void* x, int3
 HALO_API halo_status halo_linear_forward_shared(halo_linear* layer, const halo_ctx* src, halo_ctx* ctx, void* y,
                                        int32_t y_dtype, halo_stream_t stream);
 
+/* halo_linear_forward_shared for the up projection of a Llama MLP with the
+ * SwiGLU product fused into the GEMM epilogue: u (b x n, bf16) = the
+ * projection's output, h = silu(g) * u (bf16, exactly halo_swiglu_forward of
+ * g and u) with g (b x n, bf16) the gate projection's output, read tile by
+ * tile while the tensor cores run (model.hpp:169-171 with the Llama gate).
+ * n must be a multiple of 256 and u, g, h 16-byte aligned
+ * (HALO_ERR_INVALID_ARGUMENT otherwise: use halo_linear_forward_shared +
+ * halo_swiglu_forward). */
+HALO_API halo_status halo_linear_forward_shared_swiglu(halo_linear* layer, const halo_ctx* src, halo_ctx* ctx,
+                                                       const void* g, void* u, void* h, halo_stream_t stream);
+
 /* backward, halo_linear.hpp:305-439: e_y (b x n) -> e_x (b x m), grad_w
  * (n x m; may be NULL to skip G).  Granularity::row: the row scales sit on
  * the contracted dim of E and G, so both products are the reference's

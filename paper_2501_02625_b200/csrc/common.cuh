@@ -89,7 +89,13 @@ __device__ __forceinline__ float warp_max(float v) {
 // SwiGLU glue (the Llama MLP's activation; not part of the reference path).
 // Every rounding is spelled out so the fused kernels (K1 swiglu-absmax, K2
 // swiglu-absmax) and the stand-alone glue kernels produce identical bits.
-__device__ __forceinline__ float swiglu_sigmoid(float g) { return __frcp_rn(__fadd_rn(1.0f, __expf(-g))); }
+// sigmoid(g) = 1 / (1 + exp(-g)) on the SFU (ex2.approx, rcp.approx: one
+// MUFU op each; the SwiGLU GEMM epilogue runs this per element)
+__device__ __forceinline__ float swiglu_sigmoid(float g) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(1.0f, __expf(-g))));
+    return r;
+}
 // h = silu(g) * u
 __device__ __forceinline__ float swiglu_fwd1(float g, float u) {
     return __fmul_rn(__fmul_rn(g, swiglu_sigmoid(g)), u);

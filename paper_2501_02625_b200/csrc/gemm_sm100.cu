@@ -102,6 +102,9 @@ struct GemmArgs {
     // peer GPU's HBM (TMA stores over NVLink).  0 parts = tmC.
     const CUtensorMap* c_maps;
     int c_parts, c_len;
+    // SwiGLU epilogue (the up projection of a Llama MLP): C = u (bf16) and
+    // h = silu(g) * u into tmH, g [M][N] bf16 read from HBM (glu_g != null)
+    const __nv_bfloat16* glu_g;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -381,9 +384,13 @@ __device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int&
 template <int FMT, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmC, GemmArgs p) {
+           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmH, GemmArgs p) {
     using C = GemmCfg<CG>;
-    constexpr int STAGES = C::STAGES;
+    // SwiGLU epilogue: one operand stage fewer, its smem doubles the
+    // epilogue staging (u and h boxes side by side)
+    const bool glu = p.glu_g != nullptr;
+    const int STAGES = glu ? C::STAGES - 1 : C::STAGES;
+    const int stg_bytes = glu ? 2 * STG_BYTES : STG_BYTES;
     constexpr int B_STAGE_BYTES = C::B_STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     // 1024 B alignment (128 B swizzle atoms) by pointer arithmetic on the
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
     // epilogue staging (1 KB aligned: 128 B-swizzled TMA-store boxes), then barriers
     float* stg = reinterpret_cast<float*>(sB + STAGES * B_STAGE_BYTES);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES + STG_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES + stg_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
@@ -562,7 +569,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // column half h of the 256-column accumulator
         const int ew = warp - 4;
         const int q = ew & 3, h = ew >> 2;
-        float* S = stg + ew * (32 * 32);
+        float* S = stg + ew * (glu ? 2 : 1) * (32 * 32);
         const float sa = *p.sa, sb = *p.sb;
         const double ss = (double)sa * (double)sb;
         const float ssf = (float)ss;
@@ -729,12 +736,74 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tile_coords(t, mt, nt, mb, nb);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
             const int row0 = mb * C::TILE_M + (int)rank * BM + q * 32;
             const int row = row0 + lane;
+            // SwiGLU epilogue: this lane's row of g, the first chunk fetched
+            // while the tile's mainloop still runs (rows >= M read row M-1;
+            // their outputs are clipped by the TMA store)
+            const uint4* grow = nullptr;
+            uint4 gn[4];
+            if (p.glu_g) {
+                grow = reinterpret_cast<const uint4*>(p.glu_g + (int64_t)min(row, p.M - 1) * p.N + nb * BN);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) gn[k] = __ldg(grow + 16 * h + k);
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
             const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             if (p.dbg_skip_epi == 1) {
+            } else if (p.glu_g) {
+                // ---- SwiGLU epilogue: u = the bf16 output, h = silu(g) * u
+                // exactly as k_swiglu_fwd computes it from bf16 g and u; u and
+                // h leave as 32-row x 128 B boxes (chunks c, c+1) from the two
+                // 4 KB halves of the warp's staging buffer
+                uint4* RU = reinterpret_cast<uint4*>(S) + lane * 8;
+                uint4* RH = RU + 256;
+#pragma unroll 1
+                for (int c = 4 * h; c < 4 * h + 4; ++c) {
+                    uint4 gc[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) gc[k] = gn[k];
+                    if (c + 1 < 4 * h + 4 && p.dbg_skip_epi != 8) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) gn[k] = __ldg(grow + 4 * (c + 1) + k);
+                    }
+                    uint32_t r[32];
+                    tmem_ld32(tacc + c * 32, r);
+                    float v[32];
+                    cvt(r, v, row, nb * BN + c * 32);
+                    if ((c & 1) == 0) {
+                        if (lane == 0) bulk_wait_read0();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t gw[4] = {gc[k].x, gc[k].y, gc[k].z, gc[k].w};
+                        uint32_t uw[4], hw[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uw[j] = pack_bf16x2(v[8 * k + 2 * j], v[8 * k + 2 * j + 1]);
+                            if (p.dbg_skip_epi == 9)  // timing experiment: no silu
+                                hw[j] = uw[j] ^ gw[j];
+                            else
+                                hw[j] = pack_bf16x2(swiglu_fwd1(__uint_as_float(gw[j] << 16), __uint_as_float(uw[j] << 16)),
+                                                    swiglu_fwd1(__uint_as_float(gw[j] & 0xFFFF0000u),
+                                                                __uint_as_float(uw[j] & 0xFFFF0000u)));
+                        }
+                        const int slot = (4 * (c & 1) + k) ^ (lane & 7);
+                        RU[slot] = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+                        RH[slot] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    }
+                    if (c & 1) {
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmC, S, nb * BN + (c - 1) * 32, row0);
+                            tma_store_2d(&tmH, S + 1024, nb * BN + (c - 1) * 32, row0);
+                            bulk_commit();
+                        }
+                    }
+                }
             } else if (p.dbg_skip_epi == 4) {
                 // timing experiment: TMEM loads + conversion, no stores
                 uint32_t x = 0;
@@ -992,6 +1061,22 @@ ShardScope::~ShardScope() {
 }
 bool ShardScope::active() { return t_shard_a || t_shard_b || t_scatter_c; }
 
+namespace {
+thread_local const void* t_glu_g = nullptr;
+thread_local void* t_glu_h = nullptr;
+thread_local bool t_glu_used = false;
+}  // namespace
+GluScope::GluScope(const void* g, void* h) {
+    t_glu_g = g;
+    t_glu_h = h;
+    t_glu_used = false;
+}
+GluScope::~GluScope() {
+    t_glu_g = nullptr;
+    t_glu_h = nullptr;
+}
+bool GluScope::used() { return t_glu_used; }
+
 bool encode_scatter_maps(void* const* recv, int parts, int slot, int64_t len, int64_t cols, CUtensorMap* out) {
     auto enc = get_encode();
     if (!enc) return false;
@@ -1081,11 +1166,30 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         const char* e = getenv("HALO_GEMM_TMA_STORE");
         return e ? atoi(e) : 1;
     }();
-    CUtensorMap mc;
+    CUtensorMap mc, mh;
     std::memset(&mc, 0, sizeof(mc));
+    std::memset(&mh, 0, sizeof(mh));
     const int esz = out_kind == 1 ? 2 : 4;
     args.tma_store = 0;
-    if (scc) {
+    if (t_glu_g) {
+        // SwiGLU epilogue: u and h as 32-row x 128 B boxes (128 B swizzle)
+        if (out_kind != 1 || out_trans || xf_lb || scc || N % BN || (uintptr_t)out % 16 ||
+            (uintptr_t)t_glu_g % 16 || (uintptr_t)t_glu_h % 16 || !tma_store_env)
+            return -1;
+        auto enc = get_encode();
+        const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+        const cuuint64_t strides[1] = {(cuuint64_t)N * 2};
+        const cuuint32_t box[2] = {64, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        for (int i = 0; i < 2; ++i)
+            if (!enc || enc(i ? &mh : &mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, i ? t_glu_h : out, dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return -2;
+        args.tma_store = 1;
+        args.glu_g = static_cast<const __nv_bfloat16*>(t_glu_g);
+        t_glu_used = true;
+    } else if (scc) {
         mc = scc->maps_host0;
         args.tma_store = 1;
         args.c_maps = scc->maps;
@@ -1111,7 +1215,7 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         const int grid = tiles < num_sms() ? tiles : num_sms();
         auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 1> : fmt == FMT_E3M2 ? k_gemm<FMT_E3M2, 1> : k_gemm<FMT_E4M3, 1>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<1>());
-        kern<<<grid, GEMM_THREADS, gemm_smem<1>(), st>>>(ma, mb, mc, args);
+        kern<<<grid, GEMM_THREADS, gemm_smem<1>(), st>>>(ma, mb, mc, mh, args);
     } else {
         auto kern = fmt == FMT_INT8 ? k_gemm<FMT_INT8, 2> : fmt == FMT_E3M2 ? k_gemm<FMT_E3M2, 2> : k_gemm<FMT_E4M3, 2>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<2>());
@@ -1138,7 +1242,7 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         const int grid = 2 * (tiles < mp ? tiles : mp);
         cfg.gridDim = dim3(grid, 1, 1);
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, args);
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mh, args);
         if (le != cudaSuccess) return (int)le;
     }
     const cudaError_t e = cudaGetLastError();

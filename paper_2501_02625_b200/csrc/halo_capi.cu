@@ -1198,6 +1198,21 @@ extern "C" halo_status halo_linear_forward_shared(halo_linear* l, const halo_ctx
     return cuda_check("forward_shared");
 }
 
+extern "C" halo_status halo_linear_forward_shared_swiglu(halo_linear* l, const halo_ctx* src, halo_ctx* c,
+                                                         const void* g, void* u, void* h, halo_stream_t stream) {
+    if (!g || !h || !u) return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared_swiglu: null argument");
+    if (l && (l->n % 256 || (uintptr_t)g % 16 || (uintptr_t)u % 16 || (uintptr_t)h % 16))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared_swiglu: out_features % 256 and 16 B alignment required");
+    GluScope glu(g, h);
+    const halo_status r = halo_linear_forward_shared(l, src, c, u, HALO_DTYPE_BF16, stream);
+    if (r != HALO_OK) return r;
+    if (!GluScope::used()) {
+        c->valid = false;
+        return fail(HALO_ERR_INVALID_ARGUMENT, "forward_shared_swiglu: the GEMM did not run the SwiGLU epilogue");
+    }
+    return HALO_OK;
+}
+
 // out = P (fp32, rows x cols) optionally right-rotated, converted to dtype
 static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
                          cudaStream_t st) {

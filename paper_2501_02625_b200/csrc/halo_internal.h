@@ -81,6 +81,13 @@ struct ShardScope {
     ~ShardScope();
     static bool active();  // sharded / scattered operands installed on this thread
 };
+// SwiGLU epilogue for the next run_gemm_v on this thread (the up projection
+// of a Llama MLP): C = u (bf16), h = silu(g) * u; g, h [M][N] bf16
+struct GluScope {
+    GluScope(const void* g, void* h);
+    ~GluScope();
+    static bool used();  // the GEMM under this scope took the SwiGLU epilogue
+};
 // receive buffers recv[i] = [parts][len][cols] fp32 of rank i; maps for slot `slot`
 bool encode_scatter_maps(void* const* recv, int parts, int slot, int64_t len, int64_t cols, CUtensorMap* out);
 bool encode_shard_maps(const uint8_t* const* parts, int n, int64_t inner, int64_t rows, CUtensorMap* out);

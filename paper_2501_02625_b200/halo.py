@@ -508,6 +508,21 @@ class HaloLinearLayer:
         ctx._shared_src = src  # keep the borrowed codes alive
         return y
 
+    def forward_shared_swiglu(self, src: SavedContext, ctx: SavedContext, g: torch.Tensor):
+        """forward_shared() of the up projection with the SwiGLU product in
+        the GEMM epilogue: returns (u, h = silu(g) * u), both bf16, h
+        identical to halo_swiglu_forward(g, u).  out_features % 256 == 0."""
+        b = src._layer_b
+        if g.dtype != torch.bfloat16 or tuple(g.shape) != (b, self.out_features) or not g.is_contiguous():
+            raise ValueError("forward_shared_swiglu: g must be a contiguous bf16 (b x out_features) tensor")
+        u = torch.empty((b, self.out_features), dtype=torch.bfloat16, device=self.w.device)
+        h = torch.empty_like(u)
+        check(lib().halo_linear_forward_shared_swiglu(self._h, src._h, ctx._h, _ptr(g), _ptr(u), _ptr(h), _stream()))
+        self._last_b = b
+        ctx._layer_b = b
+        ctx._shared_src = src
+        return u, h
+
     def backward(self, ctx: SavedContext, e_y: torch.Tensor, need_grad_w: bool = True,
                  e_x_dtype=None) -> BackwardResult:
         _need_cuda(e_y)

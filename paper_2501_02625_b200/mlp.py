@@ -37,6 +37,9 @@ class HaloMLP:
         # SwiGLU forward fused with the down projection's absmax pass
         # (halo_swiglu_forward_absmax, bit-exact; off: measured slower, see DESIGN)
         self.fuse_fwd = os.environ.get("HALO_MLP_FUSE_FWD", "0") == "1"
+        # SwiGLU product in the up projection's GEMM epilogue (bit-identical;
+        # HALO_MLP_GLU_EPI=0: the separate halo_swiglu_forward kernel)
+        self.glu_epi = os.environ.get("HALO_MLP_GLU_EPI", "1") == "1" and hidden % 256 == 0
         # tests: a dict here collects the step's intermediate tensors
         self.trace = None
         # HQ-FSDP hooks: pre(name, phase) runs before a projection's GEMMs
@@ -59,14 +62,18 @@ class HaloMLP:
         g = self.gate.forward(x, self.ctx[0])
         # up_proj sees the same X under the same quantizer: reuse gate's (XH)_Q
         self._pre("up", "fwd")
-        u = self.up.forward_shared(self.ctx[0], self.ctx[1]) if self.share_x else self.up.forward(x, self.ctx[1])
-        h = torch.empty_like(g)
-        if self.fuse_fwd:
-            # SwiGLU + the down projection's absmax pass in one read of g, u
-            check(lib().halo_swiglu_forward_absmax(self.down._h, self.ctx[2]._h, halo._ptr(g), halo._ptr(u),
-                                                   halo._ptr(h), g.shape[0], g.shape[1], halo._stream()))
+        if self.share_x and self.glu_epi and not self.fuse_fwd:
+            # h = silu(g) * u computed in the up projection's GEMM epilogue
+            u, h = self.up.forward_shared_swiglu(self.ctx[0], self.ctx[1], g)
         else:
-            check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
+            u = self.up.forward_shared(self.ctx[0], self.ctx[1]) if self.share_x else self.up.forward(x, self.ctx[1])
+            h = torch.empty_like(g)
+            if self.fuse_fwd:
+                # SwiGLU + the down projection's absmax pass in one read of g, u
+                check(lib().halo_swiglu_forward_absmax(self.down._h, self.ctx[2]._h, halo._ptr(g), halo._ptr(u),
+                                                       halo._ptr(h), g.shape[0], g.shape[1], halo._stream()))
+            else:
+                check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
         self._act = (g, u)
         self._pre("down", "fwd")
         y = self.down.forward(h, self.ctx[2])

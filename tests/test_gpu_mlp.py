@@ -150,6 +150,48 @@ def test_mlp_fused_forward_glue_bitexact(M, fmt):
         assert torch.equal(u, v)
 
 
+@pytest.mark.parametrize("fmt,b,m,n,gran", [(0, 1000, 512, 768, "tensor"), (1, 777, 256, 512, "tensor"),
+                                            (2, 300, 512, 256, "tensor"), (0, 1000, 512, 768, "row"),
+                                            (0, 2048, 4096, 14336, "tensor")])
+def test_swiglu_epilogue_bitexact(M, fmt, b, m, n, gran):
+    """The up projection with h = silu(g) * u in its GEMM epilogue
+    (halo_linear_forward_shared_swiglu) == forward_shared + the separate
+    halo_swiglu_forward kernel: same u and h bits, ragged token counts
+    (rows past b clipped), every format, row granularity, and a cfg2-wide
+    (14336-column) projection."""
+    halo, _ = M
+    from paper_2501_02625_b200._lib import check, lib
+    gen = torch.Generator(device="cuda").manual_seed(b + n)
+    bf = torch.bfloat16
+    scheme = halo.halo2(fmt, 256, halo.GRAN_ROW if gran == "row" else halo.GRAN_TENSOR)
+    halo.allow_dequantized_products(gran == "row")  # row-granularity layers (their backward) need the opt-in
+    wg = (torch.randn(n, m, generator=gen, device="cuda") / m ** 0.5).to(bf)
+    wu = (torch.randn(n, m, generator=gen, device="cuda") / m ** 0.5).to(bf)
+    x = torch.randn(b, m, generator=gen, device="cuda").to(bf)
+    gate = halo.HaloLinearLayer(wg, scheme, out_dtype=bf)
+    up = halo.HaloLinearLayer(wu, scheme, out_dtype=bf)
+    cg, c1, c2 = halo.SavedContext(), halo.SavedContext(), halo.SavedContext()
+    g = gate.forward(x, cg)
+    u_ref = up.forward_shared(cg, c1)
+    h_ref = torch.empty_like(g)
+    check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u_ref), halo._ptr(h_ref), g.numel(), halo._stream()))
+    u, h = up.forward_shared_swiglu(cg, c2, g)
+    torch.cuda.synchronize()
+    halo.allow_dequantized_products(False)
+    assert torch.equal(u, u_ref)
+    assert torch.equal(h, h_ref)
+
+
+def test_swiglu_epilogue_rejects_unaligned_width(M):
+    halo, _ = M
+    bf = torch.bfloat16
+    gate = halo.HaloLinearLayer(torch.randn(384, 256, device="cuda").to(bf), halo.halo2(0, 256), out_dtype=bf)
+    up = halo.HaloLinearLayer(torch.randn(384, 256, device="cuda").to(bf), halo.halo2(0, 256), out_dtype=bf)
+    cg = halo.SavedContext()
+    g = gate.forward(torch.randn(256, 256, device="cuda").to(bf), cg)
+    with pytest.raises(ValueError):
+        up.forward_shared_swiglu(cg, halo.SavedContext(), g)
+
 
 @pytest.mark.parametrize("plane", ["native", "torch"])
 def test_fsdp_mlp_world1_matches_mlp(M, plane):
