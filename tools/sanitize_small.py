@@ -108,5 +108,16 @@ xa = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
 ra = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
 ha, ma = block._AddRMSNormFn.apply(xa, ra, torch.ones(512, device=dev, requires_grad=True), 1e-5)
 ((ha * 0.5).sum() + ma.sum()).backward()
+# SwiGLU GEMM epilogue (halo_linear_forward_shared_swiglu): ragged token count
+wgs = (torch.randn(512, 256, device=dev) / 16).to(bf)
+gate_s = halo.HaloLinearLayer(wgs, halo.halo2(halo.INT8, 256), out_dtype=bf)
+up_s = halo.HaloLinearLayer(wgs.clone(), halo.halo2(halo.INT8, 256), out_dtype=bf)
+cgs = halo.SavedContext()
+gs = gate_s.forward(torch.randn(300, 256, device=dev).to(bf), cgs)
+up_s.forward_shared_swiglu(cgs, halo.SavedContext(), gs)
+# the block's first norm with the residual-gradient sum (block.py _RMSNormTeeFn)
+xt_ = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
+xr_, at_ = block._RMSNormTeeFn.apply(xt_, torch.ones(512, device=dev, requires_grad=True), 1e-5)
+((xr_ * 0.5).sum() + at_.sum()).backward()
 torch.cuda.synchronize()
 print("sanitize workload (round-2 kernels) done")
