@@ -741,12 +741,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             // SwiGLU epilogue: this lane's row of g, the first chunk fetched
             // while the tile's mainloop still runs (rows >= M read row M-1;
             // their outputs are clipped by the TMA store)
+            // (two chunks in flight: chunk i+2's load issues when chunk i is consumed)
             const uint4* grow = nullptr;
-            uint4 gn[4];
+            uint4 gq[2][4];
             if (p.glu_g) {
-                grow = reinterpret_cast<const uint4*>(p.glu_g + (int64_t)min(row, p.M - 1) * p.N + nb * BN);
+                grow = reinterpret_cast<const uint4*>(p.glu_g + (int64_t)min(row, p.M - 1) * p.N + nb * BN) + 16 * h;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) gn[k] = __ldg(grow + 16 * h + k);
+                for (int k = 0; k < 8; ++k) gq[k >> 2][k & 3] = __ldg(grow + k);
             }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -759,14 +760,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 // 4 KB halves of the warp's staging buffer
                 uint4* RU = reinterpret_cast<uint4*>(S) + lane * 8;
                 uint4* RH = RU + 256;
-#pragma unroll 1
-                for (int c = 4 * h; c < 4 * h + 4; ++c) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int c = 4 * h + i;
                     uint4 gc[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) gc[k] = gn[k];
-                    if (c + 1 < 4 * h + 4 && p.dbg_skip_epi != 8) {
+                    for (int k = 0; k < 4; ++k) gc[k] = gq[i & 1][k];
+                    if (i + 2 < 4 && p.dbg_skip_epi != 8) {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) gn[k] = __ldg(grow + 4 * (c + 1) + k);
+                        for (int k = 0; k < 4; ++k) gq[i & 1][k] = __ldg(grow + 4 * (i + 2) + k);
                     }
                     uint32_t r[32];
                     tmem_ld32(tacc + c * 32, r);
