@@ -198,11 +198,23 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bflo
     }
 }
 
-__global__ void k_sum_rows(const float* __restrict__ part, int nparts, int dim, float* __restrict__ out) {
+// dgain[c] = sum over the partials in order (double); 64-thread CTAs so the
+// 4096 columns spread over 64 SMs, 32 partial loads in flight per thread
+// (latency-bound: only dim threads exist)
+__global__ void __launch_bounds__(64) k_sum_rows(const float* __restrict__ part, int nparts, int dim,
+                                                 float* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= dim) return;
     double s = 0.0;
-    for (int i = 0; i < nparts; ++i) s += (double)part[(int64_t)i * dim + c];
+    int i = 0;
+    for (; i + 32 <= nparts; i += 32) {
+        float q[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) q[u] = __ldg(part + (int64_t)(i + u) * dim + c);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) s += (double)q[u];
+    }
+    for (; i < nparts; ++i) s += (double)part[(int64_t)i * dim + c];
     out[c] = (float)s;
 }
 
@@ -292,7 +304,7 @@ bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* g
         if (exact) HALO_NB(float, true, false); else HALO_NB(float, false, false);
     }
 #undef HALO_NB
-    k_sum_rows<<<(dim + 255) / 256, 256, 0, st>>>(scratch, (int)grid, dim, dgain);
+    k_sum_rows<<<(dim + 63) / 64, 64, 0, st>>>(scratch, (int)grid, dim, dgain);
     return true;
 }
 
