@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_fwd(const __nv_bflo
 // to part[blockIdx.x].  The second read of x / dy hits L2.  Phase 2 walks
 // its rows UNROLL at a time with every load issued before the math, so a
 // thread keeps 2 * UNROLL 16-byte requests in flight.
-constexpr int BWD_ROWS = 16;
+constexpr int BWD_ROWS = 8;
 constexpr int BWD_UNROLL = 4;
 // RES: dx = RN_bf16(RN_bf16(dx_norm) + dres) -- the autograd engine's bf16
 // accumulation of the residual-stream gradient, fused into the store.
@@ -198,23 +198,39 @@ __global__ void __launch_bounds__(32 * NORM_WARPS) k_rmsnorm_bwd(const __nv_bflo
     }
 }
 
-// dgain[c] = sum over the partials in order (double); 64-thread CTAs so the
-// 4096 columns spread over 64 SMs, 32 partial loads in flight per thread
-// (latency-bound: only dim threads exist)
-__global__ void __launch_bounds__(64) k_sum_rows(const float* __restrict__ part, int nparts, int dim,
-                                                 float* __restrict__ out) {
+// dgain[c] = the partials summed in double, deterministically in two levels:
+// level 1 sums each group of SUM_GROUP consecutive partials in order (every
+// (group, column) a thread: the whole GPU streams the partials), level 2 the
+// group sums in order (a short latency chain per column)
+constexpr int SUM_GROUP = 16;
+__global__ void __launch_bounds__(256) k_sum_rows1(const float* __restrict__ part, int nparts, int dim,
+                                                   double* __restrict__ gsum) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= dim) return;
+    const int i0 = blockIdx.y * SUM_GROUP, i1 = min(i0 + SUM_GROUP, nparts);
+    float q[SUM_GROUP];
+#pragma unroll
+    for (int u = 0; u < SUM_GROUP; ++u) q[u] = i0 + u < i1 ? __ldg(part + (int64_t)(i0 + u) * dim + c) : 0.f;
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < SUM_GROUP; ++u)
+        if (i0 + u < i1) s += (double)q[u];
+    gsum[(int64_t)blockIdx.y * dim + c] = s;
+}
+__global__ void __launch_bounds__(64) k_sum_rows2(const double* __restrict__ gsum, int ngroups, int dim,
+                                                  float* __restrict__ out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= dim) return;
     double s = 0.0;
     int i = 0;
-    for (; i + 32 <= nparts; i += 32) {
-        float q[32];
+    for (; i + 16 <= ngroups; i += 16) {
+        double q[16];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) q[u] = __ldg(part + (int64_t)(i + u) * dim + c);
+        for (int u = 0; u < 16; ++u) q[u] = gsum[(int64_t)(i + u) * dim + c];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) s += (double)q[u];
+        for (int u = 0; u < 16; ++u) s += q[u];
     }
-    for (; i < nparts; ++i) s += (double)part[(int64_t)i * dim + c];
+    for (; i < ngroups; ++i) s += gsum[(int64_t)i * dim + c];
     out[c] = (float)s;
 }
 
@@ -283,7 +299,11 @@ bool run_rmsnorm_fwd(const void* x, const float* gain, void* y, int y_dtype, flo
     return true;
 }
 
-int64_t rmsnorm_bwd_scratch(int64_t rows, int dim) { return (rows + BWD_ROWS - 1) / BWD_ROWS * (int64_t)dim; }
+// floats: the per-CTA partials, then the level-1 group sums (doubles)
+int64_t rmsnorm_bwd_scratch(int64_t rows, int dim) {
+    const int64_t parts = (rows + BWD_ROWS - 1) / BWD_ROWS, groups = (parts + SUM_GROUP - 1) / SUM_GROUP;
+    return parts * dim + 2 * groups * dim + 2;
+}
 
 bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* gain, const float* rstd, void* dx,
                      float* dgain, float* scratch, int64_t rows, int dim, bool mean, cudaStream_t st, const void* dres) {
@@ -304,7 +324,11 @@ bool run_rmsnorm_bwd(const void* x, const void* dy, int dy_dtype, const float* g
         if (exact) HALO_NB(float, true, false); else HALO_NB(float, false, false);
     }
 #undef HALO_NB
-    k_sum_rows<<<(dim + 63) / 64, 64, 0, st>>>(scratch, (int)grid, dim, dgain);
+    const int groups = (int)((grid + SUM_GROUP - 1) / SUM_GROUP);
+    // 8-byte aligned group sums after the partials
+    double* gsum = reinterpret_cast<double*>(scratch + (((int64_t)grid * dim + 1) & ~(int64_t)1));
+    k_sum_rows1<<<dim3((dim + 255) / 256, groups), 256, 0, st>>>(scratch, (int)grid, dim, gsum);
+    k_sum_rows2<<<(dim + 63) / 64, 64, 0, st>>>(gsum, groups, dim, dgain);
     return true;
 }
 
