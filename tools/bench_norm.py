@@ -1,4 +1,4 @@
-"""RMSNorm backward at the Llama block shape (8192 x 4096, bf16): the plain and
+"""RMSNorm forward / backward at the Llama block shape (8192 x 4096, bf16): the plain and
 the residual-gradient (RES) forms through the C ABI, CUDA-event times.
 Usage: python tools/bench_norm.py [reps]"""
 import os
@@ -37,7 +37,21 @@ def plain():
                                       halo._ptr(dw), rows, dim, 1, halo._stream()))
 
 
-for name, fn in (("res", res), ("plain", plain)):
+h_ = torch.empty_like(x)
+
+
+def fwd():
+    check(lib().halo_rmsnorm_forward(halo._ptr(x), halo._ptr(w), halo._ptr(a), 1, halo._ptr(rstd), rows, dim, 1, 1e-5,
+                                     halo._stream()))
+
+
+def fwd_add():
+    check(lib().halo_add_rmsnorm_forward(halo._ptr(x), halo._ptr(dres), halo._ptr(w), halo._ptr(h_), halo._ptr(a),
+                                         halo._ptr(rstd), rows, dim, 1e-5, halo._stream()))
+
+
+NBYTES = {"res": 4, "plain": 3, "fwd": 2, "fwd_add": 4}
+for name, fn in (("res", res), ("plain", plain), ("fwd", fwd), ("fwd_add", fwd_add)):
     for _ in range(3):
         fn()
     t = 0.0
@@ -50,5 +64,5 @@ for name, fn in (("res", res), ("plain", plain)):
         torch.cuda.synchronize()
         t += e0.elapsed_time(e1)
     ms = t / reps
-    nbytes = rows * dim * 2 * (4 if name == "res" else 3)
+    nbytes = rows * dim * 2 * NBYTES[name]
     print(f"{name}: {ms * 1e3:.1f} us  ({nbytes / ms / 1e6:.0f} GB/s over {nbytes / 1e6:.0f} MB)")
