@@ -263,6 +263,15 @@ HALO_API halo_status halo_linear_forward_shared(halo_linear* layer, const halo_c
 HALO_API halo_status halo_linear_forward_shared_swiglu(halo_linear* layer, const halo_ctx* src, halo_ctx* ctx,
                                                        const void* g, void* u, void* h, halo_stream_t stream);
 
+/* halo_linear_forward with the residual add of the block that follows the
+ * projection (model.hpp:159-209: y = h + MLP(.), the MLP's last projection)
+ * in the GEMM epilogue: y = RN_bf16(res + RN_bf16(x W^T)) (bf16), exactly a
+ * bf16 forward output added to res as torch adds two bf16 tensors.  res and
+ * y b x n bf16, n a multiple of 256, 16-byte aligned (HALO_ERR_INVALID_ARGUMENT
+ * otherwise: use halo_linear_forward + halo_add). */
+HALO_API halo_status halo_linear_forward_residual(halo_linear* layer, const void* x, int32_t x_dtype, int64_t b,
+                                                  const void* res, void* y, halo_ctx* ctx, halo_stream_t stream);
+
 /* backward, halo_linear.hpp:305-439: e_y (b x n) -> e_x (b x m), grad_w
  * (n x m; may be NULL to skip G).  Granularity::row: the row scales sit on
  * the contracted dim of E and G, so both products are the reference's

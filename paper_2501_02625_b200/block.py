@@ -56,6 +56,37 @@ class _HaloMLPFn(torch.autograd.Function):
         return dx, None
 
 
+class _HaloMLPResFn(torch.autograd.Function):
+    """h + MLP(m) with the residual add in the down projection's GEMM
+    epilogue (mlp.HaloMLP.forward(m, residual=h)); dh = dy."""
+
+    @staticmethod
+    def forward(ctx, m, h, mlp):
+        ctx.mlp = mlp
+        return mlp.forward(m.contiguous(), residual=h)
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx, grads = ctx.mlp.backward(dy.contiguous())
+        for lin, g in zip(ctx.mlp.owners, grads):
+            lin.grad = g if lin.grad is None else lin.grad + g
+        return dx, dy, None
+
+
+class HaloMLPCall:
+    """The block's mlp_fn over a HaloMLP: mlp_fn(m) = MLP(m) and, for
+    attention_block's residual, mlp_fn(m, h) = h + MLP(m) in one epilogue."""
+    residual = True
+
+    def __init__(self, mlp):
+        self.mlp = mlp
+
+    def __call__(self, m, h=None):
+        if h is None:
+            return _HaloMLPFn.apply(m, self.mlp)
+        return _HaloMLPResFn.apply(m, h, self.mlp)
+
+
 class HaloLinear:
     """One projection: weight [out, in] (bf16), a reusable SavedContext."""
 
@@ -261,6 +292,8 @@ def attention_block(x, qkv_fn, o_fn, mlp_fn, n1, n2, cs, seq, heads, kv_heads):
         m = _rmsnorm(h, n2)
     else:
         h, m = _AddRMSNormFn.apply(x, o_fn(att), n2, 1e-5)  # h = x + O(att); m = rmsnorm(h)
+    if getattr(mlp_fn, "residual", False) and not _UNFUSED_GLUE:
+        return mlp_fn(m, h)  # y = h + MLP(m), the add in the down projection's epilogue
     return h + mlp_fn(m)
 
 
@@ -298,7 +331,7 @@ class LlamaBlock:
     def forward(self, x):
         """x: [batch * seq, hidden] bf16 (requires_grad for the backward)."""
         if self.mlp is not None:
-            mlp_fn = lambda m: _HaloMLPFn.apply(m, self.mlp)  # noqa: E731
+            mlp_fn = HaloMLPCall(self.mlp)
         else:
             mlp_fn = lambda m: self.down(F.silu(self.gate(m)) * self.up(m))  # noqa: E731
         return attention_block(x, self.qkv, self.o, mlp_fn, self.n1, self.n2, self.cs, self.seq, self.heads, self.kv)

@@ -103,8 +103,11 @@ struct GemmArgs {
     const CUtensorMap* c_maps;
     int c_parts, c_len;
     // SwiGLU epilogue (the up projection of a Llama MLP): C = u (bf16) and
-    // h = silu(g) * u into tmH, g [M][N] bf16 read from HBM (glu_g != null)
+    // h = silu(g) * u into tmH, g [M][N] bf16 read from HBM (glu_g != null);
+    // glu_res: residual epilogue instead, C = RN_bf16(g + RN_bf16(acc)) (the
+    // block's y = h + MLP(.) as torch adds two bf16 tensors), no tmH
     const __nv_bfloat16* glu_g;
+    int glu_res;
 };
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     using C = GemmCfg<CG>;
     // SwiGLU epilogue: one operand stage fewer, its smem doubles the
     // epilogue staging (u and h boxes side by side)
-    const bool glu = p.glu_g != nullptr;
+    const bool glu = p.glu_g != nullptr && !p.glu_res;
     const int STAGES = glu ? C::STAGES - 1 : C::STAGES;
     const int stg_bytes = glu ? 2 * STG_BYTES : STG_BYTES;
     constexpr int B_STAGE_BYTES = C::B_STAGE_BYTES;
@@ -785,7 +788,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             uw[j] = pack_bf16x2(v[8 * k + 2 * j], v[8 * k + 2 * j + 1]);
-                            if (p.dbg_skip_epi == 9)  // timing experiment: no silu
+                            if (p.glu_res)  // y = RN(res + RN(acc))
+                                uw[j] = pack_bf16x2(__uint_as_float(gw[j] << 16) + __uint_as_float(uw[j] << 16),
+                                                    __uint_as_float(gw[j] & 0xFFFF0000u) +
+                                                        __uint_as_float(uw[j] & 0xFFFF0000u));
+                            else if (p.dbg_skip_epi == 9)  // timing experiment: no silu
                                 hw[j] = uw[j] ^ gw[j];
                             else
                                 hw[j] = pack_bf16x2(swiglu_fwd1(__uint_as_float(gw[j] << 16), __uint_as_float(uw[j] << 16)),
@@ -794,14 +801,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         }
                         const int slot = (4 * (c & 1) + k) ^ (lane & 7);
                         RU[slot] = make_uint4(uw[0], uw[1], uw[2], uw[3]);
-                        RH[slot] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        if (!p.glu_res) RH[slot] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                     }
                     if (c & 1) {
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
                             tma_store_2d(&tmC, S, nb * BN + (c - 1) * 32, row0);
-                            tma_store_2d(&tmH, S + 1024, nb * BN + (c - 1) * 32, row0);
+                            if (!p.glu_res) tma_store_2d(&tmH, S + 1024, nb * BN + (c - 1) * 32, row0);
                             bulk_commit();
                         }
                     }
@@ -1175,6 +1182,7 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
     args.tma_store = 0;
     if (t_glu_g) {
         // SwiGLU epilogue: u and h as 32-row x 128 B boxes (128 B swizzle)
+        // (t_glu_h null: the residual epilogue, C only)
         if (out_kind != 1 || out_trans || xf_lb || scc || N % BN || (uintptr_t)out % 16 ||
             (uintptr_t)t_glu_g % 16 || (uintptr_t)t_glu_h % 16 || !tma_store_env)
             return -1;
@@ -1183,13 +1191,14 @@ int run_gemm_v(int fmt, const uint8_t* A, const uint8_t* B, int64_t M, int64_t N
         const cuuint64_t strides[1] = {(cuuint64_t)N * 2};
         const cuuint32_t box[2] = {64, 32};
         const cuuint32_t estr[2] = {1, 1};
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < (t_glu_h ? 2 : 1); ++i)
             if (!enc || enc(i ? &mh : &mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, i ? t_glu_h : out, dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
                 return -2;
         args.tma_store = 1;
         args.glu_g = static_cast<const __nv_bfloat16*>(t_glu_g);
+        args.glu_res = t_glu_h ? 0 : 1;
         t_glu_used = true;
     } else if (scc) {
         mc = scc->maps_host0;

@@ -1213,6 +1213,21 @@ extern "C" halo_status halo_linear_forward_shared_swiglu(halo_linear* l, const h
     return HALO_OK;
 }
 
+extern "C" halo_status halo_linear_forward_residual(halo_linear* l, const void* x, int32_t x_dtype, int64_t b,
+                                                    const void* res, void* y, halo_ctx* c, halo_stream_t stream) {
+    if (!res || !y) return fail(HALO_ERR_INVALID_ARGUMENT, "forward_residual: null argument");
+    if (l && (l->n % 256 || (uintptr_t)res % 16 || (uintptr_t)y % 16))
+        return fail(HALO_ERR_INVALID_ARGUMENT, "forward_residual: out_features % 256 and 16 B alignment required");
+    GluScope glu(res, nullptr);
+    const halo_status r = halo_linear_forward(l, x, x_dtype, b, y, HALO_DTYPE_BF16, c, stream);
+    if (r != HALO_OK) return r;
+    if (!GluScope::used()) {
+        c->valid = false;
+        return fail(HALO_ERR_INVALID_ARGUMENT, "forward_residual: the GEMM did not run the residual epilogue");
+    }
+    return HALO_OK;
+}
+
 // out = P (fp32, rows x cols) optionally right-rotated, converted to dtype
 static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
                          cudaStream_t st) {

@@ -82,7 +82,8 @@ struct ShardScope {
     static bool active();  // sharded / scattered operands installed on this thread
 };
 // SwiGLU epilogue for the next run_gemm_v on this thread (the up projection
-// of a Llama MLP): C = u (bf16), h = silu(g) * u; g, h [M][N] bf16
+// of a Llama MLP): C = u (bf16), h = silu(g) * u; g, h [M][N] bf16.  h null:
+// the residual epilogue, C = RN_bf16(g + RN_bf16(acc))
 struct GluScope {
     GluScope(const void* g, void* h);
     ~GluScope();

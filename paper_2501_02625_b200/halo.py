@@ -496,6 +496,22 @@ class HaloLinearLayer:
         ctx._layer_b = b
         return y
 
+    def forward_residual(self, x: torch.Tensor, ctx: SavedContext, res: torch.Tensor) -> torch.Tensor:
+        """res + forward(x) with the add in the GEMM epilogue (bf16 output,
+        out_features % 256 == 0): identical to ``res + self.forward(x, ctx)``
+        for a bf16 layer."""
+        _need_cuda(x)
+        if x.dim() != 2 or x.shape[1] != self.in_features:
+            raise ValueError("halo layer: input feature dim mismatch")
+        b = x.shape[0]
+        if res.dtype != torch.bfloat16 or tuple(res.shape) != (b, self.out_features) or not res.is_contiguous():
+            raise ValueError("forward_residual: res must be a contiguous bf16 (b x out_features) tensor")
+        y = torch.empty((b, self.out_features), dtype=torch.bfloat16, device=x.device)
+        check(lib().halo_linear_forward_residual(self._h, _ptr(x), _dt(x), b, _ptr(res), _ptr(y), ctx._h, _stream()))
+        self._last_b = b
+        ctx._layer_b = b
+        return y
+
     def forward_shared(self, src: SavedContext, ctx: SavedContext) -> torch.Tensor:
         """forward() on the X already quantized in ``src`` (another layer's
         context with the same in_features and X quantizer): the gate/up pattern

@@ -40,6 +40,9 @@ class HaloMLP:
         # SwiGLU product in the up projection's GEMM epilogue (bit-identical;
         # HALO_MLP_GLU_EPI=0: the separate halo_swiglu_forward kernel)
         self.glu_epi = os.environ.get("HALO_MLP_GLU_EPI", "1") == "1" and hidden % 256 == 0
+        # forward(x, residual): the add in the down projection's GEMM epilogue
+        # (bit-identical; HALO_MLP_RES_EPI=0: a separate bf16 add)
+        self.res_epi = os.environ.get("HALO_MLP_RES_EPI", "1") == "1"
         # tests: a dict here collects the step's intermediate tensors
         self.trace = None
         # HQ-FSDP hooks: pre(name, phase) runs before a projection's GEMMs
@@ -57,7 +60,9 @@ class HaloMLP:
             return self.post_grad(name, grad)
         return grad
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, residual: torch.Tensor = None) -> torch.Tensor:
+        """y = down(silu(gate(x)) * up(x)), plus ``residual`` when given (the
+        block's y = h + MLP(.), added in the down projection's GEMM epilogue)."""
         self._pre("gate", "fwd")
         g = self.gate.forward(x, self.ctx[0])
         # up_proj sees the same X under the same quantizer: reuse gate's (XH)_Q
@@ -76,7 +81,12 @@ class HaloMLP:
                 check(lib().halo_swiglu_forward(halo._ptr(g), halo._ptr(u), halo._ptr(h), g.numel(), halo._stream()))
         self._act = (g, u)
         self._pre("down", "fwd")
-        y = self.down.forward(h, self.ctx[2])
+        if residual is None:
+            y = self.down.forward(h, self.ctx[2])
+        elif self.res_epi and self.down.out_features % 256 == 0 and self.down.out_dtype == torch.bfloat16:
+            y = self.down.forward_residual(h, self.ctx[2], residual.contiguous())
+        else:
+            y = residual + self.down.forward(h, self.ctx[2])
         if self.trace is not None:
             self.trace.update(g=g, u=u, h=h, y=y)
         return y

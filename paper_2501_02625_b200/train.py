@@ -38,7 +38,7 @@ import torch.distributed as dist
 
 from . import fsdp, halo
 from ._lib import DTYPE_BF16, DTYPE_F32, check, lib
-from .block import HaloLinear, _HaloMLPFn, attention_block, rope_table
+from .block import HaloLinear, HaloMLPCall, attention_block, rope_table
 
 
 @dataclass
@@ -250,7 +250,7 @@ class HqFsdpLlama:
         d = self.d
         n1, n2 = self.norms[l]
         ex = self._exec(l)
-        return attention_block(x, ex.lin["qkv"], ex.lin["o"], lambda m: _HaloMLPFn.apply(m, ex.mlp), n1, n2,
+        return attention_block(x, ex.lin["qkv"], ex.lin["o"], HaloMLPCall(ex.mlp), n1, n2,
                                self.cs, d.seq, d.heads, d.kv_heads)
 
     # --------------------------------------------------------------- step

@@ -182,6 +182,48 @@ def test_swiglu_epilogue_bitexact(M, fmt, b, m, n, gran):
     assert torch.equal(h, h_ref)
 
 
+@pytest.mark.parametrize("fmt,b", [(0, 1000), (1, 512), (0, 8192)])
+def test_residual_epilogue_bitexact(M, fmt, b):
+    """HaloMLP.forward(x, residual=r) (the add in the down projection's GEMM
+    epilogue, halo_linear_forward_residual) == r + HaloMLP.forward(x) as torch
+    adds the two bf16 tensors; ragged and cfg2-sized token counts."""
+    halo, mlp = M
+    wg, wu, wd, g = _weights(1024, 512, seed=13)
+    x = torch.randn(b, 512, generator=g, device="cuda").to(torch.bfloat16)
+    r = torch.randn(b, 512, generator=g, device="cuda").to(torch.bfloat16)
+    m = mlp.HaloMLP(wg, wu, wd, halo.halo2(fmt, 256))
+    y_ref = r + m.forward(x)
+    y = m.forward(x, residual=r)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+
+
+def test_block_fused_glue_matches_unfused(M, monkeypatch):
+    """block.attention_block with every glue fusion (tee'd first norm, fused
+    residual add + norm, one q/k/v split, the residual add in the down
+    projection's epilogue) == the unfused composition: output, input gradient,
+    weight and norm-gain gradients bit-identical."""
+    halo, _ = M
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    from paper_2501_02625_b200 import block
+    kw = dict(hidden=512, heads=4, kv_heads=2, inter=1024, seq=256, seed=3)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(512, 512, generator=g, device="cuda").to(torch.bfloat16)
+    dy = (torch.randn(512, 512, generator=g, device="cuda") * 1e-2).to(torch.bfloat16)
+    outs = []
+    with sdpa_kernel(SDPBackend.MATH):
+        for unfused in (False, True):
+            monkeypatch.setattr(block, "_UNFUSED_GLUE", unfused)
+            blk = block.LlamaBlock(halo.halo2(halo.INT8, 256), **kw)
+            xi = x.detach().requires_grad_(True)
+            y = blk.forward(xi)
+            y.backward(dy)
+            outs.append([y.detach(), xi.grad] + [l.grad for l in blk.linears()] + [blk.n1.grad, blk.n2.grad])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 def test_swiglu_epilogue_rejects_unaligned_width(M):
     halo, _ = M
     bf = torch.bfloat16
