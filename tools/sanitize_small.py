@@ -115,6 +115,9 @@ up_s = halo.HaloLinearLayer(wgs.clone(), halo.halo2(halo.INT8, 256), out_dtype=b
 cgs = halo.SavedContext()
 gs = gate_s.forward(torch.randn(300, 256, device=dev).to(bf), cgs)
 up_s.forward_shared_swiglu(cgs, halo.SavedContext(), gs)
+# residual epilogue (halo_linear_forward_residual): ragged token count
+dn_s = halo.HaloLinearLayer((torch.randn(256, 512, device=dev) / 16).to(bf), halo.halo2(halo.INT8, 256), out_dtype=bf)
+dn_s.forward_residual(gs, halo.SavedContext(), torch.randn(300, 256, device=dev).to(bf))
 # the block's first norm with the residual-gradient sum (block.py _RMSNormTeeFn)
 xt_ = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
 xr_, at_ = block._RMSNormTeeFn.apply(xt_, torch.ones(512, device=dev, requires_grad=True), 1e-5)
