@@ -272,6 +272,15 @@ HALO_API halo_status halo_linear_forward_shared_swiglu(halo_linear* layer, const
 HALO_API halo_status halo_linear_forward_residual(halo_linear* layer, const void* x, int32_t x_dtype, int64_t b,
                                                   const void* res, void* y, halo_ctx* ctx, halo_stream_t stream);
 
+/* halo_linear_backward with e_x accumulated onto a bf16 addend: e_x =
+ * RN_bf16(e_x_add + RN_bf16(E_X)) -- the sum of the input gradients of two
+ * projections reading the same X (the Llama gate / up pair), fused into the
+ * E path's K4 store where the scheme has one (HALO-2, block 64..256), else a
+ * separate add.  Identical to halo_linear_backward + halo_add. */
+HALO_API halo_status halo_linear_backward_acc(halo_linear* layer, const halo_ctx* ctx, const void* e_y,
+                                              int32_t e_dtype, const void* e_x_add, void* e_x, int32_t ex_dtype,
+                                              void* grad_w, int32_t gw_dtype, halo_stream_t stream);
+
 /* backward, halo_linear.hpp:305-439: e_y (b x n) -> e_x (b x m), grad_w
  * (n x m; may be NULL to skip G).  Granularity::row: the row scales sit on
  * the contracted dim of E and G, so both products are the reference's

@@ -130,6 +130,8 @@ def lib():
     L.halo_linear_forward_shared_swiglu.restype = C.c_int
     L.halo_linear_forward_residual.argtypes = [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]
     L.halo_linear_forward_residual.restype = C.c_int
+    L.halo_linear_backward_acc.argtypes = [_vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _i32, _vp]
+    L.halo_linear_backward_acc.restype = C.c_int
     L.halo_linear_create.argtypes = [C.POINTER(Scheme), _vp, _i32, _i64, _i64, C.POINTER(_vp)]
     L.halo_linear_destroy.argtypes = [_vp]
     L.halo_linear_set_weight.argtypes = [_vp, _vp, _i32]
@@ -249,7 +251,7 @@ EXPORTS = (
     "halo_rotate_absmax", "halo_left_rotate_quantize", "halo_padded_batch", "halo_transform_right",
     "halo_transform_left", "halo_qmatmul", "halo_qmatmul_rotate", "halo_rotate_quantize_rows",
     "halo_qmatmul_scaled", "halo_linear_forward_shared", "halo_linear_forward_shared_swiglu",
-    "halo_linear_forward_residual",
+    "halo_linear_forward_residual", "halo_linear_backward_acc",
     "halo_linear_create", "halo_linear_destroy",
     "halo_linear_set_weight", "halo_linear_set_qweight", "halo_ctx_create", "halo_ctx_destroy",
     "halo_linear_forward", "halo_linear_backward", "halo_linear_export_inference_weights",

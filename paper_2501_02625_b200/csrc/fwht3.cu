@@ -508,6 +508,16 @@ struct RowsCore {
                     }
                 }
             } else if constexpr (MODE == V3_XFORM) {
+                // the optional bf16 addend (see below): all 8 loads in flight first
+                uint2 addq[8];
+                if constexpr (sizeof(OutT) == 2) {
+                    if (codes) {
+#pragma unroll
+                        for (int b = 0; b < 8; ++b)
+                            addq[b] = e0 + 32 * b < n ? __ldg(reinterpret_cast<const uint2*>(codes) + (e0 + 32 * b) / 4)
+                                                      : make_uint2(0u, 0u);
+                    }
+                }
 #pragma unroll
                 for (int b = 0; b < 8; ++b) {
                     if (e0 + 32 * b < n) {
@@ -515,8 +525,18 @@ struct RowsCore {
                         if constexpr (sizeof(OutT) == 4) {
                             *reinterpret_cast<float4*>(out + e0 + 32 * b) = make_float4(a.x, a.y, c.x, c.y);
                         } else {
-                            *reinterpret_cast<uint2*>(out + e0 + 32 * b) =
-                                make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(c.x, c.y));
+                            uint2 o = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(c.x, c.y));
+                            if (codes) {
+                                // XFORM: `codes` carries an optional bf16 addend
+                                // (rows_xform_add): out = RN(add + RN(value)),
+                                // a bf16 tensor add of the transformed output
+                                const uint2 q = addq[b];
+                                o.x = pack_bf16x2(__uint_as_float(q.x << 16) + __uint_as_float(o.x << 16),
+                                                  __uint_as_float(q.x & 0xFFFF0000u) + __uint_as_float(o.x & 0xFFFF0000u));
+                                o.y = pack_bf16x2(__uint_as_float(q.y << 16) + __uint_as_float(o.y << 16),
+                                                  __uint_as_float(q.y & 0xFFFF0000u) + __uint_as_float(o.y & 0xFFFF0000u));
+                            }
+                            *reinterpret_cast<uint2*>(out + e0 + 32 * b) = o;
                         }
                     }
                 }
@@ -1138,6 +1158,16 @@ bool rows_lb(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t
 
 // B = 2^lb with lb in [0, 10]; n a multiple of 16 (and of B).  B = 512 / 1024
 // (RowsCore::finish_wide) only for whole 1024-element chunks.
+// K4 (transform-only, fp32 in, bf16 out) with a bf16 addend fused into the
+// store: out = RN_bf16(add + RN_bf16(H-rotated in)).  Only the exchange path
+// of the row kernels (B = 64 .. 256) implements it; false = not handled.
+bool rows_xform_add(const float* in, int64_t n, int64_t B, const void* add, void* out, cudaStream_t st) {
+    if (B != 64 && B != 128 && B != 256) return false;
+    if (n % 16 || (uintptr_t)in % 32 || (uintptr_t)add % 32 || (uintptr_t)out % 16) return false;
+    return rows_v3(V3_XFORM, 0, DT_F32, in, n, B, nullptr, nullptr,
+                   const_cast<uint8_t*>(static_cast<const uint8_t*>(add)), out, DT_BF16, nullptr, nullptr, st);
+}
+
 bool rows_v3(int mode, int fmt, int in_dtype, const void* in, int64_t n, int64_t B, unsigned* amax, const float* sup,
              uint8_t* codes, void* out, int out_dtype, unsigned* err, float* sout, cudaStream_t st) {
     if (n % 16 || B < 1 || B > 1024 || (B & (B - 1))) return false;

@@ -920,7 +920,7 @@ static halo_status quantize_weight(halo_linear* l, halo_ctx* c, bool rotated, Bu
 }
 
 static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
-                         cudaStream_t st);
+                         cudaStream_t st, const void* add = nullptr, bool* add_used = nullptr);
 
 extern "C" halo_status halo_linear_forward(halo_linear* l, const void* x, int32_t x_dtype, int64_t b, void* y,
                                            int32_t y_dtype, halo_ctx* c, halo_stream_t stream) {
@@ -1228,9 +1228,25 @@ extern "C" halo_status halo_linear_forward_residual(halo_linear* l, const void* 
     return HALO_OK;
 }
 
+// halo_linear_backward_acc: a bf16 addend for the E path of this thread's
+// next halo_linear_backward (e_x = add + E_X), fused when the K4 kernel can
+namespace {
+thread_local const void* t_ex_add = nullptr;
+thread_local bool t_ex_add_used = false;
+}  // namespace
+
 // out = P (fp32, rows x cols) optionally right-rotated, converted to dtype
+// (add: a bf16 addend fused into the store when the K4 kernel can, *add_used
+// then set -- the E path of halo_linear_backward_acc)
 static void finish_right(const float* P, void* out, int32_t dtype, int64_t rows, int64_t cols, int64_t B, bool rotate,
-                         cudaStream_t st) {
+                         cudaStream_t st, const void* add, bool* add_used) {
+    if (add && rotate && dtype == HALO_DTYPE_BF16) {
+        ProfScope ps(PC_K4, (double)rows * cols * (4 + 2 + 2), st);
+        if (rows_xform_add(P, rows * cols, B, add, out, st)) {
+            *add_used = true;
+            return;
+        }
+    }
     // B == 1 is the identity transform with norm 1: an exact copy/convert
     ProfScope ps(PC_K4, (double)rows * cols * (4 + dt_bytes(dtype)), st);
     BaseScope ht(true);  // transform_right_ht (H^T; = H for power-of-two blocks)
@@ -1463,6 +1479,9 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
                                             halo_stream_t stream) {
     if (!l || !cc || !e_y || !e_x) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
     halo_ctx* c = const_cast<halo_ctx*>(cc);  // scratch buffers only; saved codes are read-only
+    // halo_linear_backward_acc's addend: only the tensor path's E K4 takes it
+    const void* ex_add = t_ex_add;
+    t_ex_add = nullptr;
     if (!c->valid) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: backward without forward context");
     if (c->gran == HALO_GRAN_MX) return backward_mx(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
     if (c->row_gran || c->gran == HALO_GRAN_COLUMN) return backward_grouped(l, c, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, (cudaStream_t)stream);
@@ -1538,7 +1557,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
                      P, b, nullptr, nullptr, nullptr, st);
         }
         // prod = transform_right_ht(prod)  (:410-411)
-        finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st);
+        finish_right(P, e_x, ex_dtype, b, m, Bm, s.E.right, st, ex_add, &t_ex_add_used);
     } else {
         c->b_pad = b;
         const halo_status r = rotate_quantize_impl(e_y, e_dtype, b, n, 1, false, fmt, nullptr, c->S()->eq.as<uint8_t>(),
@@ -1557,7 +1576,7 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
             float* P = c->S()->scratch.as<float>();
             int gr = prof_gemm(fmt, c->S()->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, P, 0, st);
             if (gr != 0) return fail(HALO_ERR_CUDA, "backward: E GEMM launch failed");
-            finish_right(P, e_x, ex_dtype, b, m, Bm, true, st);
+            finish_right(P, e_x, ex_dtype, b, m, Bm, true, st, ex_add, &t_ex_add_used);
         } else {
             int gr = prof_gemm(fmt, c->S()->eq.as<uint8_t>(), wq, b, m, n, 1, 0, &d->scale[SE], sw, e_x,
                               ex_dtype == HALO_DTYPE_F32 ? 0 : 1, st);
@@ -1604,6 +1623,24 @@ extern "C" halo_status halo_linear_backward(halo_linear* l, const halo_ctx* cc, 
         }
     }
     return cuda_check("backward");
+}
+
+extern "C" halo_status halo_linear_backward_acc(halo_linear* l, const halo_ctx* cc, const void* e_y, int32_t e_dtype,
+                                                const void* e_x_add, void* e_x, int32_t ex_dtype, void* grad_w,
+                                                int32_t gw_dtype, halo_stream_t stream) {
+    if (!e_x_add) return fail(HALO_ERR_INVALID_ARGUMENT, "backward_acc: null addend");
+    if (ex_dtype != HALO_DTYPE_BF16) return fail(HALO_ERR_INVALID_ARGUMENT, "backward_acc: e_x must be bf16");
+    if (!l || !cc) return fail(HALO_ERR_INVALID_ARGUMENT, "halo layer: null argument");
+    t_ex_add = e_x_add;  // taken (and cleared) by halo_linear_backward on entry
+    t_ex_add_used = false;
+    const halo_status r = halo_linear_backward(l, cc, e_y, e_dtype, e_x, ex_dtype, grad_w, gw_dtype, stream);
+    const bool fused = t_ex_add_used;
+    t_ex_add = nullptr;
+    t_ex_add_used = false;
+    if (r != HALO_OK || fused) return r;
+    // the E path had no fusable K4 (other schemes / blocks): a separate add
+    run_add(e_x_add, e_x, e_x, DT_BF16, cc->b * l->m, (cudaStream_t)stream);
+    return cuda_check("backward_acc");
 }
 
 extern "C" halo_status halo_linear_export_inference_weights(halo_linear* l, uint8_t* codes, float* scale,

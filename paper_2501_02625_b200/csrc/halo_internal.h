@@ -81,6 +81,9 @@ struct ShardScope {
     ~ShardScope();
     static bool active();  // sharded / scattered operands installed on this thread
 };
+// K4 with a fused bf16 addend (fwht3.cu): out = RN(add + RN(rotated in)),
+// B in {64, 128, 256}; false = not handled (caller adds separately)
+bool rows_xform_add(const float* in, int64_t n, int64_t B, const void* add, void* out, cudaStream_t st);
 // SwiGLU epilogue for the next run_gemm_v on this thread (the up projection
 // of a Llama MLP): C = u (bf16), h = silu(g) * u; g, h [M][N] bf16.  h null:
 // the residual epilogue, C = RN_bf16(g + RN_bf16(acc))

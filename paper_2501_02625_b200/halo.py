@@ -540,7 +540,9 @@ class HaloLinearLayer:
         return u, h
 
     def backward(self, ctx: SavedContext, e_y: torch.Tensor, need_grad_w: bool = True,
-                 e_x_dtype=None) -> BackwardResult:
+                 e_x_dtype=None, e_x_add: torch.Tensor = None) -> BackwardResult:
+        """e_x_add (bf16, b x in_features): return e_x_add + E_X instead of
+        E_X (halo_linear_backward_acc: the add fused into the K4 store)."""
         _need_cuda(e_y)
         b = getattr(ctx, "_layer_b", None)
         if b is None:
@@ -552,8 +554,15 @@ class HaloLinearLayer:
         scatter = getattr(self, "_scatter", None) is not None
         g = torch.empty((self.out_features, self.in_features), dtype=self.grad_dtype, device=e_y.device) \
             if need_grad_w and not scatter else None
-        check(lib().halo_linear_backward(self._h, ctx._h, _ptr(e_y), _dt(e_y), _ptr(e_x), _DT[ex_dt], _ptr(g),
-                                         _DT[self.grad_dtype], _stream()))
+        if e_x_add is not None:
+            if e_x_add.dtype != torch.bfloat16 or tuple(e_x_add.shape) != (b, self.in_features) or \
+                    not e_x_add.is_contiguous() or ex_dt != torch.bfloat16:
+                raise ValueError("backward: e_x_add must be a contiguous bf16 (b x in_features) tensor, e_x bf16")
+            check(lib().halo_linear_backward_acc(self._h, ctx._h, _ptr(e_y), _dt(e_y), _ptr(e_x_add), _ptr(e_x),
+                                                 _DT[ex_dt], _ptr(g), _DT[self.grad_dtype], _stream()))
+        else:
+            check(lib().halo_linear_backward(self._h, ctx._h, _ptr(e_y), _dt(e_y), _ptr(e_x), _DT[ex_dt], _ptr(g),
+                                             _DT[self.grad_dtype], _stream()))
         return BackwardResult(e_x, g)
 
     def export_inference_weights(self, path: str | None = None):

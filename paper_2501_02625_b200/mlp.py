@@ -43,6 +43,9 @@ class HaloMLP:
         # forward(x, residual): the add in the down projection's GEMM epilogue
         # (bit-identical; HALO_MLP_RES_EPI=0: a separate bf16 add)
         self.res_epi = os.environ.get("HALO_MLP_RES_EPI", "1") == "1"
+        # dx = ex_gate + ex_up fused into the up projection's K4 store
+        # (halo_linear_backward_acc, bit-identical; HALO_MLP_ACC_DX=0: halo_add)
+        self.acc_dx = os.environ.get("HALO_MLP_ACC_DX", "1") == "1"
         # tests: a dict here collects the step's intermediate tensors
         self.trace = None
         # HQ-FSDP hooks: pre(name, phase) runs before a projection's GEMMs
@@ -110,11 +113,16 @@ class HaloMLP:
         bg = self.gate.backward(self.ctx[0], dg, need_grad_w)
         gg = self._post("gate", bg.grad_w)
         self._pre("up", "bwd")
-        bu = self.up.backward(self.ctx[1], du, need_grad_w)
+        if self.trace is None and self.acc_dx:
+            # dx = ex_gate + ex_up, the add fused into up's K4 store
+            bu = self.up.backward(self.ctx[1], du, need_grad_w, e_x_add=bg.e_x)
+            dx = bu.e_x
+        else:
+            bu = self.up.backward(self.ctx[1], du, need_grad_w)
+            dx = torch.empty_like(bg.e_x)
+            check(lib().halo_add(halo._ptr(bg.e_x), halo._ptr(bu.e_x), halo._ptr(dx), DTYPE_BF16, dx.numel(),
+                                 halo._stream()))
         gu = self._post("up", bu.grad_w)
-        dx = torch.empty_like(bg.e_x)
-        check(lib().halo_add(halo._ptr(bg.e_x), halo._ptr(bu.e_x), halo._ptr(dx), DTYPE_BF16, dx.numel(),
-                             halo._stream()))
         if self.trace is not None:
             self.trace.update(dh=bd.e_x, dg=dg, du=du, ex_gate=bg.e_x, ex_up=bu.e_x)
         return dx, (gg, gu, gd)

@@ -198,6 +198,31 @@ def test_residual_epilogue_bitexact(M, fmt, b):
     assert torch.equal(y, y_ref)
 
 
+@pytest.mark.parametrize("scheme,b", [("halo2_int8_256", 1000), ("halo2_fp8_128", 512), ("halo2_int8_512", 768),
+                                      ("halo1_int8_256", 512)])
+def test_backward_acc_bitexact(M, scheme, b):
+    """halo_linear_backward_acc (e_x = add + E_X, the add fused into the E
+    path's K4 store for HALO-2 blocks <= 256, a separate add otherwise) ==
+    halo_linear_backward then a bf16 add; grad_w unchanged."""
+    halo, _ = M
+    kind, fmt, block = scheme.split("_")
+    sch = getattr(halo, kind)(halo.INT8 if fmt == "int8" else halo.FP8_E4M3, int(block))
+    g = torch.Generator(device="cuda").manual_seed(b)
+    bf = torch.bfloat16
+    w = (torch.randn(1024, 512, generator=g, device="cuda") / 512 ** 0.5).to(bf)
+    x = torch.randn(b, 512, generator=g, device="cuda").to(bf)
+    e = (torch.randn(b, 1024, generator=g, device="cuda") * 1e-2).to(bf)
+    a = torch.randn(b, 512, generator=g, device="cuda").to(bf)
+    lay = halo.HaloLinearLayer(w, sch, out_dtype=bf)
+    ctx = halo.SavedContext()
+    lay.forward(x, ctx)
+    ref = lay.backward(ctx, e)
+    got = lay.backward(ctx, e, e_x_add=a)
+    torch.cuda.synchronize()
+    assert torch.equal(got.e_x, (a.float() + ref.e_x.float()).to(bf))
+    assert torch.equal(got.grad_w, ref.grad_w)
+
+
 def test_block_fused_glue_matches_unfused(M, monkeypatch):
     """block.attention_block with every glue fusion (tee'd first norm, fused
     residual add + norm, one q/k/v split, the residual add in the down
