@@ -118,6 +118,11 @@ up_s.forward_shared_swiglu(cgs, halo.SavedContext(), gs)
 # residual epilogue (halo_linear_forward_residual): ragged token count
 dn_s = halo.HaloLinearLayer((torch.randn(256, 512, device=dev) / 16).to(bf), halo.halo2(halo.INT8, 256), out_dtype=bf)
 dn_s.forward_residual(gs, halo.SavedContext(), torch.randn(300, 256, device=dev).to(bf))
+# dX accumulated into the K4 store (halo_linear_backward_acc), ragged tokens
+cac = halo.SavedContext()
+la = halo.HaloLinearLayer((torch.randn(512, 256, device=dev) / 16).to(bf), halo.halo2(halo.INT8, 256), out_dtype=bf)
+la.forward(torch.randn(300, 256, device=dev).to(bf), cac)
+la.backward(cac, torch.randn(300, 512, device=dev).to(bf) * 1e-2, e_x_add=torch.randn(300, 256, device=dev).to(bf))
 # the block's first norm with the residual-gradient sum (block.py _RMSNormTeeFn)
 xt_ = torch.randn(64, 512, device=dev).to(bf).requires_grad_(True)
 xr_, at_ = block._RMSNormTeeFn.apply(xt_, torch.ones(512, device=dev, requires_grad=True), 1e-5)
